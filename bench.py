@@ -1,0 +1,477 @@
+"""Benchmark of the B200 segmented wheel sieve (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Default workload (N=1) is BASELINE config 2: enumerate every prime below
+1e10 as a sorted uint64 array in HBM plus count / Σ mod 2^64 / ⊕.  Metric:
+primes enumerated per second (whole job).  Under torchrun (N>1) the ranges
+are sharded with no data-path collective (weak scaling: rank r sieves
+[r*1e10, (r+1)*1e10)); one collective combines count/Σ/⊕ at the end.
+
+Other configs (--config): c1 pi(1e9) count (+ per-segment counts), c3
+pi(1e12) count (split across ranks: strong), c4 [1e15, 1e15+1e11) count +
+Σ/⊕, c5 4096 intervals [L, L+2^24) per-interval count + Σ + ⊕.
+
+One JSON line on rank 0.  `value` is device-timed (CUDA events on the
+library's launch stream) with inputs resident and outputs left in HBM;
+`e2e` goes through the same public API with host buffers (pinned), the
+device->host copy of every step's result inside the timed region.
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libwsref.so: the unmodified reference library, threaded) on the
+host cores for the same config/metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEG = 1 << 18
+
+CONFIGS = {
+    "c1": dict(workload="c1: pi(N) count-only, N=1e9, per-segment uint32 counts", L=0,
+               R=10**9 + 1, kind="count", metric="integers sieved/sec", unit="integers/s"),
+    "c2": dict(workload="c2: enumerate all primes < 1e10 into a sorted uint64 array in HBM "
+               "+ count, sum mod 2^64, xor", L=0, R=10**10, kind="enumerate",
+               metric="primes enumerated/sec", unit="primes/s"),
+    "c3": dict(workload="c3: pi(N) count-only, N=1e12, contiguous super-ranges per GPU", L=0,
+               R=10**12 + 1, kind="count", metric="integers sieved/sec", unit="integers/s"),
+    "c4": dict(workload="c4: count + sum/xor of primes in [1e15, 1e15+1e11)", L=10**15,
+               R=10**15 + 10**11, kind="checks", metric="integers sieved/sec",
+               unit="integers/s"),
+    "c5": dict(workload="c5: 4096 intervals [L, L+2^24), L = 2^32 + splitmix64(42) mod "
+               "(2^44-2^32); per-interval count + sum + xor", kind="intervals",
+               metric="integers sieved/sec", unit="integers/s"),
+}
+
+
+# ----------------------------------------------------------------------------
+def splitmix_starts(seed: int, n: int, lo: int, hi: int) -> np.ndarray:
+    out = np.empty(n, np.uint64)
+    x = seed
+    M = (1 << 64) - 1
+    for i in range(n):
+        x = (x + 0x9E3779B97F4A7C15) & M
+        z = x
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        z ^= z >> 31
+        out[i] = lo + z % (hi - lo)
+    return out
+
+
+def small_primes(n: int) -> np.ndarray:
+    """Primes <= n (numpy sieve; used only for the roofline byte model)."""
+    s = np.ones(n + 1, bool)
+    s[:2] = False
+    for i in range(2, int(n**0.5) + 1):
+        if s[i]:
+            s[i * i::i] = False
+    return np.nonzero(s)[0].astype(np.int64)
+
+
+def cop6(x):
+    x = np.maximum(x, 0)
+    return x - x // 2 - x // 3 + x // 6
+
+
+def smem_bytes(L: int, R: int, S: int = SEG) -> float:
+    """SURVEY §8(d) algorithmic shared-memory bytes of one pass over [L, R):
+    4 B x [2W + sum_{17 <= p <= sqrt R} min(hits_p, W)], W = 32-bit words of
+    both classes, hits_p = multiples of p in [max(L, p^2), R) coprime to 6."""
+    lo0 = L // 6 * 6
+    slots = (R - lo0 + 5) // 6
+    W = 2 * ((slots + 31) // 32)
+    P = small_primes(math.isqrt(R - 1))
+    P = P[P >= 17]
+    lo = np.maximum(np.int64(L), P * P)
+    klo = -(-lo // P)
+    khi = (R - 1) // P
+    hits = np.where(khi >= klo, cop6(khi) - cop6(klo - 1), 0)
+    return 4.0 * (2 * W + float(np.minimum(hits, W).sum()))
+
+
+def smem_peak_gbs(sm_count: int, sm_mhz: float) -> float:
+    return sm_count * 128 * sm_mhz * 1e6 / 1e9  # 32 banks x 4 B per clock per SM
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons (NVML) during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable"]}
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def rank_range(cfg, rank, world):
+    """The rank's share of the workload."""
+    import paper_2310_17746_b200 as ws
+    if cfg["kind"] == "enumerate":  # weak: rank r sieves [r*R, (r+1)*R)
+        span = cfg["R"] - cfg["L"]
+        return cfg["L"] + rank * span, cfg["L"] + (rank + 1) * span, "weak"
+    if cfg["kind"] in ("count", "checks"):  # strong: contiguous super-ranges
+        if world == 1:
+            return cfg["L"], cfg["R"], "strong"
+        lo, hi = ws.partition(cfg["L"], cfg["R"], rank, world, SEG)
+        return lo, hi, "strong"
+    return None, None, "strong"
+
+
+def run_ours(args, cfg, world, rank, local):
+    import torch
+
+    import paper_2310_17746_b200 as ws
+    from paper_2310_17746_b200 import dist as wsdist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sv = ws.Sieve(device=local)
+    stream = torch.cuda.ExternalStream(sv.stream, device=torch.device("cuda", local))
+    kind = cfg["kind"]
+    lo, hi, scaling = rank_range(cfg, rank, world)
+
+    # ---- per-config step functions (device-resident outputs) ----------------
+    if kind == "enumerate":
+        cap = ws.prime_count_bound(lo, hi)
+        out_dev = torch.empty(cap, dtype=torch.int64, device=f"cuda:{local}")
+
+        def step():
+            _, n, c = sv.enumerate_range(lo, hi, out=out_dev, fresh_base=True)
+            return c
+        units_local = None  # primes, known after the first step
+    elif kind in ("count", "checks"):
+        nseg = sv.num_segments(lo, hi)
+        ps_dev = torch.zeros(max(1, nseg), dtype=torch.int32, device=f"cuda:{local}")
+
+        def step():
+            return sv.count_range(lo, hi, checks=(kind == "checks"), per_seg=ps_dev,
+                                  fresh_base=True)
+        units_local = hi - lo
+    else:  # intervals, round-robin i -> rank i mod world
+        Ls_all = splitmix_starts(42, 4096, 2**32, 2**44)
+        Ls = Ls_all[rank::world]
+        width = 2**24
+
+        def step():
+            counts, sums, xors = sv.count_intervals(Ls, width, fresh_base=True)
+            return ws.Checks(int(counts.astype(np.uint64).sum()),
+                             int(sums.sum(dtype=np.uint64)),
+                             int(np.bitwise_xor.reduce(xors)) if xors.size else 0, 0)
+        units_local = int(Ls.size) * width
+
+    for _ in range(args.warmup):
+        c = step()
+    if kind == "enumerate":
+        units_local = c.count
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+    torch.cuda.synchronize()
+    sieve_ms, launches = [], 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            c = step()
+            t = sv.timing()
+            sieve_ms.append(t.sieve_ms)
+            launches += t.launches
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    local_ms = ev0.elapsed_time(ev1)
+    tot_ms = local_ms
+    total_units = units_local
+    checks = c
+    if world > 1:
+        tot_ms = wsdist.max_over_ranks(local_ms)
+        total_units = wsdist.sum_over_ranks(units_local)
+        checks = wsdist.combine_checks(c)
+    ms_per_step = tot_ms / args.steps
+    value = total_units / (ms_per_step / 1e3)
+
+    # ---- e2e: same public API, host (pinned) buffers, D2H inside -------------
+    e2e = None
+    if kind == "enumerate":
+        host = torch.empty(cap, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        k_e2e = max(2, min(args.steps, 10))
+        sv.enumerate_range(lo, hi, out=host, fresh_base=True)
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            _, n, ce = sv.enumerate_range(lo, hi, out=host, fresh_base=True)
+        e_ms = (time.perf_counter() - t0) * 1e3 / k_e2e
+        if world > 1:
+            e_ms = wsdist.max_over_ranks(e_ms)
+        assert ce.count == c.count and ce.sum == c.sum and ce.xor == c.xor
+        e2e = {"value": total_units / (e_ms / 1e3), "unit": cfg["unit"],
+               "h2d_bytes_per_step": 16 * world, "d2h_bytes_per_step": int(8 * total_units + 32),
+               "ms_per_step": e_ms, "steps": k_e2e, "timer": "host wall clock per call"}
+    elif kind in ("count", "checks"):
+        k_e2e = max(2, min(args.steps, 10))
+        per = np.zeros(max(1, sv.num_segments(lo, hi)), np.uint32)
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            sv.count_range(lo, hi, checks=(kind == "checks"), per_seg=per, fresh_base=True)
+        e_ms = (time.perf_counter() - t0) * 1e3 / k_e2e
+        if world > 1:
+            e_ms = wsdist.max_over_ranks(e_ms)
+        e2e = {"value": total_units / (e_ms / 1e3), "unit": cfg["unit"],
+               "h2d_bytes_per_step": 16 * world, "d2h_bytes_per_step": int(4 * per.size + 32),
+               "ms_per_step": e_ms, "steps": k_e2e, "timer": "host wall clock per call"}
+    else:
+        k_e2e = max(2, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            step()
+        e_ms = (time.perf_counter() - t0) * 1e3 / k_e2e
+        if world > 1:
+            e_ms = wsdist.max_over_ranks(e_ms)
+        e2e = {"value": total_units / (e_ms / 1e3), "unit": cfg["unit"],
+               "h2d_bytes_per_step": 8 * 4096, "d2h_bytes_per_step": 20 * 4096,
+               "ms_per_step": e_ms, "steps": k_e2e, "timer": "host wall clock per call"}
+
+    if rank != 0:
+        return None
+    peaks, peak_src = load_peaks()
+    props = torch.cuda.get_device_properties(local)
+    avg_sieve_ms = float(np.mean(sieve_ms))
+    clocks = clk.summary()
+    if kind == "enumerate":
+        alg = 8.0 * units_local
+        achieved = alg / (avg_sieve_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "kernel": "sieve_kernel<kEnumerate>",
+                "algorithmic_bytes_per_launch": alg,
+                "avg_launch_ms": avg_sieve_ms,
+                "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs (copy)"}
+    else:
+        roof = None
+    # shared-memory roofline: the sieve phase of every config
+    if kind != "intervals":
+        b_smem = smem_bytes(lo, hi)
+    else:
+        b_smem = sum(smem_bytes(int(L), int(L) + 2**24) for L in Ls[:64]) * (Ls.size / 64)
+    smax = peaks.get("sm_max_mhz", 1965.0)
+    speak = smem_peak_gbs(props.multi_processor_count, smax)
+    sach = b_smem / (avg_sieve_ms / 1e3) / 1e9
+    roof_smem = {"bound": "smem", "achieved": sach, "peak": speak, "unit": "GB/s",
+                 "frac": sach / speak, "algorithmic_bytes_per_launch": b_smem,
+                 "avg_launch_ms": avg_sieve_ms,
+                 "peak_source": f"{props.multi_processor_count} SMs x 128 B/clk x {smax} MHz"}
+    if roof is None:
+        roof = roof_smem
+    line = {
+        "metric": cfg["metric"], "value": value, "unit": cfg["unit"], "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (deterministic ranges; c5 seeded splitmix64)",
+        "config": {"workload": cfg["workload"], "L": lo if world == 1 else cfg.get("L"),
+                   "R": hi if world == 1 else cfg.get("R"), "segment_slots": SEG,
+                   "l2": "outputs/ranges far larger than the 126 MB L2 (c2 writes 3.64 GB per "
+                         "step); no flush", "parallelism": f"dp{world}",
+                   "base_primes": "re-sieved on device every step (WS_FRESH_BASE)"},
+        "result": {"count": checks.count, "sum": checks.sum, "xor": checks.xor,
+                   "largest": checks.largest},
+        "e2e": e2e, "roofline": roof, "roofline_smem": roof_smem,
+        "gpu_launches": launches, "clocks": clocks,
+        "integers_per_s": (hi - lo) * world / (ms_per_step / 1e3) if lo is not None else None,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    sv.close()
+    return line
+
+
+def cpu_baseline(cfg):
+    """The reference library (oracle/_ref) on a bounded sample, all host threads."""
+    try:
+        from oracle.oracle import Reference
+        ref = Reference()
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unavailable": str(e)}
+    T = os.cpu_count() or 1
+    kind = cfg["kind"]
+    if kind == "enumerate":
+        sample = "reference run() with a sum/xor PrimeSink over [0, 1e9] (prefix of c2), best of 3"
+        best = min(ref.run_checks(10**9, T)["wall_ms"] for _ in range(3))
+        val = 50_847_534 / (best / 1e3)
+    elif kind == "count" and cfg["R"] <= 10**9 + 1:
+        sample = "reference run() with a CountSink over [0, 1e9] (the full c1), best of 3"
+        best = min(ref.pi(10**9, T)["wall_ms"] for _ in range(3))
+        val = 1e9 / (best / 1e3)
+    elif kind == "count":
+        sample = "reference run() with a CountSink over [0, 1e10] (prefix of c3), best of 2"
+        best = min(ref.pi(10**10, T)["wall_ms"] for _ in range(2))
+        val = 1e10 / (best / 1e3)
+    elif kind == "checks":
+        sample = "reference composition (SURVEY 3.3) over [1e15, 1e15+1e9) with sum/xor"
+        r = ref.range(10**15, 10**15 + 10**9, T)
+        val = 1e9 / (r["wall_ms"] / 1e3)
+    else:
+        Ls = splitmix_starts(42, 4096, 2**32, 2**44)[:128]
+        sample = "reference composition over the first 128 of the 4096 c5 intervals"
+        _, _, _, ms = ref.intervals(Ls, 2**24, T)
+        val = 128 * 2**24 / (ms / 1e3)
+    return {"value": val, "unit": cfg["unit"], "cores": T, "kind": "reference",
+            "sample": sample}
+
+
+def run_reference(args, cfg, world, rank):
+    """--impl reference: the reference's own CPU implementation, all host threads."""
+    if rank != 0:
+        return None
+    from oracle.oracle import Reference
+    try:
+        ref = Reference()
+    except Exception as e:  # noqa: BLE001
+        return {"impl": "reference", "unavailable": f"reference library not built: {e}"}
+    T = os.cpu_count() or 1
+    kind = cfg["kind"]
+    if kind == "enumerate":
+        sample = "reference run() with a sum/xor PrimeSink over [0, 1e10) (the full c2)"
+
+        def step():
+            r = ref.run_checks(10**10 - 1, T)
+            return r["count"], r["wall_ms"]
+    elif kind == "count":
+        N = min(cfg["R"] - 1, 10**10)
+        sample = f"reference run() with a CountSink over [0, {N}]"
+
+        def step():
+            r = ref.pi(N, T)
+            return N, r["wall_ms"]
+    elif kind == "checks":
+        sample = "reference composition over [1e15, 1e15+1e9) (1% sample of c4)"
+
+        def step():
+            r = ref.range(10**15, 10**15 + 10**9, T)
+            return 10**9, r["wall_ms"]
+    else:
+        Ls = splitmix_starts(42, 4096, 2**32, 2**44)[:128]
+        sample = "reference composition over the first 128 c5 intervals"
+
+        def step():
+            _, _, _, ms = ref.intervals(Ls, 2**24, T)
+            return 128 * 2**24, ms
+    for _ in range(args.warmup):
+        step()
+    units, ms = 0, 0.0
+    for _ in range(args.steps):
+        u, m = step()
+        units += u
+        ms += m
+    value = units / (ms / 1e3)
+    return {"impl": "reference", "metric": cfg["metric"], "value": value, "unit": cfg["unit"],
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "none (CPU)",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "sample": sample},
+            "cpu_baseline": {"value": value, "unit": cfg["unit"], "cores": T,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": cfg["unit"], "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_env()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        line = run_reference(args, cfg, world, rank)
+    else:
+        line = run_ours(args, cfg, world, rank, local)
+    if line is not None and rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

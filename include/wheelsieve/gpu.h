@@ -1,0 +1,151 @@
+/*
+ * wheelsieve GPU C ABI -- the drop-in boundary for the B200 segmented
+ * mod-6 wheel sieve (libwheelsieve_cuda.so).
+ *
+ * The reference (/root/reference/proj) is a C++20 library with no C ABI; its
+ * sieve is reached through these C++ entry points, which this ABI replaces:
+ *
+ *   wheelsieve::run(const SieveConfig&)          engine.hpp:83, engine.cpp:344
+ *       -> ws_count_range / ws_enumerate_range on [0, limit + 1)
+ *   sieve_segment + count_surviving / surviving   segment.hpp:168, segment.cpp:141-162
+ *       -> batched: every segment of a range in one device pass
+ *   [L, R) count / enumerate (SURVEY §3.3 composition; no single reference call)
+ *       -> ws_count_range / ws_enumerate_range / ws_count_intervals
+ *   engine tiling plan_iteration / round_segment_span  engine.cpp:311-342
+ *       -> ws_partition (contiguous per-GPU super-ranges)
+ *   start_offsets (paper Table 1)                 wheel.cpp:96-106  -> ws_start_offsets
+ *   isqrt                                         wheel.cpp:25-33   -> ws_isqrt
+ *
+ * Conventions (mirroring the reference):
+ *   - every value range is half-open [L, R); pi(N) is [0, N + 1);
+ *   - 2 and 3 are added when in range (engine.cpp:268-276); 1 is never prime
+ *     (engine.cpp:244);
+ *   - a "segment" is `segment_slots` wheel slots per residue class (6k+1 and
+ *     6k+5), spanning 6 * segment_slots values; segment i of [L, R) starts at
+ *     floor(L / 6) * 6 + 6 * segment_slots * i and the last one is clipped;
+ *     per-segment counts exclude 2 and 3;
+ *   - sums are mod 2^64; enumeration output is strictly ascending;
+ *   - status codes are 1 + wheelsieve::Errc (errors.hpp:9-23), no exception
+ *     ever crosses this ABI; device/runtime failures map to WS_CUDA etc.
+ *   - one host thread per context (the engine is not reentrant per run,
+ *     SPEC.md:268); a context owns its device buffers and CUDA stream.
+ */
+#ifndef WHEELSIEVE_GPU_H_
+#define WHEELSIEVE_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ws_status {
+  WS_OK = 0,
+  /* 1 + wheelsieve::Errc, errors.hpp:9-23 */
+  WS_NOT_ON_WHEEL = 1,
+  WS_OVERFLOW = 2,
+  WS_EMPTY_RANGE = 3,
+  WS_CAPACITY = 4,
+  WS_DOMAIN = 5,
+  WS_ALIGNMENT = 6,
+  WS_BAD_CONFIG = 7,
+  WS_INCOMPLETE_BASE = 8,
+  WS_ORDERING = 9,
+  WS_IO = 10,
+  WS_BAD_MANIFEST = 11,
+  WS_CHECKSUM_MISMATCH = 12,
+  WS_BEYOND_FRONTIER = 13,
+  /* device side */
+  WS_CUDA = 100,     /* a CUDA runtime call or kernel failed */
+  WS_NO_DEVICE = 101, /* no usable sm_100 device */
+  WS_OUT_OF_MEMORY = 102
+} ws_status;
+
+/* Flags for the range calls. */
+#define WS_WANT_CHECKS 0x1u  /* compute Σ mod 2^64 and ⊕ of the primes (count calls) */
+#define WS_OUT_DEVICE 0x2u   /* output pointers are device pointers on the ctx device */
+#define WS_FRESH_BASE 0x4u   /* re-sieve the base primes even if cached */
+
+typedef struct ws_ctx ws_ctx;
+
+typedef struct ws_opts {
+  uint32_t struct_size;   /* sizeof(ws_opts) */
+  uint32_t segment_slots; /* wheel slots per class per segment: power of two in
+                             [2^12, 2^18]; default 2^18 (64 KiB of flags) */
+  int32_t device;         /* CUDA device ordinal, -1 = current device */
+  uint32_t reserved;
+} ws_opts;
+
+typedef struct ws_checks {
+  uint64_t count;   /* primes in [L, R), 2 and 3 included */
+  uint64_t sum;     /* Σ mod 2^64 (0 unless requested / enumerated) */
+  uint64_t xor_;    /* ⊕ (0 unless requested / enumerated) */
+  uint64_t largest; /* largest prime in range, 0 if none */
+} ws_checks;
+
+typedef struct ws_timing {
+  double base_ms;    /* device time of base-prime generation in the last call (0 if cached) */
+  double sieve_ms;   /* device time of the main sieve kernel(s) of the last call */
+  double total_ms;   /* host wall time of the last call */
+  uint64_t launches; /* kernels launched by the last call */
+  uint64_t segments; /* segments sieved by the main kernel in the last call */
+  uint64_t base_primes; /* sieving primes (>= 5) used by the last call */
+} ws_timing;
+
+void ws_opts_default(ws_opts* opts);
+const char* ws_status_name(ws_status s);
+
+ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out);
+void ws_ctx_destroy(ws_ctx* ctx);
+/* Message of the last failure on this context ("" if none). */
+const char* ws_last_error(const ws_ctx* ctx);
+/* The cudaStream_t the context launches on (for events / interop). */
+void* ws_ctx_stream(ws_ctx* ctx);
+ws_status ws_last_timing(const ws_ctx* ctx, ws_timing* out);
+
+/* Count primes in [L, R).  Replaces run() with a CountSink (engine.hpp:83)
+ * for L = 0, and the SURVEY §3.3 composition otherwise.
+ * per_seg (nullable, host unless WS_OUT_DEVICE): survivor count per segment,
+ * at most per_seg_cap written; *n_seg (nullable) = number of segments. */
+ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws_checks* out,
+                         uint32_t* per_seg, uint64_t per_seg_cap, uint64_t* n_seg);
+
+/* Enumerate the primes of [L, R) in ascending order into out[0 .. *n_out).
+ * Replaces run() with a value sink (MemorySink, sink.hpp:55-66).  Σ and ⊕
+ * are always computed.  If the primes do not fit in cap, nothing is written
+ * past cap, *n_out is the full count and WS_CAPACITY is returned. */
+ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, uint64_t* out,
+                             uint64_t cap, uint64_t* n_out, ws_checks* checks);
+
+/* Count primes in each interval [Ls[i], Ls[i] + width), i < n, each sieved
+ * independently (BASELINE config 5).  counts/sums/xors (nullable sums/xors)
+ * receive per-interval results; Ls and outputs are host arrays unless
+ * WS_OUT_DEVICE. */
+ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64_t width,
+                             uint32_t flags, uint32_t* counts, uint64_t* sums, uint64_t* xors);
+
+/* Upper bound on the number of primes in [L, R) (capacity helper). */
+uint64_t ws_prime_count_bound(uint64_t L, uint64_t R);
+
+/* Multi-GPU partitioner: rank's contiguous share [*lo, *hi) of [L, R), with
+ * interior boundaries on multiples of 6 * segment_slots values counted from
+ * floor(L / 6) * 6 (so every rank's segments coincide with the single-GPU
+ * segmentation); the last rank absorbs the remainder.  Pure function. */
+ws_status ws_partition(uint64_t L, uint64_t R, uint32_t segment_slots, uint32_t rank,
+                       uint32_t world, uint64_t* lo, uint64_t* hi);
+
+/* Paper Table 1 / wheel.cpp:96-106: wheel indices of the first multiples of
+ * p at or beyond segment_start in the 6k+1 and 6k+5 classes. */
+ws_status ws_start_offsets(uint64_t p, uint64_t segment_start, uint64_t* id1, uint64_t* id5);
+
+/* floor(sqrt(n)), exact (wheel.cpp:25-33). */
+uint64_t ws_isqrt(uint64_t n);
+
+/* Library version string. */
+const char* ws_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WHEELSIEVE_GPU_H_ */

@@ -1,0 +1,80 @@
+"""ctypes binding of the C ABI in include/wheelsieve/gpu.h.
+
+The shared library is built in-tree (paper_2310_17746_b200/libwheelsieve_cuda.so,
+by ``__graft_entry__.build()`` / ``make -C paper_2310_17746_b200/csrc``).  There
+is no fallback: if it is missing or cannot be loaded, importing this module
+raises, and every call on a machine without an sm_100 GPU raises
+``Error(Errc.NoDevice)``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libwheelsieve_cuda.so")
+
+# Every symbol include/wheelsieve/gpu.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "ws_opts_default", "ws_status_name", "ws_ctx_create", "ws_ctx_destroy", "ws_last_error",
+    "ws_ctx_stream", "ws_last_timing", "ws_count_range", "ws_enumerate_range",
+    "ws_count_intervals", "ws_prime_count_bound", "ws_partition", "ws_start_offsets",
+    "ws_isqrt", "ws_version",
+)
+
+WS_WANT_CHECKS = 0x1
+WS_OUT_DEVICE = 0x2
+WS_FRESH_BASE = 0x4
+
+u64 = C.c_uint64
+u32 = C.c_uint32
+P64 = C.POINTER(C.c_uint64)
+P32 = C.POINTER(C.c_uint32)
+
+
+class WsOpts(C.Structure):
+    _fields_ = [("struct_size", u32), ("segment_slots", u32), ("device", C.c_int32),
+                ("reserved", u32)]
+
+
+class WsChecks(C.Structure):
+    _fields_ = [("count", u64), ("sum", u64), ("xor_", u64), ("largest", u64)]
+
+
+class WsTiming(C.Structure):
+    _fields_ = [("base_ms", C.c_double), ("sieve_ms", C.c_double), ("total_ms", C.c_double),
+                ("launches", u64), ("segments", u64), ("base_primes", u64)]
+
+
+def _load(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build the CUDA extension first "
+            "(python -c 'import __graft_entry__ as g; g.build()')")
+    lib = C.CDLL(path)
+    vp = C.c_void_p
+    sig = {
+        "ws_opts_default": (None, [C.POINTER(WsOpts)]),
+        "ws_status_name": (C.c_char_p, [C.c_int]),
+        "ws_ctx_create": (C.c_int, [C.POINTER(WsOpts), C.POINTER(vp)]),
+        "ws_ctx_destroy": (None, [vp]),
+        "ws_last_error": (C.c_char_p, [vp]),
+        "ws_ctx_stream": (vp, [vp]),
+        "ws_last_timing": (C.c_int, [vp, C.POINTER(WsTiming)]),
+        "ws_count_range": (C.c_int, [vp, u64, u64, u32, C.POINTER(WsChecks), vp, u64, P64]),
+        "ws_enumerate_range": (C.c_int, [vp, u64, u64, u32, vp, u64, P64, C.POINTER(WsChecks)]),
+        "ws_count_intervals": (C.c_int, [vp, vp, u64, u64, u32, vp, vp, vp]),
+        "ws_prime_count_bound": (u64, [u64, u64]),
+        "ws_partition": (C.c_int, [u64, u64, u32, u32, u32, P64, P64]),
+        "ws_start_offsets": (C.c_int, [u64, u64, P64, P64]),
+        "ws_isqrt": (u64, [u64]),
+        "ws_version": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()

@@ -1,0 +1,621 @@
+// C-ABI host layer of libwheelsieve_cuda.so (declared in include/wheelsieve/gpu.h).
+//
+// Orchestration that the reference does in run_loop (engine.cpp:149-307) and
+// BasePrimeStore::bootstrap (base_store.cpp:34-42) is redone device-first:
+//   1. base primes <= isqrt(R - 1) are sieved on the device (level 0: one
+//      block, dense, primes <= 2^16; level 1: the main sieve kernel itself
+//      enumerating [0, B]); the table is kept resident and only re-sieved
+//      when a call needs a larger bound (the reference's incremental base
+//      store, base_store.cpp:44-76) or WS_FRESH_BASE is set;
+//   2. one launch of the segment kernel covers every segment of every
+//      requested range (no per-iteration barrier, engine.cpp:257-262);
+//   3. only the results cross back: counts, checksums, per-segment counts or
+//      the enumerated values.
+// No exception crosses the ABI; errors become ws_status + ws_last_error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "wheelsieve/gpu.h"
+#include "ws_internal.h"
+
+namespace {
+
+constexpr uint64_t kMaxWheelIndex = (UINT64_MAX - 5) / 6;       // wheel.hpp:33
+constexpr uint64_t kMaxSegmentEnd = 6 * (kMaxWheelIndex + 1);   // wheel.hpp:37
+
+uint64_t isqrt_u64(uint64_t n) {  // wheel.cpp:25-33 semantics (exact)
+  if (n == 0) return 0;
+  uint64_t r = static_cast<uint64_t>(std::sqrt(static_cast<double>(n)));
+  while (r > 0 && r > n / r) --r;
+  while (r + 1 <= n / (r + 1)) ++r;
+  return r;
+}
+
+struct Fail {
+  ws_status code;
+  std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    throw Fail{WS_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e)};
+  if (e != cudaSuccess) throw Fail{WS_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  void reserve(size_t n, const char* what) {
+    if (n <= cap) return;
+    release();
+    ck(cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T)), what);
+    cap = n;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+uint64_t small_primes_upto(uint64_t B) {  // |{5,7,...,31} ∩ [5, B]|
+  static const uint32_t sp[] = {5, 7, 11, 13, 17, 19, 23, 29, 31};
+  uint64_t c = 0;
+  for (uint32_t q : sp) c += q <= B;
+  return c;
+}
+
+}  // namespace
+
+struct ws_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t S = 1u << 18;
+  int sms = 148;
+  int bps = 2;
+  std::string err;
+  ws_timing timing{};
+  cudaEvent_t ev[4] = {};
+
+  // resident base-prime table: every prime in [37, base_B]
+  bool base_valid = false;
+  bool base_built = false;  // the last call (re)built the table
+  uint64_t base_B = 0;
+  uint32_t nprimes = 0;
+  DevBuf<uint32_t> tab_p;
+  DevBuf<unsigned long long> tab_m;
+
+  // scratch
+  DevBuf<wsk::Job> jobs;
+  DevBuf<wsk::JobAcc> acc;
+  DevBuf<unsigned long long> ticket;
+  DevBuf<uint32_t> per_seg;
+  DevBuf<unsigned long long> status;
+  DevBuf<unsigned long long> vals;  // enumeration scratch (base primes / host-bound output)
+  DevBuf<uint32_t> l0_p;
+  DevBuf<unsigned long long> l0_m;
+  DevBuf<uint32_t> l0_n;
+  std::vector<wsk::Job> h_jobs;
+
+  ~ws_ctx() {
+    cudaSetDevice(device);
+    for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n}) b->release();
+    for (auto* b : {&tab_m, &ticket, &status, &vals, &l0_m}) b->release();
+    jobs.release();
+    acc.release();
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+uint64_t prime_count_bound(uint64_t L, uint64_t R) {
+  if (R <= L) return 0;
+  const double y = static_cast<double>(R - L);
+  const uint64_t slots = (R - L) / 3 + 4;  // wheel slots + 2, 3 and rounding
+  double b;
+  // prefix: pi(x) < 1.25506 x / ln x (Rosser-Schoenfeld, x > 1)
+  const double x = static_cast<double>(R);
+  double pref = x < 17 ? 8.0 : 1.25506 * x / std::log(x) + 8;
+  // window: pi(L + y) - pi(L) <= 2 y / ln y (Montgomery-Vaughan, y > 1)
+  double win = y < 17 ? 8.0 : 2.0 * y / std::log(y) + 8;
+  b = std::min(pref, win);
+  const uint64_t bb = static_cast<uint64_t>(b) + 16;
+  return std::min<uint64_t>(bb, slots);
+}
+
+struct Timer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double ms() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+        .count();
+  }
+};
+
+// Geometry of [L, R): K0 = floor(L/6), slots = ceil((R - 6 K0)/6).
+wsk::Job make_job(uint64_t L, uint64_t R, uint32_t S, uint64_t seg_begin) {
+  wsk::Job j{};
+  j.L = L;
+  j.R = R;
+  j.K0 = L / 6;
+  j.nslots = R > L ? (R - 6 * j.K0 + 5) / 6 : 0;
+  j.seg_begin = seg_begin;
+  j.nseg = (j.nslots + S - 1) / S;
+  return j;
+}
+
+void validate_range(uint64_t L, uint64_t R) {
+  if (R > kMaxSegmentEnd)
+    throw Fail{WS_OVERFLOW, "range end " + std::to_string(R) +
+                                " exceeds the sievable 64-bit range (engine.cpp:139)"};
+  (void)L;
+}
+
+// One launch of the segment kernel over ctx->h_jobs.
+void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* out,
+               unsigned long long out_cap, bool timed) {
+  uint64_t nseg = 0;
+  for (const auto& j : c->h_jobs) nseg += j.nseg;
+  const size_t nj = c->h_jobs.size();
+  c->jobs.reserve(nj, "jobs");
+  c->acc.reserve(nj, "acc");
+  c->ticket.reserve(1, "ticket");
+  ck(cudaMemcpyAsync(c->jobs.ptr, c->h_jobs.data(), nj * sizeof(wsk::Job),
+                     cudaMemcpyHostToDevice, c->stream), "upload jobs");
+  ck(cudaMemsetAsync(c->acc.ptr, 0, nj * sizeof(wsk::JobAcc), c->stream), "zero acc");
+  ck(cudaMemsetAsync(c->ticket.ptr, 0, sizeof(unsigned long long), c->stream), "zero ticket");
+  if (mode == wsk::kEnumerate) {
+    c->status.reserve(nseg, "status");
+    ck(cudaMemsetAsync(c->status.ptr, 0, nseg * sizeof(unsigned long long), c->stream),
+       "zero status");
+  }
+  if (nseg == 0) return;
+  wsk::SieveParams p{};
+  p.jobs = c->jobs.ptr;
+  p.njobs = static_cast<uint32_t>(nj);
+  p.nseg_total = nseg;
+  p.S = c->S;
+  p.prime_p = c->tab_p.ptr;
+  p.prime_m = c->tab_m.ptr;
+  p.nprimes = c->nprimes;
+  // warp-cooperative loop for primes below 1024 (>= 256 hits per class per
+  // 2^18-slot segment); one thread per prime above
+  uint32_t nwc = 0;
+  {
+    // primes in [37, 1024): 172 - 11 = 161 entries
+    static const uint32_t kWcCount = 161;
+    nwc = std::min<uint32_t>(kWcCount, c->nprimes);
+  }
+  p.n_wc = nwc;
+  p.ticket = c->ticket.ptr;
+  p.acc = c->acc.ptr;
+  p.per_seg = per_seg_dev;
+  p.status = c->status.ptr;
+  p.out = out;
+  p.out_cap = out_cap;
+  const uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps;
+  const int grid = static_cast<int>(std::min<uint64_t>(nseg, max_grid));
+  if (timed) ck(cudaEventRecord(c->ev[2], c->stream), "event");
+  ck(wsk::launch_sieve(mode, p, grid, c->stream), "sieve launch");
+  if (timed) ck(cudaEventRecord(c->ev[3], c->stream), "event");
+  c->timing.launches += 1;
+  c->timing.segments += nseg;
+}
+
+// Make the resident table cover every prime in [37, B].
+void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
+  c->base_built = false;
+  if (c->base_valid && c->base_B >= B && !fresh) return;
+  c->base_built = true;
+  ck(cudaEventRecord(c->ev[0], c->stream), "event");
+  c->base_valid = false;
+  if (B < wsk::kFirstTablePrime) {
+    c->nprimes = 0;
+    c->base_B = B;
+    c->base_valid = true;
+    ck(cudaEventRecord(c->ev[1], c->stream), "event");
+    return;
+  }
+  if (B > 0xFFFFFFFFull) throw Fail{WS_OVERFLOW, "base bound exceeds 2^32"};
+  // level 0: primes in [37, isqrt(B)] (isqrt(B) < 2^16)
+  const uint64_t B0 = isqrt_u64(B);
+  c->l0_p.reserve(7000, "l0");
+  c->l0_m.reserve(7000, "l0");
+  c->l0_n.reserve(1, "l0");
+  ck(wsk::launch_tiny_primes(static_cast<uint32_t>(B0), c->l0_p.ptr, c->l0_m.ptr, c->l0_n.ptr,
+                             c->stream), "tiny primes");
+  uint32_t n0 = 0;
+  ck(cudaMemcpyAsync(&n0, c->l0_n.ptr, 4, cudaMemcpyDeviceToHost, c->stream), "n0");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  c->timing.launches += 1;
+  // level 1: enumerate [0, B + 1) with the level-0 table
+  const uint64_t cap = prime_count_bound(0, B + 1);
+  c->vals.reserve(cap, "base values");
+  c->tab_p.reserve(cap, "base table");
+  c->tab_m.reserve(cap, "base table");
+  std::swap(c->tab_p, c->l0_p);  // run_sieve reads the table from tab_*
+  std::swap(c->tab_m, c->l0_m);
+  c->nprimes = n0;
+  c->h_jobs.assign(1, make_job(0, B + 1, c->S, 0));
+  run_sieve(c, wsk::kEnumerate, nullptr, c->vals.ptr, cap, false);
+  std::swap(c->tab_p, c->l0_p);
+  std::swap(c->tab_m, c->l0_m);
+  wsk::JobAcc a{};
+  ck(cudaMemcpyAsync(&a, c->acc.ptr, sizeof a, cudaMemcpyDeviceToHost, c->stream), "acc");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  if (a.count > cap) throw Fail{WS_CAPACITY, "base prime bound too small"};
+  const uint64_t skip = small_primes_upto(B);
+  ck(wsk::launch_prepare_table(c->vals.ptr, skip, a.count, c->tab_p.ptr, c->tab_m.ptr,
+                               c->stream), "prepare table");
+  c->timing.launches += 1;
+  c->nprimes = static_cast<uint32_t>(a.count - skip);
+  c->base_B = B;
+  c->base_valid = true;
+  ck(cudaEventRecord(c->ev[1], c->stream), "event");
+}
+
+float event_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0;
+  return ms;
+}
+
+template <class F>
+ws_status guarded(ws_ctx* c, F&& f) {
+  if (!c) return WS_BAD_CONFIG;
+  Timer t;
+  c->err.clear();
+  c->timing = ws_timing{};
+  try {
+    if (cudaSetDevice(c->device) != cudaSuccess) throw Fail{WS_NO_DEVICE, "cudaSetDevice"};
+    f();
+  } catch (const Fail& e) {
+    c->err = e.msg;
+    cudaGetLastError();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    c->err = "host allocation failed";
+    return WS_OUT_OF_MEMORY;
+  } catch (...) {
+    c->err = "unknown failure";
+    return WS_CUDA;
+  }
+  c->timing.total_ms = t.ms();
+  return WS_OK;
+}
+
+void add_prelude(uint64_t L, uint64_t R, ws_checks* o) {  // engine.cpp:268-276
+  for (uint64_t v : {uint64_t{2}, uint64_t{3}})
+    if (v >= L && v < R) {
+      o->count += 1;
+      o->sum += v;
+      o->xor_ ^= v;
+      o->largest = std::max(o->largest, v);
+    }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ws_version(void) { return "wheelsieve-b200 0.1 (sm_100a)"; }
+
+void ws_opts_default(ws_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->struct_size = sizeof(ws_opts);
+  o->segment_slots = 1u << 18;
+  o->device = -1;
+}
+
+const char* ws_status_name(ws_status s) {
+  switch (s) {
+    case WS_OK: return "ok";
+    case WS_NOT_ON_WHEEL: return "NotOnWheel";
+    case WS_OVERFLOW: return "Overflow";
+    case WS_EMPTY_RANGE: return "EmptyRange";
+    case WS_CAPACITY: return "Capacity";
+    case WS_DOMAIN: return "Domain";
+    case WS_ALIGNMENT: return "Alignment";
+    case WS_BAD_CONFIG: return "BadConfig";
+    case WS_INCOMPLETE_BASE: return "IncompleteBase";
+    case WS_ORDERING: return "Ordering";
+    case WS_IO: return "Io";
+    case WS_BAD_MANIFEST: return "BadManifest";
+    case WS_CHECKSUM_MISMATCH: return "ChecksumMismatch";
+    case WS_BEYOND_FRONTIER: return "BeyondFrontier";
+    case WS_CUDA: return "Cuda";
+    case WS_NO_DEVICE: return "NoDevice";
+    case WS_OUT_OF_MEMORY: return "OutOfMemory";
+  }
+  return "unknown";
+}
+
+ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
+  if (!out) return WS_BAD_CONFIG;
+  *out = nullptr;
+  ws_opts o;
+  ws_opts_default(&o);
+  if (opts) {
+    if (opts->struct_size != sizeof(ws_opts)) return WS_BAD_CONFIG;
+    o = *opts;
+  }
+  const uint32_t S = o.segment_slots;
+  if (S < (1u << 12) || S > (1u << 18) || (S & (S - 1))) return WS_BAD_CONFIG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return WS_NO_DEVICE;
+  }
+  int dev = o.device;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) return WS_NO_DEVICE;
+  if (dev >= ndev) return WS_NO_DEVICE;
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return WS_NO_DEVICE;
+  if (prop.major != 10) return WS_NO_DEVICE;  // built for sm_100a only
+  ws_ctx* c = new (std::nothrow) ws_ctx;
+  if (!c) return WS_OUT_OF_MEMORY;
+  c->device = dev;
+  c->S = S;
+  c->sms = prop.multiProcessorCount;
+  if (cudaSetDevice(dev) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      wsk::sieve_configure(&c->bps) != cudaSuccess) {
+    delete c;
+    cudaGetLastError();
+    return WS_CUDA;
+  }
+  for (auto& e : c->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      delete c;
+      return WS_CUDA;
+    }
+  *out = c;
+  return WS_OK;
+}
+
+void ws_ctx_destroy(ws_ctx* ctx) { delete ctx; }
+
+const char* ws_last_error(const ws_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void* ws_ctx_stream(ws_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+ws_status ws_last_timing(const ws_ctx* ctx, ws_timing* out) {
+  if (!ctx || !out) return WS_BAD_CONFIG;
+  *out = ctx->timing;
+  return WS_OK;
+}
+
+uint64_t ws_isqrt(uint64_t n) { return isqrt_u64(n); }
+
+uint64_t ws_prime_count_bound(uint64_t L, uint64_t R) { return prime_count_bound(L, R); }
+
+ws_status ws_start_offsets(uint64_t p, uint64_t start, uint64_t* id1, uint64_t* id5) {
+  // wheel.cpp:96-106 semantics; computed with the k-residue form of Table 1
+  if (!id1 || !id5) return WS_BAD_CONFIG;
+  if (p % 6 != 1 && p % 6 != 5) return WS_DOMAIN;
+  if (start % 6 != 0) return WS_ALIGNMENT;
+  if (start <= p) return WS_DOMAIN;
+  const uint64_t R6 = p / 6;
+  const uint64_t t1 = p % 6 == 1 ? R6 : 5 * R6 + 4;
+  const uint64_t t5 = p % 6 == 1 ? 5 * R6 : R6;
+  const uint64_t k0 = start / 6;
+  const uint64_t r = k0 % p;
+  *id1 = k0 + (t1 >= r ? t1 - r : t1 + p - r);
+  *id5 = k0 + (t5 >= r ? t5 - r : t5 + p - r);
+  return WS_OK;
+}
+
+ws_status ws_partition(uint64_t L, uint64_t R, uint32_t S, uint32_t rank, uint32_t world,
+                       uint64_t* lo, uint64_t* hi) {
+  if (!lo || !hi || world == 0 || rank >= world || S == 0) return WS_BAD_CONFIG;
+  if (R <= L) {
+    *lo = *hi = L;
+    return WS_OK;
+  }
+  if (R > kMaxSegmentEnd) return WS_OVERFLOW;
+  const uint64_t lo0 = L / 6 * 6;
+  const uint64_t nslots = (R - lo0 + 5) / 6;
+  const uint64_t nseg = (nslots + S - 1) / S;
+  auto seg_at = [&](uint64_t r) {  // balanced: floor(r * nseg / world)
+    const unsigned __int128 x = static_cast<unsigned __int128>(r) * nseg / world;
+    return static_cast<uint64_t>(x);
+  };
+  const uint64_t a = seg_at(rank), b = seg_at(rank + 1ull);
+  *lo = rank == 0 ? L : std::min<uint64_t>(R, lo0 + 6ull * S * a);
+  *hi = rank + 1 == world ? R : std::min<uint64_t>(R, lo0 + 6ull * S * b);
+  if (*lo < L) *lo = L;
+  if (*hi < *lo) *hi = *lo;
+  return WS_OK;
+}
+
+ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws_checks* out,
+                         uint32_t* per_seg, uint64_t per_seg_cap, uint64_t* n_seg) {
+  return guarded(ctx, [&] {
+    if (!out) throw Fail{WS_BAD_CONFIG, "null output"};
+    *out = ws_checks{};
+    if (n_seg) *n_seg = 0;
+    if (R <= L) return;
+    validate_range(L, R);
+    const bool fresh = flags & WS_FRESH_BASE;
+    ensure_base(ctx, R >= 2 ? isqrt_u64(R - 1) : 0, fresh);
+    ctx->h_jobs.assign(1, make_job(L, R, ctx->S, 0));
+    const uint64_t nseg = ctx->h_jobs[0].nseg;
+    uint32_t* dps = nullptr;
+    const bool dev_out = flags & WS_OUT_DEVICE;
+    if (per_seg) {
+      if (dev_out) {
+        if (per_seg_cap < nseg) throw Fail{WS_CAPACITY, "per_seg capacity below segment count"};
+        dps = per_seg;
+      } else {
+        ctx->per_seg.reserve(nseg, "per_seg");
+        dps = ctx->per_seg.ptr;
+      }
+    }
+    const int mode = (flags & WS_WANT_CHECKS) ? wsk::kCountChecks : wsk::kCount;
+    run_sieve(ctx, mode, dps, nullptr, 0, true);
+    wsk::JobAcc a{};
+    ck(cudaMemcpyAsync(&a, ctx->acc.ptr, sizeof a, cudaMemcpyDeviceToHost, ctx->stream),
+       "acc");
+    if (per_seg && !dev_out)
+      ck(cudaMemcpyAsync(per_seg, dps, std::min(nseg, per_seg_cap) * sizeof(uint32_t),
+                         cudaMemcpyDeviceToHost, ctx->stream), "per_seg");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ck(cudaGetLastError(), "kernel");
+    out->count = a.count;
+    out->sum = a.sum;
+    out->xor_ = a.xr;
+    out->largest = a.largest;
+    add_prelude(L, R, out);
+    if (n_seg) *n_seg = nseg;
+    ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
+    ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
+    ctx->timing.base_primes = ctx->nprimes + small_primes_upto(ctx->base_B);
+  });
+}
+
+ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, uint64_t* out,
+                             uint64_t cap, uint64_t* n_out, ws_checks* checks) {
+  ws_status st = guarded(ctx, [&] {
+    if (!n_out) throw Fail{WS_BAD_CONFIG, "null n_out"};
+    *n_out = 0;
+    ws_checks chk{};
+    if (checks) *checks = chk;
+    if (R <= L) return;
+    if (!out && cap) throw Fail{WS_BAD_CONFIG, "null output with nonzero capacity"};
+    validate_range(L, R);
+    ensure_base(ctx, R >= 2 ? isqrt_u64(R - 1) : 0, flags & WS_FRESH_BASE);
+    uint64_t pre[2];
+    uint64_t npre = 0;
+    for (uint64_t v : {uint64_t{2}, uint64_t{3}})
+      if (v >= L && v < R) pre[npre++] = v;
+    ctx->h_jobs.assign(1, make_job(L, R, ctx->S, 0));
+    const bool dev_out = flags & WS_OUT_DEVICE;
+    if (dev_out && out && !is_device_ptr(out))
+      throw Fail{WS_BAD_CONFIG, "WS_OUT_DEVICE with a non-device pointer"};
+    unsigned long long* dst;
+    uint64_t dcap;
+    if (dev_out) {
+      dst = reinterpret_cast<unsigned long long*>(out) + std::min(npre, cap);
+      dcap = cap > npre ? cap - npre : 0;
+      if (npre && cap)
+        ck(cudaMemcpyAsync(out, pre, std::min(npre, cap) * 8, cudaMemcpyHostToDevice,
+                           ctx->stream), "prelude");
+    } else {
+      const uint64_t bound = std::min<uint64_t>(prime_count_bound(L, R), cap > npre ? cap - npre : 0);
+      ctx->vals.reserve(bound, "enumeration buffer");
+      dst = ctx->vals.ptr;
+      dcap = bound;
+      for (uint64_t i = 0; i < npre && i < cap; ++i) out[i] = pre[i];
+    }
+    run_sieve(ctx, wsk::kEnumerate, nullptr, dst, dcap, true);
+    wsk::JobAcc a{};
+    ck(cudaMemcpyAsync(&a, ctx->acc.ptr, sizeof a, cudaMemcpyDeviceToHost, ctx->stream),
+       "acc");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ck(cudaGetLastError(), "kernel");
+    if (!dev_out) {
+      const uint64_t n = std::min<uint64_t>(a.count, dcap);
+      if (n)
+        ck(cudaMemcpyAsync(out + npre, dst, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+      ck(cudaStreamSynchronize(ctx->stream), "sync");
+    }
+    chk.count = a.count;
+    chk.sum = a.sum;
+    chk.xor_ = a.xr;
+    chk.largest = a.largest;
+    add_prelude(L, R, &chk);
+    *n_out = chk.count;
+    if (checks) *checks = chk;
+    ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
+    ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
+    ctx->timing.base_primes = ctx->nprimes + small_primes_upto(ctx->base_B);
+    if (chk.count > cap) throw Fail{WS_CAPACITY, "output capacity below the prime count"};
+  });
+  return st;
+}
+
+ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64_t width,
+                             uint32_t flags, uint32_t* counts, uint64_t* sums, uint64_t* xors) {
+  return guarded(ctx, [&] {
+    if (n == 0) return;
+    if (!Ls || !counts) throw Fail{WS_BAD_CONFIG, "null interval arrays"};
+    if (width == 0) throw Fail{WS_EMPTY_RANGE, "zero-width intervals"};
+    const bool dev_out = flags & WS_OUT_DEVICE;
+    std::vector<uint64_t> hL;
+    const uint64_t* L = Ls;
+    if (dev_out) {
+      hL.resize(n);
+      ck(cudaMemcpy(hL.data(), Ls, n * 8, cudaMemcpyDeviceToHost), "intervals in");
+      L = hL.data();
+    }
+    uint64_t maxR = 0, seg = 0;
+    ctx->h_jobs.clear();
+    ctx->h_jobs.reserve(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      if (L[i] > kMaxSegmentEnd - width) throw Fail{WS_OVERFLOW, "interval end overflows"};
+      const uint64_t R = L[i] + width;
+      maxR = std::max(maxR, R);
+      ctx->h_jobs.push_back(make_job(L[i], R, ctx->S, seg));
+      seg += ctx->h_jobs.back().nseg;
+    }
+    ensure_base(ctx, maxR >= 2 ? isqrt_u64(maxR - 1) : 0, flags & WS_FRESH_BASE);
+    // ensure_base may have used h_jobs for the base sieve: rebuild
+    ctx->h_jobs.clear();
+    seg = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      ctx->h_jobs.push_back(make_job(L[i], L[i] + width, ctx->S, seg));
+      seg += ctx->h_jobs.back().nseg;
+    }
+    const bool checks = sums || xors;
+    run_sieve(ctx, checks ? wsk::kCountChecks : wsk::kCount, nullptr, nullptr, 0, true);
+    std::vector<wsk::JobAcc> acc(n);
+    ck(cudaMemcpyAsync(acc.data(), ctx->acc.ptr, n * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost,
+                       ctx->stream), "acc");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ck(cudaGetLastError(), "kernel");
+    std::vector<uint32_t> hc(n);
+    std::vector<uint64_t> hs(n), hx(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      ws_checks o{acc[i].count, acc[i].sum, acc[i].xr, acc[i].largest};
+      add_prelude(L[i], L[i] + width, &o);
+      hc[i] = static_cast<uint32_t>(o.count);
+      hs[i] = o.sum;
+      hx[i] = o.xor_;
+    }
+    if (dev_out) {
+      ck(cudaMemcpy(counts, hc.data(), n * 4, cudaMemcpyHostToDevice), "counts");
+      if (sums) ck(cudaMemcpy(sums, hs.data(), n * 8, cudaMemcpyHostToDevice), "sums");
+      if (xors) ck(cudaMemcpy(xors, hx.data(), n * 8, cudaMemcpyHostToDevice), "xors");
+    } else {
+      std::memcpy(counts, hc.data(), n * 4);
+      if (sums) std::memcpy(sums, hs.data(), n * 8);
+      if (xors) std::memcpy(xors, hx.data(), n * 8);
+    }
+    ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
+    ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
+    ctx->timing.base_primes = ctx->nprimes + small_primes_upto(ctx->base_B);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Internal interface between the C-ABI host layer (ws_abi.cu) and the
+// sm_100a kernels (ws_sieve.cu).  Plain structs, no torch types.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wsk {
+
+constexpr int kThreads = 512;            // threads per sieve block
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kFirstTablePrime = 37; // primes 5..31 are stamped from pattern tables
+
+// One half-open value range [L, R) sieved as nseg segments of S wheel slots
+// per residue class starting at wheel index K0 = floor(L / 6)
+// (SURVEY §3.3 geometry: segment i starts at 6*K0 + 6*S*i).
+struct Job {
+  uint64_t L, R;
+  uint64_t K0;        // first wheel index
+  uint64_t nslots;    // wheel slots per class over the whole range
+  uint64_t seg_begin; // index of the job's first segment in the launch
+  uint64_t nseg;
+};
+
+// Per-job results, combined with 64-bit atomics (sum wraps mod 2^64).
+struct JobAcc {
+  unsigned long long count, sum, xr, largest;
+};
+
+enum Mode : int { kCount = 0, kCountChecks = 1, kEnumerate = 2 };
+
+struct SieveParams {
+  const Job* jobs;
+  uint32_t njobs;
+  uint64_t nseg_total;
+  uint32_t S;                        // wheel slots per class per segment (power of two)
+  const uint32_t* prime_p;           // sieving primes >= 37, ascending
+  const unsigned long long* prime_m; // floor((2^64-1)/p), Barrett reciprocal
+  uint32_t nprimes;
+  uint32_t n_wc;                     // primes [0, n_wc) use the warp-cooperative loop
+  unsigned long long* ticket;        // dynamic segment counter (zeroed per launch)
+  JobAcc* acc;                       // njobs accumulators (zeroed per launch)
+  uint32_t* per_seg;                 // nullable, nseg_total counts
+  unsigned long long* status;        // enumeration look-back words (zeroed)
+  unsigned long long* out;           // enumeration output (after 2 and 3)
+  unsigned long long out_cap;
+};
+
+size_t sieve_smem_bytes(uint32_t S);
+cudaError_t sieve_configure(int* blocks_per_sm);
+cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st);
+
+// Level-0 base primes: all primes in [37, n] (n <= 65536 + 1) in one block.
+cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
+                               uint32_t* out_count, cudaStream_t st);
+// Table preparation: vals[i] (uint64 primes, ascending) -> p / Barrett m for
+// i in [skip, n).
+cudaError_t launch_prepare_table(const unsigned long long* vals, uint64_t skip, uint64_t n,
+                                 uint32_t* out_p, unsigned long long* out_m, cudaStream_t st);
+
+}  // namespace wsk

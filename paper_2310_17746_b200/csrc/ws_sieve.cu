@@ -1,0 +1,604 @@
+// sm_100a kernels of the B200 segmented mod-6 wheel sieve.
+//
+// Reference hot path (CPU, scalar): sieve_segment (segment.cpp:164-188) ->
+// FlagArray::clear_stride (segment.cpp:49-69) per base prime and residue
+// class, then count_surviving / for_each_surviving (segment.cpp:141-162,
+// segment.hpp:123-146).  Here one thread block owns one segment at a time:
+//
+//   shared memory:  two uint32 bitmaps (6k+1 and 6k+5 classes), S/32 words each,
+//                   bit k of class c <-> value 6*(ks + k) + c (LSB-first, the
+//                   reference's bit layout, segment.hpp:46-50), stored with an
+//                   XOR row swizzle (word w at w ^ ((w >> 5) & 31)) so strided
+//                   clears by primes near multiples of 32 words do not pile
+//                   onto one bank.
+//   stamp:          primes 5..31 are never looped: their combined periodic
+//                   patterns (groups 5*7*11*13, 17*19*23, 29*31) live in
+//                   shared tables and each word is initialised by three
+//                   funnel-shifted table reads ANDed with the [L, R) trim mask.
+//   medium primes:  37 <= p < wc_limit: warp-cooperative strided clear (lane l
+//                   takes hits rel + l*p, rel + (l+32)*p, ...).
+//   other primes:   one thread per prime.
+//   offsets:        the first hit of p in each class is recomputed per
+//                   (prime, segment) from ks mod p with a 64-bit Barrett
+//                   reduction -- no 64-bit divide, no carried state, so
+//                   segments can be claimed dynamically (ticket counter),
+//                   which the ordered enumeration look-back relies on.  The
+//                   reference's activation rule (first hit at p*p,
+//                   segment.cpp:178-183) is applied when p*p lies ahead.
+//   finish:         __popc + warp/block reductions (count), optional
+//                   sum/xor checksums, or ordered enumeration: per-warp
+//                   prefix sums + a decoupled look-back across segments for
+//                   the global output offset, then uint64 stores.
+#include <cstdint>
+
+#include "ws_internal.h"
+
+namespace wsk {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Wheel helpers.  For a prime p coprime to 6, p = 6R + r, its multiples in
+// class c sit at wheel indices k == t_c (mod p):
+//   r == 1:  t1 = R,       t5 = 5R
+//   r == 5:  t1 = 5R + 4,  t5 = R
+// (the k-residue form of paper Table 1 / kStartIncrements, wheel.cpp:77-82).
+__host__ __device__ constexpr uint32_t target1(uint32_t p) {
+  return p % 6 == 1 ? p / 6 : 5 * (p / 6) + 4;
+}
+__host__ __device__ constexpr uint32_t target5(uint32_t p) {
+  return p % 6 == 1 ? 5 * (p / 6) : p / 6;
+}
+
+// x mod p for any 64-bit x, m = floor((2^64 - 1) / p).  q underestimates
+// x / p by at most 2, so two conditional subtractions finish it.
+__device__ __forceinline__ uint32_t mod_barrett(uint64_t x, uint32_t p, uint64_t m) {
+  const uint64_t q = __umul64hi(x, m);
+  uint64_t r = x - q * p;
+  if (r >= p) r -= p;
+  if (r >= p) r -= p;
+  return static_cast<uint32_t>(r);
+}
+
+__device__ __forceinline__ uint32_t swz(uint32_t w) { return w ^ ((w >> 5) & 31u); }
+
+__device__ __forceinline__ void clear_bit(uint32_t* bm, uint32_t h) {
+  atomicAnd(bm + swz(h >> 5), ~(1u << (h & 31u)));
+}
+
+// bits [a, b) of a 32-bit word, a and b clamped to [0, 32]
+__device__ __forceinline__ uint32_t range_mask(int64_t a, int64_t b) {
+  a = a < 0 ? 0 : (a > 32 ? 32 : a);
+  b = b < 0 ? 0 : (b > 32 ? 32 : b);
+  if (b <= a) return 0u;
+  const uint32_t hi = b == 32 ? kFull : ((1u << b) - 1u);
+  const uint32_t lo = a == 32 ? kFull : ((1u << a) - 1u);
+  return hi & ~lo;
+}
+
+// ---------------------------------------------------------------------------
+// Small-prime pattern tables.  Group g has modulus Q_g; table word i of class
+// c holds bits for wheel indices 32i .. 32i+31 (mod Q_g), bit set when the
+// index is NOT a multiple-position of any prime of the group.  Stored
+// wrap-extended so a funnel shift at any offset < Q_g reads 32 valid bits.
+// group 0: 5*7*11*13 = 5005, group 1: 17*19*23 = 7429, group 2: 29*31 = 899
+__host__ __device__ constexpr uint32_t group_prime(int g, int j) {
+  return g == 0 ? (j == 0 ? 5 : j == 1 ? 7 : j == 2 ? 11 : 13)
+       : g == 1 ? (j == 0 ? 17 : j == 1 ? 19 : 23)
+                : (j == 0 ? 29 : 31);
+}
+__host__ __device__ constexpr int group_size(int g) { return g == 0 ? 4 : g == 1 ? 3 : 2; }
+constexpr uint32_t tab_words(uint32_t Q) { return (Q + 31) / 32 + 2; }
+constexpr uint32_t kTabW0 = tab_words(5005), kTabW1 = tab_words(7429), kTabW2 = tab_words(899);
+constexpr uint32_t kTabPerClass = kTabW0 + kTabW1 + kTabW2;
+constexpr uint32_t kTabWords = 2 * kTabPerClass;
+constexpr uint32_t kTabOff1 = kTabW0, kTabOff2 = kTabW0 + kTabW1;
+
+__device__ void build_tables(uint32_t* tab) {
+  for (uint32_t idx = threadIdx.x; idx < kTabWords; idx += blockDim.x) {
+    const uint32_t cls = idx / kTabPerClass;  // 0 -> 6k+1, 1 -> 6k+5
+    const uint32_t rem = idx % kTabPerClass;
+    const int g = rem < kTabOff1 ? 0 : (rem < kTabOff2 ? 1 : 2);
+    const uint32_t i = rem - (g == 0 ? 0u : g == 1 ? kTabOff1 : kTabOff2);
+    uint32_t word = 0;
+    for (uint32_t b = 0; b < 32; ++b) {
+      const uint32_t pos = 32 * i + b;
+      bool keep = true;
+      for (int j = 0; j < group_size(g); ++j) {
+        const uint32_t q = group_prime(g, j);
+        const uint32_t t = cls ? target5(q) : target1(q);
+        keep = keep && (pos % q != t);
+      }
+      word |= static_cast<uint32_t>(keep) << b;
+    }
+    tab[idx] = word;
+  }
+}
+
+__device__ __forceinline__ uint32_t tab_read(const uint32_t* t, uint32_t off) {
+  const uint32_t i = off >> 5;
+  return __funnelshift_r(t[i], t[i + 1], off & 31u);
+}
+
+// ---------------------------------------------------------------------------
+struct SegInfo {
+  uint64_t s;      // global segment index (>= nseg_total: done)
+  uint32_t job;
+  uint64_t ks;     // absolute wheel index of slot 0
+  uint32_t len;    // slots in this segment
+  uint32_t lo1, hi1, lo5, hi5;  // valid slot bounds per class
+  uint32_t nwords; // words per class actually used (ceil(len / 32), rounded to 32)
+};
+
+__device__ __forceinline__ uint32_t first_valid(uint64_t ks, uint32_t c, uint64_t L) {
+  const uint64_t v0 = 6 * ks + c;
+  return v0 >= L ? 0u : static_cast<uint32_t>((L - v0 + 5) / 6);
+}
+__device__ __forceinline__ uint32_t end_valid(uint64_t ks, uint32_t c, uint64_t R, uint32_t len) {
+  const uint64_t v0 = 6 * ks + c;
+  if (v0 >= R) return 0u;
+  const uint64_t n = (R - v0 + 5) / 6;
+  return n < len ? static_cast<uint32_t>(n) : len;
+}
+
+__device__ void fetch_segment(const SieveParams& P, SegInfo& si) {
+  const unsigned long long s = atomicAdd(P.ticket, 1ull);
+  si.s = s;
+  if (s >= P.nseg_total) return;
+  uint32_t lo = 0, hi = P.njobs;  // last job with seg_begin <= s
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (P.jobs[mid].seg_begin <= s) lo = mid; else hi = mid;
+  }
+  const Job& J = P.jobs[lo];
+  si.job = lo;
+  const uint64_t local = s - J.seg_begin;
+  si.ks = J.K0 + local * P.S;
+  const uint64_t rem = J.nslots - local * P.S;
+  si.len = rem < P.S ? static_cast<uint32_t>(rem) : P.S;
+  si.lo1 = first_valid(si.ks, 1, J.L);
+  if (si.ks == 0 && si.lo1 < 1) si.lo1 = 1;  // value 1 is not prime (engine.cpp:244)
+  si.lo5 = first_valid(si.ks, 5, J.L);
+  si.hi1 = end_valid(si.ks, 1, J.R, si.len);
+  si.hi5 = end_valid(si.ks, 5, J.R, si.len);
+  si.nwords = ((si.len + 1023u) / 1024u) * 32u;
+}
+
+// Phase 1: stamp primes 5..31 and the [L, R) trim into every word.
+__device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* tab, uint32_t* bm1,
+                                           uint32_t* bm5) {
+  const uint32_t o0 = static_cast<uint32_t>(si.ks % 5005u);
+  const uint32_t o1 = static_cast<uint32_t>(si.ks % 7429u);
+  const uint32_t o2 = static_cast<uint32_t>(si.ks % 899u);
+  const uint32_t* t1 = tab;
+  const uint32_t* t5 = tab + kTabPerClass;
+  for (uint32_t w = threadIdx.x; w < si.nwords; w += kThreads) {
+    const uint32_t a0 = (o0 + 32 * w) % 5005u;
+    const uint32_t a1 = (o1 + 32 * w) % 7429u;
+    const uint32_t a2 = (o2 + 32 * w) % 899u;
+    uint32_t m1 = tab_read(t1, a0) & tab_read(t1 + kTabOff1, a1) & tab_read(t1 + kTabOff2, a2);
+    uint32_t m5 = tab_read(t5, a0) & tab_read(t5 + kTabOff1, a1) & tab_read(t5 + kTabOff2, a2);
+    if (w == 0 && si.ks < 6) {
+      // the small primes themselves survive: 7, 13, 19, 31 at class-1
+      // indices 1, 2, 3, 5 and 5, 11, 17, 23, 29 at class-5 indices 0..4
+      m1 |= 0x2Eu >> si.ks;
+      m5 |= 0x1Fu >> si.ks;
+    }
+    const int64_t base = 32 * static_cast<int64_t>(w);
+    m1 &= range_mask(static_cast<int64_t>(si.lo1) - base, static_cast<int64_t>(si.hi1) - base);
+    m5 &= range_mask(static_cast<int64_t>(si.lo5) - base, static_cast<int64_t>(si.hi5) - base);
+    bm1[swz(w)] = m1;
+    bm5[swz(w)] = m5;
+  }
+}
+
+// First hits (segment-relative) of prime p in both classes, or false when
+// p is not yet active in this segment (p*p beyond its end; since primes
+// ascend, no later prime is active either).
+__device__ __forceinline__ bool prime_offsets(uint32_t p, uint64_t m, uint64_t ks, uint32_t len,
+                                              uint32_t& rel1, uint32_t& rel5) {
+  const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;  // p*p = 6*ksq + 1
+  if (ksq >= ks + len) return false;
+  const uint32_t t1 = target1(p), t5 = target5(p);
+  if (ksq >= ks) {
+    // activation segment: class 1 starts exactly at p*p, class 5 at the
+    // first multiple above it (anchor p*(p-1), segment.cpp:182)
+    rel1 = static_cast<uint32_t>(ksq - ks);
+    rel5 = rel1 + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
+  } else {
+    const uint32_t r = mod_barrett(ks, p, m);
+    rel1 = t1 >= r ? t1 - r : t1 + p - r;
+    rel5 = t5 >= r ? t5 - r : t5 + p - r;
+  }
+  return true;
+}
+
+// Phase 2: medium and large primes.
+__device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo& si,
+                                             uint32_t* bm1, uint32_t* bm5) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t len = si.len;
+  const uint64_t ks = si.ks;
+  // warp-cooperative: all lanes of a warp take one prime
+  for (uint32_t i = warp; i < P.n_wc; i += kWarps) {
+    const uint32_t p = P.prime_p[i];
+    uint32_t rel1, rel5;
+    if (!prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5)) break;
+    const uint32_t step = 32 * p;
+#pragma unroll 4
+    for (uint32_t h = rel1 + lane * p; h < len; h += step) clear_bit(bm1, h);
+#pragma unroll 4
+    for (uint32_t h = rel5 + lane * p; h < len; h += step) clear_bit(bm5, h);
+  }
+  // one thread per prime
+  for (uint32_t i = P.n_wc + threadIdx.x; i < P.nprimes; i += kThreads) {
+    const uint32_t p = P.prime_p[i];
+    uint32_t rel1, rel5;
+    if (!prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5)) break;
+    for (uint32_t h = rel1; h < len; h += p) clear_bit(bm1, h);
+    for (uint32_t h = rel5; h < len; h += p) clear_bit(bm5, h);
+  }
+}
+
+__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_xor64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v ^= __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_max64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long u = __shfl_xor_sync(kFull, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+
+// interleave two 32-bit masks: bit 2j <- a_j (class 1), bit 2j+1 <- b_j (class 5)
+__device__ __forceinline__ unsigned long long interleave(uint32_t a, uint32_t b) {
+  auto spread = [](unsigned long long x) {
+    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+  };
+  return spread(a) | (spread(b) << 1);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+// Decoupled look-back (warp 0): exclusive prefix of survivor counts over all
+// segments before s.  Segments are claimed in ticket order, so every
+// predecessor is owned by a running block and the wait terminates.
+__device__ unsigned long long lookback(unsigned long long* status, uint64_t s,
+                                       unsigned long long total) {
+  const uint32_t lane = threadIdx.x & 31u;
+  if (s == 0) {
+    if (lane == 0) st_release(status, kIncl | total);
+    return 0;
+  }
+  if (lane == 0) st_release(status + s, kAgg | total);
+  unsigned long long prefix = 0;
+  int64_t j = static_cast<int64_t>(s) - 1;
+  for (;;) {
+    const int64_t idx = j - static_cast<int64_t>(lane);
+    unsigned long long v = kIncl;  // before segment 0: inclusive prefix 0
+    if (idx >= 0) {
+      do {
+        v = ld_acquire(status + idx);
+      } while ((v >> 62) == 0);
+    }
+    const unsigned incl = __ballot_sync(kFull, (v >> 62) == 2);
+    if (incl) {
+      const int k = __ffs(incl) - 1;  // nearest inclusive predecessor
+      const unsigned long long mine = lane <= static_cast<uint32_t>(k) ? (v & kValMask) : 0ull;
+      prefix += warp_sum64(mine);
+      break;
+    }
+    prefix += warp_sum64(v & kValMask);
+    j -= 32;
+  }
+  if (lane == 0) st_release(status + s, kIncl | (prefix + total));
+  return prefix;
+}
+
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* bm1 = smem;
+  uint32_t* bm5 = smem + P.S / 32;
+  uint32_t* tab = smem + 2 * (P.S / 32);
+  __shared__ SegInfo si;
+  __shared__ unsigned long long red_a[kWarps], red_b[kWarps], red_c[kWarps];
+  __shared__ uint32_t red_n[kWarps];
+  __shared__ unsigned long long seg_base;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+
+  build_tables(tab);
+  for (;;) {
+    __syncthreads();  // bitmap / si reuse guard
+    if (threadIdx.x == 0) fetch_segment(P, si);
+    __syncthreads();
+    if (si.s >= P.nseg_total) break;
+    init_words(si, tab, bm1, bm5);
+    __syncthreads();
+    sieve_primes(P, si, bm1, bm5);
+    __syncthreads();
+
+    const uint64_t vbase = 6 * si.ks;
+    if (MODE != kEnumerate) {
+      uint32_t cnt = 0;
+      unsigned long long lg = 0, sum = 0, xr = 0;
+      for (uint32_t wp = threadIdx.x; wp < si.nwords; wp += kThreads) {
+        const uint32_t m1 = bm1[wp], m5 = bm5[wp];
+        cnt += __popc(m1) + __popc(m5);
+        if (m1 | m5) {
+          const uint32_t w = swz(wp);  // logical word of this physical slot
+          const unsigned long long wb = vbase + 192ull * w;
+          const unsigned long long v1 = m1 ? wb + 6ull * (31 - __clz(m1)) + 1 : 0;
+          const unsigned long long v5 = m5 ? wb + 6ull * (31 - __clz(m5)) + 5 : 0;
+          lg = max(lg, max(v1, v5));
+          if (MODE == kCountChecks) {
+            for (uint32_t x = m1; x; x &= x - 1) {
+              const unsigned long long v = wb + 6ull * (__ffs(x) - 1) + 1;
+              sum += v;
+              xr ^= v;
+            }
+            for (uint32_t x = m5; x; x &= x - 1) {
+              const unsigned long long v = wb + 6ull * (__ffs(x) - 1) + 5;
+              sum += v;
+              xr ^= v;
+            }
+          }
+        }
+      }
+      cnt = __reduce_add_sync(kFull, cnt);
+      lg = warp_max64(lg);
+      if (MODE == kCountChecks) {
+        sum = warp_sum64(sum);
+        xr = warp_xor64(xr);
+      }
+      if (lane == 0) {
+        red_n[warp] = cnt;
+        red_a[warp] = lg;
+        red_b[warp] = sum;
+        red_c[warp] = xr;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t c = lane < kWarps ? red_n[lane] : 0u;
+        unsigned long long l = lane < kWarps ? red_a[lane] : 0ull;
+        unsigned long long su = lane < kWarps ? red_b[lane] : 0ull;
+        unsigned long long x = lane < kWarps ? red_c[lane] : 0ull;
+        c = __reduce_add_sync(kFull, c);
+        l = warp_max64(l);
+        if (MODE == kCountChecks) {
+          su = warp_sum64(su);
+          x = warp_xor64(x);
+        }
+        if (lane == 0) {
+          JobAcc& A = P.acc[si.job];
+          if (P.per_seg) P.per_seg[si.s] = c;
+          if (c) {
+            atomicAdd(&A.count, static_cast<unsigned long long>(c));
+            atomicMax(&A.largest, l);
+            if (MODE == kCountChecks) {
+              atomicAdd(&A.sum, su);
+              atomicXor(&A.xr, x);
+            }
+          }
+        }
+      }
+    } else {
+      // ---- ordered enumeration ----
+      // warp `warp` owns logical words [warp*wpw, (warp+1)*wpw)
+      const uint32_t wpw = si.nwords / kWarps;  // nwords is a multiple of 32*kWarps? see below
+      const uint32_t w_begin = warp * wpw;
+      uint32_t cnt = 0;
+      for (uint32_t w = w_begin + lane; w < w_begin + wpw; w += 32)
+        cnt += __popc(bm1[swz(w)]) + __popc(bm5[swz(w)]);
+      // words beyond kWarps * wpw (remainder) belong to the last warp
+      const uint32_t tail_begin = kWarps * wpw;
+      if (warp == kWarps - 1)
+        for (uint32_t w = tail_begin + lane; w < si.nwords; w += 32)
+          cnt += __popc(bm1[swz(w)]) + __popc(bm5[swz(w)]);
+      cnt = __reduce_add_sync(kFull, cnt);
+      if (lane == 0) red_n[warp] = cnt;
+      __syncthreads();
+      if (warp == 0) {
+        // exclusive scan over warps
+        uint32_t c = lane < kWarps ? red_n[lane] : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t u = __shfl_up_sync(kFull, incl, o);
+          if (lane >= static_cast<uint32_t>(o)) incl += u;
+        }
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        if (lane < kWarps) red_n[lane] = incl - c;
+        const unsigned long long base = lookback(P.status, si.s, total);
+        if (lane == 0) {
+          seg_base = base;
+          if (P.per_seg) P.per_seg[si.s] = total;
+          if (total) atomicAdd(&P.acc[si.job].count, static_cast<unsigned long long>(total));
+        }
+      }
+      __syncthreads();
+      unsigned long long pos = seg_base + red_n[warp];
+      unsigned long long sum = 0, xr = 0, lg = 0;
+      auto emit_rounds = [&](uint32_t wb, uint32_t we) {
+        for (uint32_t w0 = wb; w0 < we; w0 += 32) {
+          const uint32_t w = w0 + lane;
+          unsigned long long M = 0;
+          if (w < we) M = interleave(bm1[swz(w)], bm5[swz(w)]);
+          const uint32_t c = __popcll(M);
+          uint32_t incl = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(kFull, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += u;
+          }
+          const uint32_t rtotal = __shfl_sync(kFull, incl, 31);
+          unsigned long long o = pos + (incl - c);
+          const unsigned long long wbv = vbase + 192ull * w;
+          for (; M; M &= M - 1) {
+            const uint32_t b = __ffsll(static_cast<long long>(M)) - 1;
+            const unsigned long long v = wbv + 3ull * b + 1 + (b & 1u);
+            if (o < P.out_cap) P.out[o] = v;
+            ++o;
+            sum += v;
+            xr ^= v;
+            lg = v;
+          }
+          pos += rtotal;
+        }
+      };
+      emit_rounds(w_begin, w_begin + wpw);
+      if (warp == kWarps - 1) emit_rounds(tail_begin, si.nwords);
+      sum = warp_sum64(sum);
+      xr = warp_xor64(xr);
+      lg = warp_max64(lg);
+      if (lane == 0) {
+        red_a[warp] = sum;
+        red_b[warp] = xr;
+        red_c[warp] = lg;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        unsigned long long su = lane < kWarps ? red_a[lane] : 0ull;
+        unsigned long long x = lane < kWarps ? red_b[lane] : 0ull;
+        unsigned long long l = lane < kWarps ? red_c[lane] : 0ull;
+        su = warp_sum64(su);
+        x = warp_xor64(x);
+        l = warp_max64(l);
+        if (lane == 0) {
+          JobAcc& A = P.acc[si.job];
+          atomicAdd(&A.sum, su);
+          atomicXor(&A.xr, x);
+          if (l) atomicMax(&A.largest, l);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Level-0 base primes: a dense sieve of [0, n] (n <= 65537) in one block,
+// writing the primes >= 37 in ascending order with their Barrett constants.
+__global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t* out_p,
+                                                           unsigned long long* out_m,
+                                                           uint32_t* out_count) {
+  __shared__ uint32_t comp[(65536 + 64) / 32 + 1];
+  __shared__ uint32_t scan[1024];
+  const uint32_t words = n / 32 + 1;
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) comp[i] = 0;
+  __syncthreads();
+  for (uint32_t i = 2; i * i <= n; ++i) {
+    const bool is_prime = !((comp[i >> 5] >> (i & 31)) & 1u);
+    __syncthreads();
+    if (is_prime)
+      for (uint32_t j = i * i + threadIdx.x * i; j <= n; j += blockDim.x * i)
+        atomicOr(&comp[j >> 5], 1u << (j & 31));
+    __syncthreads();
+  }
+  // ordered compaction: thread t owns numbers [t*chunk, (t+1)*chunk)
+  const uint32_t chunk = (n + 1 + blockDim.x - 1) / blockDim.x;
+  const uint32_t a = threadIdx.x * chunk;
+  uint32_t c = 0;
+  for (uint32_t x = a; x < a + chunk && x <= n; ++x)
+    c += (x >= kFirstTablePrime) && !((comp[x >> 5] >> (x & 31)) & 1u);
+  scan[threadIdx.x] = c;
+  __syncthreads();
+  for (uint32_t o = 1; o < blockDim.x; o <<= 1) {
+    const uint32_t u = threadIdx.x >= o ? scan[threadIdx.x - o] : 0u;
+    __syncthreads();
+    scan[threadIdx.x] += u;
+    __syncthreads();
+  }
+  uint32_t pos = scan[threadIdx.x] - c;
+  for (uint32_t x = a; x < a + chunk && x <= n; ++x)
+    if (x >= kFirstTablePrime && !((comp[x >> 5] >> (x & 31)) & 1u)) {
+      out_p[pos] = x;
+      out_m[pos] = ~0ull / x;
+      ++pos;
+    }
+  if (threadIdx.x == blockDim.x - 1) *out_count = scan[threadIdx.x];
+}
+
+__global__ void prepare_table_kernel(const unsigned long long* vals, uint64_t skip, uint64_t n,
+                                     uint32_t* out_p, unsigned long long* out_m) {
+  for (uint64_t i = skip + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t p = static_cast<uint32_t>(vals[i]);
+    out_p[i - skip] = p;
+    out_m[i - skip] = ~0ull / p;
+  }
+}
+
+}  // namespace
+
+size_t sieve_smem_bytes(uint32_t S) { return (2 * (S / 32) + kTabWords) * sizeof(uint32_t); }
+
+cudaError_t sieve_configure(int* blocks_per_sm) {
+  const size_t smem = sieve_smem_bytes(1u << 18);
+  cudaError_t e;
+  for (auto fn : {sieve_kernel<kCount>, sieve_kernel<kCountChecks>, sieve_kernel<kEnumerate>}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  int worst = 1 << 30;
+  for (auto fn : {sieve_kernel<kCount>, sieve_kernel<kCountChecks>, sieve_kernel<kEnumerate>}) {
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    worst = b < worst ? b : worst;
+  }
+  *blocks_per_sm = worst < 1 ? 1 : worst;
+  return cudaSuccess;
+}
+
+cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st) {
+  const size_t smem = sieve_smem_bytes(p.S);
+  switch (mode) {
+    case kCount: sieve_kernel<kCount><<<grid, kThreads, smem, st>>>(p); break;
+    case kCountChecks: sieve_kernel<kCountChecks><<<grid, kThreads, smem, st>>>(p); break;
+    default: sieve_kernel<kEnumerate><<<grid, kThreads, smem, st>>>(p); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
+                               uint32_t* out_count, cudaStream_t st) {
+  tiny_primes_kernel<<<1, 1024, 0, st>>>(n, out_p, out_m, out_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prepare_table(const unsigned long long* vals, uint64_t skip, uint64_t n,
+                                 uint32_t* out_p, unsigned long long* out_m, cudaStream_t st) {
+  if (n <= skip) return cudaSuccess;
+  const uint64_t cnt = n - skip;
+  const int grid = static_cast<int>(cnt / 256 + 1 < 4096 ? cnt / 256 + 1 : 4096);
+  prepare_table_kernel<<<grid, 256, 0, st>>>(vals, skip, n, out_p, out_m);
+  return cudaGetLastError();
+}
+
+}  // namespace wsk

@@ -1,0 +1,429 @@
+"""Python mirror of the reference's sieve entry points over the GPU C ABI.
+
+Names and semantics follow /root/reference/proj/include/wheelsieve:
+
+* ``Errc`` / ``Error``            -- errors.hpp:9-32 (status = 1 + Errc)
+* ``isqrt``, ``start_offsets``     -- wheel.hpp:50-81 (wheel.cpp:25-33, 96-106)
+* ``round_segment_span``, ``plan_iteration`` -- engine.hpp:69-76 (engine.cpp:311-342)
+* ``run(SieveConfig)``             -- engine.hpp:83: pi / enumeration of [0, limit]
+  into a ``PrimeSink`` (sink.hpp:18-66: ``CountSink``, ``MemorySink``), with the
+  ascending-emission contract enforced by ``PrimeSink.emit`` (sink.cpp:14-37)
+* ``Sieve.count_range / enumerate_range / count_intervals`` -- the [L, R)
+  entry points the reference composes from bootstrap + SegmentBitmap +
+  sieve_segment, as single device calls
+* ``partition``                    -- contiguous per-GPU super-ranges (§8e)
+
+All compute goes through libwheelsieve_cuda.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import WS_FRESH_BASE, WS_OUT_DEVICE, WS_WANT_CHECKS, WsChecks, WsOpts, WsTiming
+
+lib = _lib.lib
+
+K_MAX_WHEEL_INDEX = (2**64 - 1 - 5) // 6          # wheel.hpp:33
+K_MAX_SEGMENT_END = 6 * (K_MAX_WHEEL_INDEX + 1)   # wheel.hpp:37
+DEFAULT_SEGMENT_SLOTS = 1 << 18
+
+
+class Errc(enum.IntEnum):
+    """errors.hpp:9-23 (same order), plus device-side codes."""
+    NotOnWheel = 0
+    Overflow = 1
+    EmptyRange = 2
+    Capacity = 3
+    Domain = 4
+    Alignment = 5
+    BadConfig = 6
+    IncompleteBase = 7
+    Ordering = 8
+    Io = 9
+    BadManifest = 10
+    ChecksumMismatch = 11
+    BeyondFrontier = 12
+    Cuda = 99
+    NoDevice = 100
+    OutOfMemory = 101
+
+
+class Error(RuntimeError):
+    """wheelsieve::Error (errors.hpp:25-32): carries an Errc."""
+
+    def __init__(self, code: Errc, what: str):
+        super().__init__(what)
+        self.code = code
+
+
+def _errc(status: int) -> Errc:
+    return Errc(status - 1)
+
+
+def _check(status: int, ctx=None, what: str = "") -> None:
+    if status == 0:
+        return
+    msg = ""
+    if ctx is not None:
+        msg = (lib.ws_last_error(ctx) or b"").decode()
+    name = (lib.ws_status_name(status) or b"?").decode()
+    raise Error(_errc(status), f"{what}: {name}: {msg}".strip(": "))
+
+
+def isqrt(n: int) -> int:
+    return int(lib.ws_isqrt(n))
+
+
+def start_offsets(p: int, segment_start: int):
+    """wheel.cpp:96-106 -> (id1, id5)."""
+    a, b = C.c_uint64(), C.c_uint64()
+    _check(lib.ws_start_offsets(p, segment_start, C.byref(a), C.byref(b)), what="start_offsets")
+    return a.value, b.value
+
+
+def prime_count_bound(L: int, R: int) -> int:
+    return int(lib.ws_prime_count_bound(L, R))
+
+
+def partition(L: int, R: int, rank: int, world: int,
+              segment_slots: int = DEFAULT_SEGMENT_SLOTS):
+    lo, hi = C.c_uint64(), C.c_uint64()
+    _check(lib.ws_partition(L, R, segment_slots, rank, world, C.byref(lo), C.byref(hi)),
+           what="partition")
+    return lo.value, hi.value
+
+
+@dataclass
+class Checks:
+    count: int
+    sum: int
+    xor: int
+    largest: int
+
+    @staticmethod
+    def of(c: WsChecks) -> "Checks":
+        return Checks(c.count, c.sum, c.xor_, c.largest)
+
+
+def _ptr(a) -> int:
+    """Data pointer of a numpy array or a torch tensor."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _is_device(a) -> bool:
+    return not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
+
+
+class Sieve:
+    """One GPU context (device buffers, stream, resident base-prime table).
+
+    Not reentrant: use one Sieve per host thread / rank."""
+
+    def __init__(self, device: int = -1, segment_slots: int = DEFAULT_SEGMENT_SLOTS):
+        o = WsOpts()
+        lib.ws_opts_default(C.byref(o))
+        o.segment_slots = segment_slots
+        o.device = device
+        h = C.c_void_p()
+        _check(lib.ws_ctx_create(C.byref(o), C.byref(h)), what="ws_ctx_create")
+        self._h = h
+        self.segment_slots = segment_slots
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.ws_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def stream(self) -> int:
+        return lib.ws_ctx_stream(self._h) or 0
+
+    def timing(self) -> WsTiming:
+        t = WsTiming()
+        _check(lib.ws_last_timing(self._h, C.byref(t)), self._h, "timing")
+        return t
+
+    # -- [L, R) entry points -------------------------------------------------
+    def count_range(self, L: int, R: int, checks: bool = False, per_seg=None,
+                    fresh_base: bool = False):
+        """Primes in [L, R).  per_seg: None, True (returns a new uint32 array)
+        or a preallocated numpy / CUDA tensor of uint32 (int32) counts."""
+        out = WsChecks()
+        n = C.c_uint64()
+        flags = (WS_WANT_CHECKS if checks else 0) | (WS_FRESH_BASE if fresh_base else 0)
+        ps_ptr, cap, ret = None, 0, None
+        if per_seg is True:
+            nseg = self.num_segments(L, R)
+            ret = np.zeros(max(1, nseg), np.uint32)
+            ps_ptr, cap = ret.ctypes.data, ret.size
+        elif per_seg is not None:
+            ps_ptr, cap = _ptr(per_seg), per_seg.numel() if _is_device(per_seg) else per_seg.size
+            if _is_device(per_seg):
+                flags |= WS_OUT_DEVICE
+        _check(lib.ws_count_range(self._h, L, R, flags, C.byref(out), ps_ptr, cap, C.byref(n)),
+               self._h, "count_range")
+        res = Checks.of(out)
+        if per_seg is True:
+            return res, ret[: n.value]
+        return res
+
+    def enumerate_range(self, L: int, R: int, out=None, fresh_base: bool = False):
+        """Sorted primes of [L, R).  out: None (a new numpy array is returned),
+        a numpy uint64 array, or a CUDA tensor (int64/uint64) on the ctx device.
+        Returns (values_or_out, n, Checks)."""
+        flags = WS_FRESH_BASE if fresh_base else 0
+        own = out is None
+        if own:
+            out = np.empty(max(1, prime_count_bound(L, R)), np.uint64)
+        if _is_device(out):
+            flags |= WS_OUT_DEVICE
+            cap = out.numel()
+        else:
+            cap = out.size
+        n = C.c_uint64()
+        chk = WsChecks()
+        _check(lib.ws_enumerate_range(self._h, L, R, flags, _ptr(out), cap, C.byref(n),
+                                      C.byref(chk)), self._h, "enumerate_range")
+        if own:
+            return out[: n.value].copy(), n.value, Checks.of(chk)
+        return out, n.value, Checks.of(chk)
+
+    def count_intervals(self, Ls, width: int, want_sums: bool = True, want_xors: bool = True,
+                        fresh_base: bool = False):
+        """Per-interval (counts uint32, sums uint64, xors uint64) of [L_i, L_i + width)."""
+        Ls = np.ascontiguousarray(Ls, dtype=np.uint64)
+        n = Ls.size
+        counts = np.zeros(n, np.uint32)
+        sums = np.zeros(n, np.uint64) if want_sums else None
+        xors = np.zeros(n, np.uint64) if want_xors else None
+        flags = WS_FRESH_BASE if fresh_base else 0
+        _check(lib.ws_count_intervals(self._h, Ls.ctypes.data, n, width, flags,
+                                      counts.ctypes.data,
+                                      sums.ctypes.data if sums is not None else None,
+                                      xors.ctypes.data if xors is not None else None),
+               self._h, "count_intervals")
+        return counts, sums, xors
+
+    def num_segments(self, L: int, R: int) -> int:
+        if R <= L:
+            return 0
+        lo0 = L // 6 * 6
+        slots = (R - lo0 + 5) // 6
+        return (slots + self.segment_slots - 1) // self.segment_slots
+
+
+# ---------------------------------------------------------------------------
+# run(SieveConfig) drop-in (engine.hpp:13-89, sink.hpp:18-66)
+
+class PrimeSink:
+    """sink.hpp:18-43: strictly ascending batches; emit_count for count sinks."""
+
+    def __init__(self):
+        self._count = 0
+        self._largest = 0
+
+    def emit(self, batch) -> None:  # sink.cpp:14-26
+        batch = np.asarray(batch, dtype=np.uint64)
+        if batch.size == 0:
+            return
+        if int(batch[0]) <= self._largest or (batch.size > 1 and not bool(np.all(batch[1:] > batch[:-1]))):
+            raise Error(Errc.Ordering, f"emit batch not strictly ascending past {self._largest}")
+        self.accept(batch)
+        self._count += int(batch.size)
+        self._largest = int(batch[-1])
+
+    def emit_count(self, n: int, largest: int) -> None:  # sink.cpp:28-37
+        if n == 0:
+            return
+        if self.wants_values():
+            raise Error(Errc.Domain, "sink needs the values; count-only emission not possible")
+        if largest <= self._largest:
+            raise Error(Errc.Ordering, f"count batch ends at {largest}, not above {self._largest}")
+        self._count += n
+        self._largest = largest
+
+    def flush(self) -> None:
+        pass
+
+    def wants_values(self) -> bool:
+        return True
+
+    def count(self) -> int:
+        return self._count
+
+    def largest(self) -> int:
+        return self._largest
+
+    def accept(self, batch) -> None:
+        raise NotImplementedError
+
+
+class CountSink(PrimeSink):
+    def wants_values(self) -> bool:
+        return False
+
+    def accept(self, batch) -> None:
+        pass
+
+
+class MemorySink(PrimeSink):
+    def __init__(self):
+        super().__init__()
+        self._chunks: List[np.ndarray] = []
+
+    def accept(self, batch) -> None:
+        self._chunks.append(np.array(batch, dtype=np.uint64))
+
+    def primes(self) -> np.ndarray:
+        return np.concatenate(self._chunks) if self._chunks else np.zeros(0, np.uint64)
+
+
+@dataclass
+class SieveConfig:
+    """engine.hpp:13-29.  `threads` is kept for signature parity (the device
+    decides its own parallelism); segment_span still sets the iteration
+    size used for emission batches and the SieveReport accounting."""
+    limit: Optional[int] = None
+    threads: int = 1
+    segment_span: int = 6_000_000
+    flag_width: int = 0
+    sink: Optional[PrimeSink] = None
+    spawn_per_iteration: bool = False
+    thread_cap: int = 1024
+
+
+@dataclass
+class SieveReport:  # engine.hpp:42-55
+    prime_count: int = 0
+    largest_prime: int = 0
+    iterations: int = 0
+    wall_ms: float = 0.0
+    peak_flag_bytes: int = 0
+    peak_flag_entries: int = 0
+    sieved_to: int = 0
+    stopped: bool = False
+    overflowed: bool = False
+
+
+class SinkFailure(Error):
+    def __init__(self, code, what, partial: SieveReport):
+        super().__init__(code, what)
+        self.partial = partial
+
+
+def round_segment_span(span: int, threads: int) -> int:  # engine.cpp:311-320
+    if threads == 0:
+        raise Error(Errc.BadConfig, "thread count must be positive")
+    align = 6 * threads
+    if span == 0:
+        return align
+    if span % align == 0:
+        return span
+    if span > 2**64 - 1 - align:
+        raise Error(Errc.Overflow, "segment span exceeds the 64-bit value range")
+    return (span // align + 1) * align
+
+
+def _validate(config: SieveConfig) -> None:  # engine.cpp:119-143 (bounded)
+    if config.sink is None:
+        raise Error(Errc.BadConfig, "config has no sink")
+    if config.threads == 0:
+        raise Error(Errc.BadConfig, "thread count must be positive")
+    if config.threads > config.thread_cap:
+        raise Error(Errc.BadConfig, "thread count exceeds the cap")
+    align = 6 * config.threads
+    if config.segment_span == 0 or config.segment_span % align:
+        raise Error(Errc.BadConfig, f"segment span {config.segment_span} is not a positive multiple of {align}")
+    if config.segment_span > K_MAX_SEGMENT_END:
+        raise Error(Errc.BadConfig, "segment span exceeds the 64-bit value range")
+    if config.limit is None:
+        raise Error(Errc.BadConfig, "bounded run requires a limit")
+    if config.limit < 2:
+        raise Error(Errc.EmptyRange, "no primes below 2")
+    if config.limit > K_MAX_SEGMENT_END - 1:
+        raise Error(Errc.Overflow, "limit exceeds the sievable 64-bit range")
+
+
+_default_sieve: Optional[Sieve] = None
+
+
+def _sieve() -> Sieve:
+    global _default_sieve
+    if _default_sieve is None:
+        _default_sieve = Sieve()
+    return _default_sieve
+
+
+def run(config: SieveConfig, sieve: Optional[Sieve] = None) -> SieveReport:
+    """engine.hpp:83 on the GPU: every prime <= limit into config.sink, 2 and
+    3 first, then ascending batches (one per iteration of segment_span)."""
+    _validate(config)
+    sv = sieve or _sieve()
+    t0 = time.perf_counter()
+    limit = config.limit
+    span = config.segment_span
+    limit_end = (limit // 6 + 1) * 6                  # engine.cpp:160
+    iters = limit_end // span + (limit_end % span != 0)
+    rep = SieveReport()
+    sub = span // config.threads
+    # analytic flag accounting (engine.cpp:218-230): the widest iteration
+    ent = 0
+    for j in range(config.threads):
+        lo = j * sub
+        if lo >= min(span, limit_end):
+            break
+        hi = min(lo + sub, min(span, limit_end))
+        ent += 2 * ((hi - lo) // 6)
+    rep.peak_flag_entries = ent
+    widths = {0: lambda n: (n + 7) // 8, 1: lambda n: n, 2: lambda n: 4 * n}
+    rep.peak_flag_bytes = sum(2 * widths[config.flag_width]((min(j * sub + sub, min(span, limit_end)) - j * sub) // 6)
+                              for j in range(config.threads) if j * sub < min(span, limit_end))
+    sink = config.sink
+    try:
+        if not sink.wants_values():
+            c = sv.count_range(0, limit + 1)
+            pre = 2 if limit >= 3 else 1
+            sink.emit_count(pre, 3 if limit >= 3 else 2)
+            if c.count > pre:
+                sink.emit_count(c.count - pre, c.largest)
+        else:
+            sink.emit(np.array([2, 3][: 2 if limit >= 3 else 1], np.uint64))
+            for i in range(iters):
+                lo = max(i * span, 4)
+                hi = min((i + 1) * span, limit + 1)
+                if hi <= lo:
+                    continue
+                vals, n, _ = sv.enumerate_range(lo, hi)
+                if n:
+                    sink.emit(vals)
+    except Error as e:
+        if isinstance(e, SinkFailure) or e.code in (Errc.Cuda, Errc.NoDevice, Errc.OutOfMemory):
+            raise
+        rep.prime_count = sink.count()
+        rep.largest_prime = sink.largest()
+        rep.wall_ms = (time.perf_counter() - t0) * 1e3
+        raise SinkFailure(e.code, str(e), rep) from e
+    rep.iterations = iters
+    rep.sieved_to = limit + 1
+    rep.prime_count = sink.count()
+    rep.largest_prime = sink.largest()
+    rep.wall_ms = (time.perf_counter() - t0) * 1e3
+    return rep

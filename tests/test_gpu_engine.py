@@ -1,0 +1,110 @@
+"""GPU: the run(SieveConfig) drop-in, mirroring the reference's
+tests/test_engine.cpp cases (file:line cited per test)."""
+import numpy as np
+import pytest
+
+import paper_2310_17746_b200 as ws
+from paper_2310_17746_b200 import (CountSink, Errc, Error, MemorySink, SieveConfig, SinkFailure,
+                                   round_segment_span, run)
+
+pytestmark = pytest.mark.gpu
+
+
+def run_collect(limit, threads, span):
+    sink = MemorySink()
+    run(SieveConfig(limit, threads, round_segment_span(span, threads), 0, sink))
+    return [int(x) for x in sink.primes()]
+
+
+def test_round_segment_span():  # test_engine.cpp:48-71
+    assert round_segment_span(6000, 1) == 6000
+    assert round_segment_span(6000, 3) == 6012
+    assert round_segment_span(600000, 3) == 600012
+    assert round_segment_span(6001, 8) == 6048
+    assert round_segment_span(0, 4) == 24
+    assert round_segment_span(1, 1) == 6
+    with pytest.raises(Error) as e:
+        round_segment_span(2**64 - 1, 1000)
+    assert e.value.code == Errc.Overflow
+    with pytest.raises(Error) as e:
+        round_segment_span(6000, 0)
+    assert e.value.code == Errc.BadConfig
+
+
+def test_tiny_limits(port):  # test_engine.cpp:113-121
+    assert run_collect(2, 1, 6000) == [2]
+    assert run_collect(3, 1, 6000) == [2, 3]
+    assert run_collect(4, 1, 6000) == [2, 3]
+    assert run_collect(5, 1, 6000) == [2, 3, 5]
+    assert run_collect(30, 1, 6000) == [int(x) for x in port.naive_sieve(30)]
+    assert run_collect(29, 1, 6000) == [int(x) for x in port.naive_sieve(30)]
+
+
+def test_limits_below_two():  # test_engine.cpp:123-133
+    for limit in (0, 1):
+        with pytest.raises(Error) as e:
+            run(SieveConfig(limit, 1, 6000, 0, MemorySink()))
+        assert e.value.code == Errc.EmptyRange
+
+
+def test_bounded_run_totals(port):  # test_engine.cpp:135-148
+    sink = MemorySink()
+    rep = run(SieveConfig(1_000_000, 2, 600000, 0, sink))
+    assert rep.prime_count == 78498 and rep.largest_prime == 999983
+    assert rep.iterations == 2 and rep.sieved_to == 1_000_001
+    assert not rep.stopped and not rep.overflowed and rep.wall_ms >= 0
+    assert np.array_equal(sink.primes(), port.naive_sieve(1_000_000))
+
+
+def test_flag_accounting():  # test_engine.cpp:150-161
+    def rep(width, threads):
+        return run(SieveConfig(10_000, threads, 6000, width, CountSink()))
+    assert rep(0, 1).peak_flag_entries == 2000
+    assert rep(0, 1).peak_flag_bytes == 250
+    assert rep(1, 1).peak_flag_bytes == 2000
+    assert rep(2, 1).peak_flag_bytes == 8000
+    assert rep(0, 4).peak_flag_entries == 2000
+
+
+def test_invariance(port):  # test_engine.cpp:163-173
+    ref = [int(x) for x in port.naive_sieve(10_000)]
+    for threads in (1, 2, 3, 8):
+        for span in (6000, 60000):
+            assert run_collect(10_000, threads, span) == ref
+
+
+def test_count_only_matches(port):  # test_engine.cpp:175-183
+    c = CountSink()
+    rep = run(SieveConfig(123_456, 3, round_segment_span(6000, 3), 0, c))
+    assert rep.prime_count == 11601 and rep.largest_prime == 123_449
+    assert c.count() == 11601 and c.largest() == 123_449
+
+
+def test_invalid_configs():  # test_engine.cpp:185-225
+    for cfg in (SieveConfig(1000, 1, 6000, 0, None), SieveConfig(1000, 0, 6000, 0, MemorySink()),
+                SieveConfig(1000, 3, 6000, 0, MemorySink()),
+                SieveConfig(1000, 2000, 6_000_000, 0, MemorySink()),
+                SieveConfig(None, 1, 6000, 0, MemorySink())):
+        with pytest.raises(Error) as e:
+            run(cfg)
+        assert e.value.code == Errc.BadConfig
+
+
+class FailingSink(MemorySink):  # test_engine.cpp:38-45
+    def accept(self, batch):
+        if len(batch) and int(batch[-1]) >= 100:
+            raise Error(Errc.Io, "disk full")
+        super().accept(batch)
+
+
+def test_sink_failure_partial(port):  # test_engine.cpp:227-238
+    sink = FailingSink()
+    with pytest.raises(SinkFailure) as e:
+        run(SieveConfig(10_000, 1, 96, 0, sink))
+    assert e.value.code == Errc.Io
+    assert e.value.partial.prime_count == 24 and e.value.partial.largest_prime == 89
+    assert np.array_equal(sink.primes(), port.naive_sieve(96))
+
+
+def test_back_to_back():  # test_engine.cpp:274-280
+    assert run_collect(100, 1, 6000) == run_collect(100, 1, 6000)

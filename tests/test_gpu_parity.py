@@ -1,0 +1,158 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference goldens.  Bar: bit-exact counts, per-segment counts, Σ mod 2^64, ⊕,
+largest prime and enumerated values."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _tuple(c):
+    return (c.count, c.sum, c.xor, c.largest)
+
+
+def test_prefix_goldens(sieve, golden):
+    for rec in golden["prefixes"]:
+        c = sieve.count_range(0, rec["limit"] + 1, checks=True)
+        assert _tuple(c) == (rec["count"], rec["sum"], rec["xor"], rec["largest"]), rec["limit"]
+        c2 = sieve.count_range(0, rec["limit"] + 1)
+        assert (c2.count, c2.largest) == (rec["count"], rec["largest"])
+
+
+def test_window_goldens_per_segment(sieve, sieve12, golden):
+    for rec in golden["windows"]:
+        c, ps = sieve.count_range(rec["L"], rec["R"], checks=True, per_seg=True)
+        assert _tuple(c) == (rec["count"], rec["sum"], rec["xor"], rec["largest"]), rec
+        assert [int(x) for x in ps] == rec["seg18"], (rec["L"], rec["R"])
+        if "seg12" in rec:
+            c12, ps12 = sieve12.count_range(rec["L"], rec["R"], checks=True, per_seg=True)
+            assert _tuple(c12) == _tuple(c)
+            assert [int(x) for x in ps12] == rec["seg12"], (rec["L"], rec["R"])
+
+
+def test_window_enumeration_goldens(sieve, golden, port):
+    for rec in golden["windows"]:
+        if rec["R"] - rec["L"] > 2 * 10**7:
+            continue
+        vals, n, c = sieve.enumerate_range(rec["L"], rec["R"])
+        assert _tuple(c) == (rec["count"], rec["sum"], rec["xor"], rec["largest"])
+        assert n == rec["count"]
+        ref = port.range(rec["L"], rec["R"], values=True)["values"]
+        assert np.array_equal(vals, ref), (rec["L"], rec["R"])
+
+
+def test_config1_per_segment_golden(sieve):
+    g = load_golden("c1_per_segment.json")
+    c, ps = sieve.count_range(0, 10**9 + 1, per_seg=True)
+    assert c.count == g["count"] == 50_847_534
+    assert c.largest == g["largest"]
+    assert [int(x) for x in ps] == g["seg18"]
+
+
+def test_config2_enumeration_checksums(sieve, golden):
+    rec = [p for p in golden["prefixes"] if p["limit"] == 10**10 - 1][0]
+    import torch
+    n_bound = 455_052_511 + 1024
+    out = torch.empty(n_bound, dtype=torch.int64, device="cuda")
+    _, n, c = sieve.enumerate_range(0, 10**10, out=out)
+    assert _tuple(c) == (rec["count"], rec["sum"], rec["xor"], rec["largest"])
+    v = out[:n]
+    assert bool((v[1:] > v[:-1]).all())  # strictly ascending
+    # the device array carries exactly the primes the checksums describe
+    assert int(v.sum().item()) % 2**64 == rec["sum"] % 2**64 or True  # int64 wraps
+    assert int(v[-1].item()) == rec["largest"] and int(v[0].item()) == 2
+    host = v.cpu().numpy().view(np.uint64)
+    assert int(host.sum(dtype=np.uint64)) == rec["sum"]
+    assert int(np.bitwise_xor.reduce(host)) == rec["xor"]
+
+
+def test_config3_pi_1e12(sieve):
+    c = sieve.count_range(0, 10**12 + 1)
+    assert c.count == 37_607_912_018  # SURVEY Appendix A (reference run(), 477 s @8T)
+    assert c.largest == 999_999_999_989
+
+
+def test_config5_intervals_golden(sieve):
+    g = load_golden("c5_intervals.json")
+    counts, sums, xors = sieve.count_intervals(np.array(g["L"], np.uint64), g["width"])
+    assert [int(x) for x in counts] == g["counts"]
+    assert [int(x) for x in sums] == g["sums"]
+    assert [int(x) for x in xors] == g["xors"]
+
+
+def test_c4_slice_golden(sieve, golden):
+    rec = [w for w in golden["windows"] if (w["L"], w["R"]) == (10**15, 10**15 + 10**8)][0]
+    c = sieve.count_range(rec["L"], rec["R"], checks=True)
+    assert _tuple(c) == (rec["count"], rec["sum"], rec["xor"], rec["largest"])
+
+
+def test_random_windows_vs_oracle(sieve, sieve12, port):
+    rng = np.random.default_rng(1234)
+    for i in range(60):
+        kind = i % 4
+        if kind == 0:
+            L = int(rng.integers(0, 3000))
+        elif kind == 1:
+            L = int(rng.integers(0, 10**9))
+        elif kind == 2:
+            L = int(rng.integers(0, 10**14))
+        else:
+            L = int(rng.integers(10**15, 10**16 - 10**7))
+        W = int(rng.integers(1, 4_000_000 if kind < 3 else 400_000))
+        ref = port.range(L, L + W, seg_slots=1 << 12, per_seg=True, values=True)
+        for sv in (sieve, sieve12):
+            c, ps = sv.count_range(L, L + W, checks=True, per_seg=True)
+            assert _tuple(c) == (ref["count"], ref["sum"], ref["xor"], ref["largest"]), (L, W)
+            if sv is sieve12:
+                assert [int(x) for x in ps] == [int(x) for x in ref["per_seg"]], (L, W)
+        vals, n, c = sieve.enumerate_range(L, L + W)
+        assert np.array_equal(vals, ref["values"]), (L, W)
+
+
+def test_tiny_ranges_exhaustive(sieve, port):
+    for L in range(0, 60):
+        for R in range(L, 80):
+            c = sieve.count_range(L, R, checks=True)
+            r = port.range(L, R)
+            assert _tuple(c) == (r["count"], r["sum"], r["xor"], r["largest"]), (L, R)
+
+
+def test_base_table_growth_and_fresh(port):
+    import paper_2310_17746_b200 as ws
+    with ws.Sieve() as s:
+        a = s.count_range(10**6, 10**6 + 10**5, checks=True)       # small base
+        b = s.count_range(10**14, 10**14 + 10**6, checks=True)     # grows the table
+        c = s.count_range(10**6, 10**6 + 10**5, checks=True)       # reuses the larger one
+        d = s.count_range(10**6, 10**6 + 10**5, checks=True, fresh_base=True)
+        assert _tuple(a) == _tuple(c) == _tuple(d)
+        r = port.range(10**14, 10**14 + 10**6)
+        assert _tuple(b) == (r["count"], r["sum"], r["xor"], r["largest"])
+
+
+def test_errors(sieve):
+    import paper_2310_17746_b200 as ws
+    K = ws.wheelsieve.K_MAX_SEGMENT_END
+    with pytest.raises(ws.Error) as e:
+        sieve.count_range(0, K + 1)
+    assert e.value.code == ws.Errc.Overflow
+    assert sieve.count_range(100, 100).count == 0
+    assert sieve.count_range(100, 50).count == 0
+    out = np.zeros(3, np.uint64)
+    with pytest.raises(ws.Error) as e:
+        sieve.enumerate_range(0, 100, out=out)
+    assert e.value.code == ws.Errc.Capacity
+    assert list(out) == [2, 3, 5]
+    with pytest.raises(ws.Error):
+        ws.Sieve(segment_slots=1000)
+
+
+def test_device_per_segment_and_timing(sieve):
+    import torch
+    nseg = sieve.num_segments(0, 10**9 + 1)
+    ps = torch.zeros(nseg, dtype=torch.int32, device="cuda")
+    c = sieve.count_range(0, 10**9 + 1, per_seg=ps)
+    assert int(ps.sum().item()) + 2 == c.count
+    t = sieve.timing()
+    assert t.sieve_ms > 0 and t.segments == nseg and t.launches >= 1
