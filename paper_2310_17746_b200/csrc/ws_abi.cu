@@ -81,7 +81,7 @@ struct ws_ctx {
   cudaStream_t stream = nullptr;
   uint32_t S = 1u << 18;
   int sms = 148;
-  int bps = 2;
+  int bps[3] = {2, 2, 2};  // resident blocks per SM per mode
   std::string err;
   ws_timing timing{};
   cudaEvent_t ev[4] = {};
@@ -204,7 +204,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.status = c->status.ptr;
   p.out = out;
   p.out_cap = out_cap;
-  const uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps;
+  const uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps[mode];
   const int grid = static_cast<int>(std::min<uint64_t>(nseg, max_grid));
   if (timed) ck(cudaEventRecord(c->ev[2], c->stream), "event");
   ck(wsk::launch_sieve(mode, p, grid, c->stream), "sieve launch");
@@ -380,7 +380,7 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   c->sms = prop.multiProcessorCount;
   if (cudaSetDevice(dev) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      wsk::sieve_configure(&c->bps) != cudaSuccess) {
+      wsk::sieve_configure(c->bps) != cudaSuccess) {
     delete c;
     cudaGetLastError();
     return WS_CUDA;

@@ -46,7 +46,8 @@ struct SieveParams {
   unsigned long long out_cap;
 };
 
-size_t sieve_smem_bytes(uint32_t S);
+size_t sieve_smem_bytes(uint32_t S, int mode);
+// blocks_per_sm[mode] for the three modes
 cudaError_t sieve_configure(int* blocks_per_sm);
 cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st);
 

@@ -63,10 +63,6 @@ __device__ __forceinline__ uint32_t mod_barrett(uint64_t x, uint32_t p, uint64_t
 
 __device__ __forceinline__ uint32_t swz(uint32_t w) { return w ^ ((w >> 5) & 31u); }
 
-__device__ __forceinline__ void clear_bit(uint32_t* bm, uint32_t h) {
-  atomicAnd(bm + swz(h >> 5), ~(1u << (h & 31u)));
-}
-
 // bits [a, b) of a 32-bit word, a and b clamped to [0, 32]
 __device__ __forceinline__ uint32_t range_mask(int64_t a, int64_t b) {
   a = a < 0 ? 0 : (a > 32 ? 32 : a);
@@ -165,7 +161,10 @@ __device__ void fetch_segment(const SieveParams& P, SegInfo& si) {
   si.nwords = ((si.len + 1023u) / 1024u) * 32u;
 }
 
-// Phase 1: stamp primes 5..31 and the [L, R) trim into every word.
+// Phase 1: stamp primes 5..31 and the [L, R) trim into every word.  The
+// bitmaps hold COMPOSITE flags (bit set = crossed off or outside [L, R)):
+// the complement of the reference's FlagArray, so crossing off is a single
+// ATOMS.OR and survivors are ~word.
 __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* tab, uint32_t* bm1,
                                            uint32_t* bm5) {
   const uint32_t o0 = static_cast<uint32_t>(si.ks % 5005u);
@@ -188,8 +187,8 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
     const int64_t base = 32 * static_cast<int64_t>(w);
     m1 &= range_mask(static_cast<int64_t>(si.lo1) - base, static_cast<int64_t>(si.hi1) - base);
     m5 &= range_mask(static_cast<int64_t>(si.lo5) - base, static_cast<int64_t>(si.hi5) - base);
-    bm1[swz(w)] = m1;
-    bm5[swz(w)] = m5;
+    bm1[swz(w)] = ~m1;
+    bm5[swz(w)] = ~m5;
   }
 }
 
@@ -214,30 +213,72 @@ __device__ __forceinline__ bool prime_offsets(uint32_t p, uint64_t m, uint64_t k
   return true;
 }
 
+__device__ __forceinline__ void mark(uint32_t* bm, uint32_t h) {
+  atomicOr(bm + swz(h >> 5), 1u << (h & 31u));
+}
+
+// Warp-cooperative strided marking of one class: lane l takes hits
+// h0 + l*p, h0 + (l+32)*p, ...  Consecutive hits of a lane are 32*p bits
+// apart, i.e. exactly p words, so the bit within the word is loop-invariant.
+__device__ __forceinline__ void mark_strided(uint32_t* bm, uint32_t h0, uint32_t p, uint32_t len,
+                                             uint32_t lane) {
+  const uint32_t h = h0 + lane * p;
+  if (h >= len) return;
+  const uint32_t bit = 1u << (h & 31u);
+  const uint32_t wlim = (len - (h & 31u) + 31u) >> 5;  // words w with 32w + bit < len
+  uint32_t w = h >> 5;
+#pragma unroll 4
+  for (; w < wlim; w += p) atomicOr(bm + swz(w), bit);
+}
+
 // Phase 2: medium and large primes.
 __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo& si,
-                                             uint32_t* bm1, uint32_t* bm5) {
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+                                             uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr,
+                                             uint32_t* lp_ctr) {
+  const uint32_t lane = threadIdx.x & 31u;
   const uint32_t len = si.len;
   const uint64_t ks = si.ks;
-  // warp-cooperative: all lanes of a warp take one prime
-  for (uint32_t i = warp; i < P.n_wc; i += kWarps) {
+  // warp-cooperative primes, handed out dynamically (largest work first)
+  for (;;) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(wc_ctr, 1u);
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= P.n_wc) break;
     const uint32_t p = P.prime_p[i];
     uint32_t rel1, rel5;
     if (!prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5)) break;
-    const uint32_t step = 32 * p;
-#pragma unroll 4
-    for (uint32_t h = rel1 + lane * p; h < len; h += step) clear_bit(bm1, h);
-#pragma unroll 4
-    for (uint32_t h = rel5 + lane * p; h < len; h += step) clear_bit(bm5, h);
+    mark_strided(bm1, rel1, p, len, lane);
+    mark_strided(bm5, rel5, p, len, lane);
   }
-  // one thread per prime
-  for (uint32_t i = P.n_wc + threadIdx.x; i < P.nprimes; i += kThreads) {
-    const uint32_t p = P.prime_p[i];
-    uint32_t rel1, rel5;
-    if (!prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5)) break;
-    for (uint32_t h = rel1; h < len; h += p) clear_bit(bm1, h);
-    for (uint32_t h = rel5; h < len; h += p) clear_bit(bm5, h);
+  // one thread per prime, in warp-sized chunks handed out dynamically; both
+  // classes advance together (their hits are the same stride p apart)
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(lp_ctr, 32u);
+    base = __shfl_sync(kFull, base, 0) + P.n_wc;
+    if (base >= P.nprimes) break;
+    const uint32_t i = base + lane;
+    uint32_t p = 0, rel1 = 0, rel5 = 0;
+    bool active = false;
+    if (i < P.nprimes) {
+      p = P.prime_p[i];
+      active = prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5);
+    }
+    if (!__any_sync(kFull, active)) break;  // primes ascend: later chunks are inactive too
+    if (!active) continue;
+    const bool one_first = rel1 <= rel5;
+    uint32_t* ba = one_first ? bm1 : bm5;
+    uint32_t* bb = one_first ? bm5 : bm1;
+    uint32_t h = one_first ? rel1 : rel5;
+    const uint32_t hb = one_first ? rel5 : rel1;
+    if (hb < len) {
+      const uint32_t d = hb - h;  // < p and < len
+      for (; h + d < len; h += p) {
+        mark(ba, h);
+        mark(bb, h + d);
+      }
+    }
+    for (; h < len; h += p) mark(ba, h);
   }
 }
 
@@ -259,18 +300,23 @@ __device__ __forceinline__ unsigned long long warp_max64(unsigned long long v) {
   }
   return v;
 }
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, uint32_t lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(kFull, v, o);
+    if (lane >= static_cast<uint32_t>(o)) v += u;
+  }
+  return v;
+}
 
-// interleave two 32-bit masks: bit 2j <- a_j (class 1), bit 2j+1 <- b_j (class 5)
-__device__ __forceinline__ unsigned long long interleave(uint32_t a, uint32_t b) {
-  auto spread = [](unsigned long long x) {
-    x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
-    x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
-    x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
-    x = (x | (x << 2)) & 0x3333333333333333ull;
-    x = (x | (x << 1)) & 0x5555555555555555ull;
-    return x;
-  };
-  return spread(a) | (spread(b) << 1);
+// spread the low 16 bits of x to the even bit positions of a 32-bit word
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -319,6 +365,15 @@ __device__ unsigned long long lookback(unsigned long long* status, uint64_t s,
   return prefix;
 }
 
+// Emission staging: per warp, up to kStage 16-bit survivor positions of one
+// 32-word round (bit 64*lane + b of the interleaved masks).
+constexpr uint32_t kStage = 1024;
+
+template <int MODE>
+constexpr size_t mode_smem_extra() {
+  return MODE == kEnumerate ? kWarps * kStage * sizeof(uint16_t) : 0;
+}
+
 // ---------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P) {
@@ -326,21 +381,27 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
   uint32_t* bm1 = smem;
   uint32_t* bm5 = smem + P.S / 32;
   uint32_t* tab = smem + 2 * (P.S / 32);
+  uint16_t* stage_all = reinterpret_cast<uint16_t*>(tab + kTabWords);
   __shared__ SegInfo si;
   __shared__ unsigned long long red_a[kWarps], red_b[kWarps], red_c[kWarps];
   __shared__ uint32_t red_n[kWarps];
+  __shared__ uint32_t wc_ctr, lp_ctr;
   __shared__ unsigned long long seg_base;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 
   build_tables(tab);
   for (;;) {
     __syncthreads();  // bitmap / si reuse guard
-    if (threadIdx.x == 0) fetch_segment(P, si);
+    if (threadIdx.x == 0) {
+      fetch_segment(P, si);
+      wc_ctr = 0;
+      lp_ctr = 0;
+    }
     __syncthreads();
     if (si.s >= P.nseg_total) break;
     init_words(si, tab, bm1, bm5);
     __syncthreads();
-    sieve_primes(P, si, bm1, bm5);
+    sieve_primes(P, si, bm1, bm5, &wc_ctr, &lp_ctr);
     __syncthreads();
 
     const uint64_t vbase = 6 * si.ks;
@@ -348,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
       uint32_t cnt = 0;
       unsigned long long lg = 0, sum = 0, xr = 0;
       for (uint32_t wp = threadIdx.x; wp < si.nwords; wp += kThreads) {
-        const uint32_t m1 = bm1[wp], m5 = bm5[wp];
+        const uint32_t m1 = ~bm1[wp], m5 = ~bm5[wp];
         cnt += __popc(m1) + __popc(m5);
         if (m1 | m5) {
           const uint32_t w = swz(wp);  // logical word of this physical slot
@@ -409,29 +470,20 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
       }
     } else {
       // ---- ordered enumeration ----
-      // warp `warp` owns logical words [warp*wpw, (warp+1)*wpw)
-      const uint32_t wpw = si.nwords / kWarps;  // nwords is a multiple of 32*kWarps? see below
+      // warp `warp` owns logical words [w_begin, w_end); the last warp also
+      // takes the remainder, so warp order is word order.
+      const uint32_t wpw = si.nwords / kWarps;
       const uint32_t w_begin = warp * wpw;
+      const uint32_t w_end = warp == kWarps - 1 ? si.nwords : w_begin + wpw;
       uint32_t cnt = 0;
-      for (uint32_t w = w_begin + lane; w < w_begin + wpw; w += 32)
-        cnt += __popc(bm1[swz(w)]) + __popc(bm5[swz(w)]);
-      // words beyond kWarps * wpw (remainder) belong to the last warp
-      const uint32_t tail_begin = kWarps * wpw;
-      if (warp == kWarps - 1)
-        for (uint32_t w = tail_begin + lane; w < si.nwords; w += 32)
-          cnt += __popc(bm1[swz(w)]) + __popc(bm5[swz(w)]);
+      for (uint32_t w = w_begin + lane; w < w_end; w += 32)
+        cnt += __popc(~bm1[swz(w)]) + __popc(~bm5[swz(w)]);
       cnt = __reduce_add_sync(kFull, cnt);
       if (lane == 0) red_n[warp] = cnt;
       __syncthreads();
       if (warp == 0) {
-        // exclusive scan over warps
-        uint32_t c = lane < kWarps ? red_n[lane] : 0u;
-        uint32_t incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t u = __shfl_up_sync(kFull, incl, o);
-          if (lane >= static_cast<uint32_t>(o)) incl += u;
-        }
+        const uint32_t c = lane < kWarps ? red_n[lane] : 0u;
+        const uint32_t incl = warp_incl_scan(c, lane);
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         if (lane < kWarps) red_n[lane] = incl - c;
         const unsigned long long base = lookback(P.status, si.s, total);
@@ -444,35 +496,78 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
       __syncthreads();
       unsigned long long pos = seg_base + red_n[warp];
       unsigned long long sum = 0, xr = 0, lg = 0;
-      auto emit_rounds = [&](uint32_t wb, uint32_t we) {
-        for (uint32_t w0 = wb; w0 < we; w0 += 32) {
-          const uint32_t w = w0 + lane;
-          unsigned long long M = 0;
-          if (w < we) M = interleave(bm1[swz(w)], bm5[swz(w)]);
-          const uint32_t c = __popcll(M);
-          uint32_t incl = c;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(kFull, incl, o);
-            if (lane >= static_cast<uint32_t>(o)) incl += u;
-          }
-          const uint32_t rtotal = __shfl_sync(kFull, incl, 31);
-          unsigned long long o = pos + (incl - c);
-          const unsigned long long wbv = vbase + 192ull * w;
-          for (; M; M &= M - 1) {
-            const uint32_t b = __ffsll(static_cast<long long>(M)) - 1;
-            const unsigned long long v = wbv + 3ull * b + 1 + (b & 1u);
-            if (o < P.out_cap) P.out[o] = v;
-            ++o;
-            sum += v;
-            xr ^= v;
-            lg = v;
-          }
-          pos += rtotal;
+      uint16_t* stage = stage_all + warp * kStage;
+      for (uint32_t w0 = w_begin; w0 < w_end; w0 += 32) {
+        const uint32_t w = w0 + lane;
+        uint32_t a = 0, b = 0;
+        if (w < w_end) {
+          a = ~bm1[swz(w)];
+          b = ~bm5[swz(w)];
         }
-      };
-      emit_rounds(w_begin, w_begin + wpw);
-      if (warp == kWarps - 1) emit_rounds(tail_begin, si.nwords);
+        // ascending value order interleaves the classes: bit 2j <- 6k+1, 2j+1 <- 6k+5
+        const uint32_t lo = spread16(a) | (spread16(b) << 1);
+        const uint32_t hi = spread16(a >> 16) | (spread16(b >> 16) << 1);
+        const uint32_t c = __popc(lo) + __popc(hi);
+        const uint32_t incl = warp_incl_scan(c, lane);
+        const uint32_t rtotal = __shfl_sync(kFull, incl, 31);
+        const unsigned long long rbase = vbase + 192ull * w0;  // value base of the round
+        if (rtotal == 0) continue;
+        if (rtotal <= kStage) {
+          // 1) each lane drops its survivor positions (64*lane + bit) into the stage
+          uint32_t o = incl - c;
+          const uint32_t eb = lane << 6;
+          for (uint32_t x = lo; x; x &= x - 1) stage[o++] = static_cast<uint16_t>(eb | (__ffs(x) - 1));
+          for (uint32_t x = hi; x; x &= x - 1)
+            stage[o++] = static_cast<uint16_t>(eb | 32u | (__ffs(x) - 1));
+          __syncwarp();
+          // 2) coalesced: lane i writes survivors i, i+32, ... of the round
+          unsigned long long* dst = P.out + pos;
+          uint32_t soff = 0, n = 0;
+          if (pos + rtotal <= P.out_cap) {
+#pragma unroll 4
+            for (uint32_t i = lane; i < rtotal; i += 32) {
+              const uint32_t e = stage[i];
+              const uint32_t bb = e & 63u;
+              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+              const unsigned long long v = rbase + off;
+              dst[i] = v;
+              soff += off;
+              ++n;
+              xr ^= v;
+            }
+          } else {
+            for (uint32_t i = lane; i < rtotal; i += 32) {
+              const uint32_t e = stage[i];
+              const uint32_t bb = e & 63u;
+              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+              const unsigned long long v = rbase + off;
+              if (pos + i < P.out_cap) dst[i] = v;
+              soff += off;
+              ++n;
+              xr ^= v;
+            }
+          }
+          sum += rbase * n + soff;
+          const uint32_t e = stage[rtotal - 1];
+          const uint32_t bb = e & 63u;
+          lg = rbase + (192u * (e >> 6) + 3u * bb + 1u + (bb & 1u));
+          __syncwarp();
+        } else {
+          unsigned long long o = pos + (incl - c);
+          for (int half = 0; half < 2; ++half)
+            for (uint32_t x = half ? hi : lo; x; x &= x - 1) {
+              const uint32_t bb = (__ffs(x) - 1) + 32u * half;
+              const unsigned long long v = rbase + (192u * lane + 3u * bb + 1u + (bb & 1u));
+              if (o < P.out_cap) P.out[o] = v;
+              ++o;
+              sum += v;
+              xr ^= v;
+              lg = max(lg, v);
+            }
+          lg = warp_max64(lg);
+        }
+        pos += rtotal;
+      }
       sum = warp_sum64(sum);
       xr = warp_xor64(xr);
       lg = warp_max64(lg);
@@ -555,29 +650,31 @@ __global__ void prepare_table_kernel(const unsigned long long* vals, uint64_t sk
 
 }  // namespace
 
-size_t sieve_smem_bytes(uint32_t S) { return (2 * (S / 32) + kTabWords) * sizeof(uint32_t); }
+size_t sieve_smem_bytes(uint32_t S, int mode) {
+  const size_t base = (2 * (S / 32) + kTabWords) * sizeof(uint32_t);
+  return base + (mode == kEnumerate ? mode_smem_extra<kEnumerate>() : 0);
+}
 
 cudaError_t sieve_configure(int* blocks_per_sm) {
-  const size_t smem = sieve_smem_bytes(1u << 18);
   cudaError_t e;
-  for (auto fn : {sieve_kernel<kCount>, sieve_kernel<kCountChecks>, sieve_kernel<kEnumerate>}) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const void* fns[3] = {reinterpret_cast<const void*>(sieve_kernel<kCount>),
+                        reinterpret_cast<const void*>(sieve_kernel<kCountChecks>),
+                        reinterpret_cast<const void*>(sieve_kernel<kEnumerate>)};
+  for (int m = 0; m < 3; ++m) {
+    const size_t smem = sieve_smem_bytes(1u << 18, m);
+    e = cudaFuncSetAttribute(fns[m], cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-  }
-  int worst = 1 << 30;
-  for (auto fn : {sieve_kernel<kCount>, sieve_kernel<kCountChecks>, sieve_kernel<kEnumerate>}) {
     int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fns[m], kThreads, smem);
     if (e != cudaSuccess) return e;
-    worst = b < worst ? b : worst;
+    blocks_per_sm[m] = b < 1 ? 1 : b;
   }
-  *blocks_per_sm = worst < 1 ? 1 : worst;
   return cudaSuccess;
 }
 
 cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st) {
-  const size_t smem = sieve_smem_bytes(p.S);
+  const size_t smem = sieve_smem_bytes(p.S, mode);
   switch (mode) {
     case kCount: sieve_kernel<kCount><<<grid, kThreads, smem, st>>>(p); break;
     case kCountChecks: sieve_kernel<kCountChecks><<<grid, kThreads, smem, st>>>(p); break;
