@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -94,7 +95,16 @@ struct ws_ctx {
   DevBuf<uint32_t> tab_p;
   DevBuf<unsigned long long> tab_m;
 
+  uint32_t n_below_S = 0;  // table primes (>= 37) below S: in-kernel; the rest bucketed
+  size_t bucket_budget = 1ull << 30;  // bytes of bucket lists per window
+  uint32_t cap_override = 0;           // test knob (WHEELSIEVE_BUCKET_CAP)
+  uint32_t piece_override = 0;         // tuning knob (WHEELSIEVE_FILL_PIECE)
+  uint32_t bucket_min_ratio = 8;       // buckets iff largest base prime >= ratio * S
+
   // scratch
+  DevBuf<uint32_t> bucket;
+  DevBuf<uint32_t> bcount;
+  DevBuf<wsk::Run> runs;
   DevBuf<wsk::Job> jobs;
   DevBuf<wsk::JobAcc> acc;
   DevBuf<unsigned long long> ticket;
@@ -108,7 +118,8 @@ struct ws_ctx {
 
   ~ws_ctx() {
     cudaSetDevice(device);
-    for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n}) b->release();
+    for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n, &bucket, &bcount}) b->release();
+    runs.release();
     for (auto* b : {&tab_m, &ticket, &status, &vals, &l0_m}) b->release();
     jobs.release();
     acc.release();
@@ -162,7 +173,16 @@ void validate_range(uint64_t L, uint64_t R) {
   (void)L;
 }
 
-// One launch of the segment kernel over ctx->h_jobs.
+// Expected large-prime hits per segment: 2 S sum_{S <= p <= P} 1/p, by
+// Mertens' estimate sum 1/p over [a, b] ~ ln(ln b / ln a).
+double expected_large_hits(uint32_t S, double pmax) {
+  if (pmax <= S) return 0;
+  return 2.0 * S * std::log(std::log(pmax) / std::log(static_cast<double>(S)));
+}
+
+// The segment kernel over every segment of ctx->h_jobs.  Without large
+// primes this is one launch; otherwise the segments are processed in windows
+// of W segments: bucket_fill (large-prime hit lists) then the sieve kernel.
 void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* out,
                unsigned long long out_cap, bool timed) {
   uint64_t nseg = 0;
@@ -170,11 +190,9 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   const size_t nj = c->h_jobs.size();
   c->jobs.reserve(nj, "jobs");
   c->acc.reserve(nj, "acc");
-  c->ticket.reserve(1, "ticket");
   ck(cudaMemcpyAsync(c->jobs.ptr, c->h_jobs.data(), nj * sizeof(wsk::Job),
                      cudaMemcpyHostToDevice, c->stream), "upload jobs");
   ck(cudaMemsetAsync(c->acc.ptr, 0, nj * sizeof(wsk::JobAcc), c->stream), "zero acc");
-  ck(cudaMemsetAsync(c->ticket.ptr, 0, sizeof(unsigned long long), c->stream), "zero ticket");
   if (mode == wsk::kEnumerate) {
     c->status.reserve(nseg, "status");
     ck(cudaMemsetAsync(c->status.ptr, 0, nseg * sizeof(unsigned long long), c->stream),
@@ -190,26 +208,102 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.prime_m = c->tab_m.ptr;
   p.nprimes = c->nprimes;
   // warp-cooperative loop for primes below 1024 (>= 256 hits per class per
-  // 2^18-slot segment); one thread per prime above
-  uint32_t nwc = 0;
-  {
-    // primes in [37, 1024): 172 - 11 = 161 entries
-    static const uint32_t kWcCount = 161;
-    nwc = std::min<uint32_t>(kWcCount, c->nprimes);
-  }
-  p.n_wc = nwc;
-  p.ticket = c->ticket.ptr;
+  // 2^18-slot segment): 161 table entries; one thread per prime above
+  p.n_wc = std::min<uint32_t>(161, c->nprimes);
+  p.n_mid = std::min<uint32_t>(std::max(c->n_below_S, p.n_wc), c->nprimes);
   p.acc = c->acc.ptr;
   p.per_seg = per_seg_dev;
   p.status = c->status.ptr;
   p.out = out;
   p.out_cap = out_cap;
   const uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps[mode];
-  const int grid = static_cast<int>(std::min<uint64_t>(nseg, max_grid));
+  // Buckets pay off only when most large primes are far above S (c4: up to
+  // 120 S, c5: 16 S); up to a few S (c3: 3.8 S) the per-(prime, segment)
+  // offset check in the kernel is cheaper than fill + apply + windowing.
+  const bool buckets = c->nprimes > p.n_mid &&
+                       c->base_B >= static_cast<uint64_t>(c->bucket_min_ratio) * c->S;
+  uint64_t W = nseg;
+  uint32_t cap = 0;
+  if (buckets) {
+    const double E = expected_large_hits(c->S, static_cast<double>(c->base_B));
+    cap = static_cast<uint32_t>(1.1 * E + 8.0 * std::sqrt(E) + 1024);
+    cap = (cap + 31) / 32 * 32;
+    if (c->cap_override) cap = c->cap_override;
+    W = std::max<uint64_t>(8, c->bucket_budget / (4ull * cap));
+    W = std::min<uint64_t>({W, wsk::kMaxWindow, nseg});
+    c->bucket.reserve(W * cap, "bucket lists");
+    c->bcount.reserve(W, "bucket counts");
+    ck(cudaMemsetAsync(c->bcount.ptr, 0, W * sizeof(uint32_t), c->stream), "zero bcount");
+  }
+  const uint64_t nwin = (nseg + W - 1) / W;
+  c->ticket.reserve(nwin, "tickets");
+  ck(cudaMemsetAsync(c->ticket.ptr, 0, nwin * sizeof(unsigned long long), c->stream),
+     "zero tickets");
+  // runs of every window, uploaded once
+  std::vector<wsk::Run> runs;
+  std::vector<uint32_t> run_off(nwin + 1, 0);
+  uint64_t piece = W;
+  if (buckets) {
+    // runs are cut into 64-segment pieces: short per-thread hit loops and a
+    // fill grid that covers the GPU (measured best for c4 and c5)
+    piece = c->piece_override ? c->piece_override : 64;
+    piece = std::min<uint64_t>(piece, W);
+    size_t j = 0;
+    for (uint64_t w = 0; w < nwin; ++w) {
+      const uint64_t ws = w * W, we = std::min(nseg, ws + W);
+      while (j < nj && c->h_jobs[j].seg_begin + c->h_jobs[j].nseg <= ws) ++j;
+      for (size_t q = j; q < nj && c->h_jobs[q].seg_begin < we; ++q) {
+        const wsk::Job& J = c->h_jobs[q];
+        const uint64_t a0 = std::max(ws, J.seg_begin), b0 = std::min(we, J.seg_begin + J.nseg);
+        // runs are cut into pieces of at most `piece` segments so the fill
+        // grid scales with the window when there are few large primes
+        for (uint64_t x = a0; x < b0; x += piece) {
+          const uint64_t y = std::min<uint64_t>(b0, x + piece);
+          wsk::Run r{};
+          r.k_lo = J.K0 + (x - J.seg_begin) * c->S;
+          r.k_hi = std::min(J.K0 + (y - J.seg_begin) * c->S, J.K0 + J.nslots);
+          r.seg0 = static_cast<uint32_t>(x - ws);
+          r.nseg = static_cast<uint32_t>(y - x);
+          runs.push_back(r);
+        }
+      }
+      run_off[w + 1] = static_cast<uint32_t>(runs.size());
+    }
+    c->runs.reserve(runs.size(), "runs");
+    ck(cudaMemcpyAsync(c->runs.ptr, runs.data(), runs.size() * sizeof(wsk::Run),
+                       cudaMemcpyHostToDevice, c->stream), "upload runs");
+    ck(cudaStreamSynchronize(c->stream), "sync runs");  // `runs` is pageable and local
+  }
   if (timed) ck(cudaEventRecord(c->ev[2], c->stream), "event");
-  ck(wsk::launch_sieve(mode, p, grid, c->stream), "sieve launch");
+  for (uint64_t w = 0; w < nwin; ++w) {
+    const uint64_t ws = w * W, we = std::min(nseg, ws + W);
+    if (buckets) {
+      wsk::FillParams f{};
+      f.runs = c->runs.ptr + run_off[w];
+      f.nruns = run_off[w + 1] - run_off[w];
+      f.prime_p = c->tab_p.ptr;
+      f.prime_m = c->tab_m.ptr;
+      f.p_begin = p.n_mid;
+      f.p_end = c->nprimes;
+      f.log2S = static_cast<uint32_t>(__builtin_ctz(c->S));
+      f.bucket = c->bucket.ptr;
+      f.bcount = c->bcount.ptr;
+      f.bcap = cap;
+      f.max_run_segs = static_cast<uint32_t>(piece);
+      ck(wsk::launch_bucket_fill(f, c->stream), "bucket fill");
+      c->timing.launches += 1;
+      p.bucket = c->bucket.ptr;
+      p.bcount = c->bcount.ptr;
+      p.bcap = cap;
+    }
+    p.s_begin = ws;
+    p.s_count = we - ws;
+    p.ticket = c->ticket.ptr + w;
+    const int grid = static_cast<int>(std::min<uint64_t>(we - ws, max_grid));
+    ck(wsk::launch_sieve(mode, p, grid, c->stream), "sieve launch");
+    c->timing.launches += 1;
+  }
   if (timed) ck(cudaEventRecord(c->ev[3], c->stream), "event");
-  c->timing.launches += 1;
   c->timing.segments += nseg;
 }
 
@@ -377,6 +471,21 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   if (!c) return WS_OUT_OF_MEMORY;
   c->device = dev;
   c->S = S;
+  {  // primes in [37, S): the in-kernel share of the table
+    std::vector<uint8_t> comp(S, 0);
+    uint32_t n = 0;
+    for (uint32_t i = 2; i < S; ++i) {
+      if (comp[i]) continue;
+      if (i >= wsk::kFirstTablePrime) ++n;
+      for (uint64_t j = static_cast<uint64_t>(i) * i; j < S; j += i) comp[j] = 1;
+    }
+    c->n_below_S = n;
+  }
+  // test / tuning knobs: bucket-list capacity per segment and window budget
+  if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CAP")) c->cap_override = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_BUCKET_BUDGET")) c->bucket_budget = std::strtoull(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_FILL_PIECE")) c->piece_override = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_BUCKET_RATIO")) c->bucket_min_ratio = std::strtoul(e, nullptr, 10);
   c->sms = prop.multiProcessorCount;
   if (cudaSetDevice(dev) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||

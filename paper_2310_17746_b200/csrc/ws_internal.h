@@ -29,15 +29,34 @@ struct JobAcc {
 
 enum Mode : int { kCount = 0, kCountChecks = 1, kEnumerate = 2 };
 
+// Large-prime buckets: per window of segments, the hits of every prime
+// p >= S (at most one per class per segment) are scattered into per-segment
+// lists of uint32 entries (slot | class << 18) by bucket_fill_kernel and
+// applied by the sieve kernel.  A list that overflows its capacity is
+// detected by the sieve kernel, which then processes that segment's large
+// primes directly (correct, just slower).
+struct Run {             // a maximal run of window segments of one job
+  uint64_t k_lo, k_hi;   // wheel-slot range [k_lo, k_hi) of the run
+  uint32_t seg0;         // window-local index of the run's first segment
+  uint32_t nseg;
+};
+
 struct SieveParams {
   const Job* jobs;
   uint32_t njobs;
-  uint64_t nseg_total;
+  uint64_t nseg_total;   // segments of all jobs
+  uint64_t s_begin;      // this launch sieves segments [s_begin, s_begin + s_count)
+  uint64_t s_count;
   uint32_t S;                        // wheel slots per class per segment (power of two)
   const uint32_t* prime_p;           // sieving primes >= 37, ascending
   const unsigned long long* prime_m; // floor((2^64-1)/p), Barrett reciprocal
   uint32_t nprimes;
   uint32_t n_wc;                     // primes [0, n_wc) use the warp-cooperative loop
+  uint32_t n_mid;                    // primes [n_wc, n_mid) one thread per prime; [n_mid,
+                                     // nprimes) from buckets (or directly if bucket == null)
+  const uint32_t* bucket;            // window lists: bucket[(s - s_begin) * bcap + i]
+  uint32_t* bcount;                  // entries per window segment (reset after use)
+  uint32_t bcap;
   unsigned long long* ticket;        // dynamic segment counter (zeroed per launch)
   JobAcc* acc;                       // njobs accumulators (zeroed per launch)
   uint32_t* per_seg;                 // nullable, nseg_total counts
@@ -50,6 +69,24 @@ size_t sieve_smem_bytes(uint32_t S, int mode);
 // blocks_per_sm[mode] for the three modes
 cudaError_t sieve_configure(int* blocks_per_sm);
 cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st);
+
+struct FillParams {
+  const Run* runs;
+  uint32_t nruns;
+  const uint32_t* prime_p;
+  const unsigned long long* prime_m;
+  uint32_t p_begin, p_end;  // large primes [p_begin, p_end) of the table
+  uint32_t log2S;
+  uint32_t* bucket;
+  uint32_t* bcount;
+  uint32_t bcap;
+  uint32_t max_run_segs;    // histogram size (dynamic shared memory)
+};
+constexpr int kFillThreads = 256;
+constexpr int kFillPrimesPerThread = 4;
+constexpr int kFillPrimesPerBlock = kFillThreads * kFillPrimesPerThread;
+constexpr uint32_t kMaxWindow = 2048;  // segments per window (<= fill histogram size)
+cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st);
 
 // Level-0 base primes: all primes in [37, n] (n <= 65536 + 1) in one block.
 cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,

@@ -7,10 +7,11 @@
 //
 //   shared memory:  two uint32 bitmaps (6k+1 and 6k+5 classes), S/32 words each,
 //                   bit k of class c <-> value 6*(ks + k) + c (LSB-first, the
-//                   reference's bit layout, segment.hpp:46-50), stored with an
-//                   XOR row swizzle (word w at w ^ ((w >> 5) & 31)) so strided
-//                   clears by primes near multiples of 32 words do not pile
-//                   onto one bank.
+//                   reference's bit layout, segment.hpp:46-50).  Flags are
+//                   COMPOSITE bits (the complement of FlagArray), so crossing
+//                   off is one ATOMS.OR.  No bank swizzle: simulated and
+//                   measured conflicts of the strided loop are lower with the
+//                   natural layout (2.4-way vs 2.8-way for p in [37, 1024)).
 //   stamp:          primes 5..31 are never looped: their combined periodic
 //                   patterns (groups 5*7*11*13, 17*19*23, 29*31) live in
 //                   shared tables and each word is initialised by three
@@ -61,7 +62,13 @@ __device__ __forceinline__ uint32_t mod_barrett(uint64_t x, uint32_t p, uint64_t
   return static_cast<uint32_t>(r);
 }
 
-__device__ __forceinline__ uint32_t swz(uint32_t w) { return w ^ ((w >> 5) & 31u); }
+// 32-bit shared-window address of a shared-memory pointer
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void atom_or_shared(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 
 // bits [a, b) of a 32-bit word, a and b clamped to [0, 32]
 __device__ __forceinline__ uint32_t range_mask(int64_t a, int64_t b) {
@@ -139,9 +146,10 @@ __device__ __forceinline__ uint32_t end_valid(uint64_t ks, uint32_t c, uint64_t 
 }
 
 __device__ void fetch_segment(const SieveParams& P, SegInfo& si) {
-  const unsigned long long s = atomicAdd(P.ticket, 1ull);
-  si.s = s;
-  if (s >= P.nseg_total) return;
+  const unsigned long long t = atomicAdd(P.ticket, 1ull);
+  si.s = t < P.s_count ? P.s_begin + t : ~0ull;
+  if (t >= P.s_count) return;
+  const uint64_t s = si.s;
   uint32_t lo = 0, hi = P.njobs;  // last job with seg_begin <= s
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) / 2;
@@ -187,8 +195,8 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
     const int64_t base = 32 * static_cast<int64_t>(w);
     m1 &= range_mask(static_cast<int64_t>(si.lo1) - base, static_cast<int64_t>(si.hi1) - base);
     m5 &= range_mask(static_cast<int64_t>(si.lo5) - base, static_cast<int64_t>(si.hi5) - base);
-    bm1[swz(w)] = ~m1;
-    bm5[swz(w)] = ~m5;
+    bm1[w] = ~m1;
+    bm5[w] = ~m5;
   }
 }
 
@@ -213,22 +221,30 @@ __device__ __forceinline__ bool prime_offsets(uint32_t p, uint64_t m, uint64_t k
   return true;
 }
 
-__device__ __forceinline__ void mark(uint32_t* bm, uint32_t h) {
-  atomicOr(bm + swz(h >> 5), 1u << (h & 31u));
+// cross off bit h of the bitmap at shared address a0
+__device__ __forceinline__ void mark(uint32_t a0, uint32_t h) {
+  atom_or_shared(a0 + ((h >> 5) << 2), 1u << (h & 31u));
 }
 
 // Warp-cooperative strided marking of one class: lane l takes hits
 // h0 + l*p, h0 + (l+32)*p, ...  Consecutive hits of a lane are 32*p bits
-// apart, i.e. exactly p words, so the bit within the word is loop-invariant.
-__device__ __forceinline__ void mark_strided(uint32_t* bm, uint32_t h0, uint32_t p, uint32_t len,
+// apart, i.e. exactly p words, so the bit within the word is loop-invariant
+// and the loop only steps a shared byte address by 4p.
+__device__ __forceinline__ void mark_strided(uint32_t a0, uint32_t h0, uint32_t p, uint32_t len,
                                              uint32_t lane) {
   const uint32_t h = h0 + lane * p;
   if (h >= len) return;
   const uint32_t bit = 1u << (h & 31u);
-  const uint32_t wlim = (len - (h & 31u) + 31u) >> 5;  // words w with 32w + bit < len
-  uint32_t w = h >> 5;
-#pragma unroll 4
-  for (; w < wlim; w += p) atomicOr(bm + swz(w), bit);
+  const uint32_t alim = a0 + (((len - (h & 31u) + 31u) >> 5) << 2);
+  const uint32_t step = 4 * p;
+  uint32_t a = a0 + ((h >> 5) << 2);
+  for (; a + 3 * step < alim; a += 4 * step) {
+    atom_or_shared(a, bit);
+    atom_or_shared(a + step, bit);
+    atom_or_shared(a + 2 * step, bit);
+    atom_or_shared(a + 3 * step, bit);
+  }
+  for (; a < alim; a += step) atom_or_shared(a, bit);
 }
 
 // Phase 2: medium and large primes.
@@ -238,6 +254,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t len = si.len;
   const uint64_t ks = si.ks;
+  const uint32_t a1 = smem_addr(bm1), a5 = smem_addr(bm5);
   // warp-cooperative primes, handed out dynamically (largest work first)
   for (;;) {
     uint32_t i = 0;
@@ -247,38 +264,48 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     const uint32_t p = P.prime_p[i];
     uint32_t rel1, rel5;
     if (!prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5)) break;
-    mark_strided(bm1, rel1, p, len, lane);
-    mark_strided(bm5, rel5, p, len, lane);
+    mark_strided(a1, rel1, p, len, lane);
+    mark_strided(a5, rel5, p, len, lane);
   }
   // one thread per prime, in warp-sized chunks handed out dynamically; both
   // classes advance together (their hits are the same stride p apart)
+  // large primes come from the window's bucket list unless it overflowed
+  const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;
+  const uint32_t lp_end = use_bucket ? P.n_mid : P.nprimes;
   for (;;) {
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(lp_ctr, 32u);
     base = __shfl_sync(kFull, base, 0) + P.n_wc;
-    if (base >= P.nprimes) break;
+    if (base >= lp_end) break;
     const uint32_t i = base + lane;
     uint32_t p = 0, rel1 = 0, rel5 = 0;
     bool active = false;
-    if (i < P.nprimes) {
+    if (i < lp_end) {
       p = P.prime_p[i];
       active = prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5);
     }
     if (!__any_sync(kFull, active)) break;  // primes ascend: later chunks are inactive too
     if (!active) continue;
-    const bool one_first = rel1 <= rel5;
-    uint32_t* ba = one_first ? bm1 : bm5;
-    uint32_t* bb = one_first ? bm5 : bm1;
-    uint32_t h = one_first ? rel1 : rel5;
-    const uint32_t hb = one_first ? rel5 : rel1;
-    if (hb < len) {
-      const uint32_t d = hb - h;  // < p and < len
-      for (; h + d < len; h += p) {
-        mark(ba, h);
-        mark(bb, h + d);
-      }
+    // both classes share the stride: h5 = h1 + d with |d| < p
+    const int32_t d = static_cast<int32_t>(rel5 - rel1);
+    const uint32_t dpos = d > 0 ? static_cast<uint32_t>(d) : 0u;
+    uint32_t h = rel1;
+    for (; h + dpos < len; h += p) {
+      mark(a1, h);
+      mark(a5, h + d);
     }
-    for (; h < len; h += p) mark(ba, h);
+    if (h < len) mark(a1, h);
+    const uint32_t h5 = h + d;
+    if (d < 0 && h5 < len) mark(a5, h5);
+  }
+  if (use_bucket) {
+    const uint64_t ls = si.s - P.s_begin;
+    const uint32_t n = P.bcount[ls];
+    const uint32_t* list = P.bucket + ls * P.bcap;
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+      const uint32_t e = __ldcs(list + i);  // streamed once
+      mark((e >> 18) ? a5 : a1, e & 0x3FFFFu);
+    }
   }
 }
 
@@ -387,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
   __shared__ uint32_t red_n[kWarps];
   __shared__ uint32_t wc_ctr, lp_ctr;
   __shared__ unsigned long long seg_base;
+  __shared__ uint32_t seg_total;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 
   build_tables(tab);
@@ -398,11 +426,12 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
       lp_ctr = 0;
     }
     __syncthreads();
-    if (si.s >= P.nseg_total) break;
+    if (si.s == ~0ull) break;
     init_words(si, tab, bm1, bm5);
     __syncthreads();
     sieve_primes(P, si, bm1, bm5, &wc_ctr, &lp_ctr);
     __syncthreads();
+    if (P.bucket != nullptr && threadIdx.x == 0) P.bcount[si.s - P.s_begin] = 0;
 
     const uint64_t vbase = 6 * si.ks;
     if (MODE != kEnumerate) {
@@ -412,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
         const uint32_t m1 = ~bm1[wp], m5 = ~bm5[wp];
         cnt += __popc(m1) + __popc(m5);
         if (m1 | m5) {
-          const uint32_t w = swz(wp);  // logical word of this physical slot
+          const uint32_t w = wp;
           const unsigned long long wb = vbase + 192ull * w;
           const unsigned long long v1 = m1 ? wb + 6ull * (31 - __clz(m1)) + 1 : 0;
           const unsigned long long v5 = m5 ? wb + 6ull * (31 - __clz(m5)) + 5 : 0;
@@ -477,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
       const uint32_t w_end = warp == kWarps - 1 ? si.nwords : w_begin + wpw;
       uint32_t cnt = 0;
       for (uint32_t w = w_begin + lane; w < w_end; w += 32)
-        cnt += __popc(~bm1[swz(w)]) + __popc(~bm5[swz(w)]);
+        cnt += __popc(~bm1[w]) + __popc(~bm5[w]);
       cnt = __reduce_add_sync(kFull, cnt);
       if (lane == 0) red_n[warp] = cnt;
       __syncthreads();
@@ -489,20 +518,22 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
         const unsigned long long base = lookback(P.status, si.s, total);
         if (lane == 0) {
           seg_base = base;
+          seg_total = total;
           if (P.per_seg) P.per_seg[si.s] = total;
           if (total) atomicAdd(&P.acc[si.job].count, static_cast<unsigned long long>(total));
         }
       }
       __syncthreads();
       unsigned long long pos = seg_base + red_n[warp];
+      const bool seg_fits = seg_base + seg_total <= P.out_cap;
       unsigned long long sum = 0, xr = 0, lg = 0;
       uint16_t* stage = stage_all + warp * kStage;
       for (uint32_t w0 = w_begin; w0 < w_end; w0 += 32) {
         const uint32_t w = w0 + lane;
         uint32_t a = 0, b = 0;
         if (w < w_end) {
-          a = ~bm1[swz(w)];
-          b = ~bm5[swz(w)];
+          a = ~bm1[w];
+          b = ~bm5[w];
         }
         // ascending value order interleaves the classes: bit 2j <- 6k+1, 2j+1 <- 6k+5
         const uint32_t lo = spread16(a) | (spread16(b) << 1);
@@ -523,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
           // 2) coalesced: lane i writes survivors i, i+32, ... of the round
           unsigned long long* dst = P.out + pos;
           uint32_t soff = 0, n = 0;
-          if (pos + rtotal <= P.out_cap) {
+          if (seg_fits) {
 #pragma unroll 4
             for (uint32_t i = lane; i < rtotal; i += 32) {
               const uint32_t e = stage[i];
@@ -593,6 +624,66 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Large-prime bucket fill.  blockIdx.y = run, blockIdx.x = chunk of
+// kFillThreads * kFillPrimesPerThread primes.  Two passes over the same hits:
+// (1) per-segment histogram in shared memory, (2) one global atomicAdd per
+// (block, segment) reserves a contiguous slice of that segment's list, then
+// every hit is written into it.  First hits use the same Barrett offsets and
+// p*p activation rule as the sieve kernel.
+template <bool kWrite>
+__device__ __forceinline__ void fill_pass(const FillParams& F, const Run& run, uint32_t* hist) {
+  const uint32_t S = 1u << F.log2S;
+  const uint32_t first = F.p_begin + blockIdx.x * (kFillThreads * kFillPrimesPerThread);
+#pragma unroll 1
+  for (int j = 0; j < kFillPrimesPerThread; ++j) {
+    const uint32_t i = first + j * kFillThreads + threadIdx.x;
+    if (i >= F.p_end) break;
+    const uint32_t p = F.prime_p[i];
+    const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;
+    if (ksq >= run.k_hi) break;  // inactive here, and so is every later prime
+    const uint32_t t1 = target1(p), t5 = target5(p);
+    uint64_t k1, k5;
+    if (ksq >= run.k_lo) {
+      k1 = ksq;
+      k5 = ksq + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
+    } else {
+      const uint32_t r = mod_barrett(run.k_lo, p, F.prime_m[i]);
+      k1 = run.k_lo + (t1 >= r ? t1 - r : t1 + p - r);
+      k5 = run.k_lo + (t5 >= r ? t5 - r : t5 + p - r);
+    }
+    for (int c = 0; c < 2; ++c) {
+      for (uint64_t k = c ? k5 : k1; k < run.k_hi; k += p) {
+        const uint32_t rel = static_cast<uint32_t>(k - run.k_lo);
+        const uint32_t seg = rel >> F.log2S;
+        if (!kWrite) {
+          atomicAdd(hist + seg, 1u);
+        } else {
+          const uint32_t pos = atomicAdd(hist + seg, 1u);
+          if (pos < F.bcap)
+            F.bucket[static_cast<uint64_t>(run.seg0 + seg) * F.bcap + pos] =
+                (rel & (S - 1)) | (static_cast<uint32_t>(c) << 18);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillParams F) {
+  extern __shared__ uint32_t hist[];  // max_run_segs counters
+  const Run run = F.runs[blockIdx.y];
+  for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) hist[i] = 0;
+  __syncthreads();
+  fill_pass<false>(F, run, hist);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) {
+    const uint32_t c = hist[i];
+    hist[i] = c ? atomicAdd(F.bcount + run.seg0 + i, c) : 0u;  // slice start
+  }
+  __syncthreads();
+  fill_pass<true>(F, run, hist);
 }
 
 // ---------------------------------------------------------------------------
@@ -680,6 +771,15 @@ cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t 
     case kCountChecks: sieve_kernel<kCountChecks><<<grid, kThreads, smem, st>>>(p); break;
     default: sieve_kernel<kEnumerate><<<grid, kThreads, smem, st>>>(p); break;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st) {
+  const uint32_t per_block = kFillThreads * kFillPrimesPerThread;
+  const uint32_t nb = (f.p_end - f.p_begin + per_block - 1) / per_block;
+  if (nb == 0 || f.nruns == 0) return cudaSuccess;
+  dim3 grid(nb, f.nruns);
+  bucket_fill_kernel<<<grid, kFillThreads, f.max_run_segs * sizeof(uint32_t), st>>>(f);
   return cudaGetLastError();
 }
 

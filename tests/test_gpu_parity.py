@@ -156,3 +156,45 @@ def test_device_per_segment_and_timing(sieve):
     assert int(ps.sum().item()) + 2 == c.count
     t = sieve.timing()
     assert t.sieve_ms > 0 and t.segments == nseg and t.launches >= 1
+
+
+def _run_isolated(code, env):
+    """Run `code` in a fresh interpreter (the bucket knobs are read when a
+    context is created)."""
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=e, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return r.stdout
+
+
+BUCKET_CODE = r"""
+import sys, json
+sys.path.insert(0, '.')
+import numpy as np
+import paper_2310_17746_b200 as ws
+from oracle.oracle import Port
+port = Port()
+s = ws.Sieve()
+out = []
+for L, R in [(10**15, 10**15 + 3 * 10**7), (2**43 - 10**6, 2**43 + 2**24), (10**12 - 7, 10**12 + 4 * 10**7 + 1)]:
+    c, ps = s.count_range(L, R, checks=True, per_seg=True)
+    r = port.range(L, R, per_seg=True)
+    assert (c.count, c.sum, c.xor, c.largest) == (r["count"], r["sum"], r["xor"], r["largest"]), (L, R)
+    assert np.array_equal(ps, r["per_seg"]), (L, R)
+    v, n, ce = s.enumerate_range(L, R)
+    assert n == r["count"] and ce.sum == r["sum"]
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"WHEELSIEVE_BUCKET_BUDGET": str(1 << 20), "WHEELSIEVE_BUCKET_RATIO": "1"},
+                                 {"WHEELSIEVE_BUCKET_CAP": "64", "WHEELSIEVE_BUCKET_RATIO": "1"},
+                                 {"WHEELSIEVE_FILL_PIECE": "3", "WHEELSIEVE_BUCKET_RATIO": "1"},
+                                 {}])
+def test_bucket_windows_and_overflow(env):
+    assert "ok" in _run_isolated(BUCKET_CODE, env)
