@@ -316,11 +316,16 @@ def run_ours(args, cfg, world, rank, local):
     props = torch.cuda.get_device_properties(local)
     avg_sieve_ms = float(np.mean(sieve_ms))
     clocks = clk.summary()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.config, {}).get("traffic_bytes_per_launch")
     if kind == "enumerate":
         alg = 8.0 * units_local
         achieved = alg / (avg_sieve_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                 "kernel": "sieve_kernel<kEnumerate>",
                 "algorithmic_bytes_per_launch": alg,
                 "avg_launch_ms": avg_sieve_ms,
@@ -337,6 +342,7 @@ def run_ours(args, cfg, world, rank, local):
     sach = b_smem / (avg_sieve_ms / 1e3) / 1e9
     roof_smem = {"bound": "smem", "achieved": sach, "peak": speak, "unit": "GB/s",
                  "frac": sach / speak, "algorithmic_bytes_per_launch": b_smem,
+                 "traffic": traffic if kind != "enumerate" else None,
                  "avg_launch_ms": avg_sieve_ms,
                  "peak_source": f"{props.multi_processor_count} SMs x 128 B/clk x {smax} MHz"}
     if roof is None:

@@ -102,8 +102,10 @@ struct ws_ctx {
   uint32_t bucket_min_ratio = 8;       // buckets iff largest base prime >= ratio * S
 
   // scratch
-  DevBuf<uint32_t> bucket;
-  DevBuf<uint32_t> bcount;
+  DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)
+  DevBuf<uint32_t> bcount[2];
+  cudaStream_t fstream = nullptr;  // bucket-fill stream
+  cudaEvent_t fill_done[2] = {}, sieve_done[2] = {};
   DevBuf<wsk::Run> runs;
   DevBuf<wsk::Job> jobs;
   DevBuf<wsk::JobAcc> acc;
@@ -118,8 +120,14 @@ struct ws_ctx {
 
   ~ws_ctx() {
     cudaSetDevice(device);
-    for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n, &bucket, &bcount}) b->release();
+    for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n, &bucket[0], &bucket[1], &bcount[0], &bcount[1]})
+      b->release();
     runs.release();
+    for (int i = 0; i < 2; ++i) {
+      if (fill_done[i]) cudaEventDestroy(fill_done[i]);
+      if (sieve_done[i]) cudaEventDestroy(sieve_done[i]);
+    }
+    if (fstream) cudaStreamDestroy(fstream);
     for (auto* b : {&tab_m, &ticket, &status, &vals, &l0_m}) b->release();
     jobs.release();
     acc.release();
@@ -231,9 +239,11 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     if (c->cap_override) cap = c->cap_override;
     W = std::max<uint64_t>(8, c->bucket_budget / (4ull * cap));
     W = std::min<uint64_t>({W, wsk::kMaxWindow, nseg});
-    c->bucket.reserve(W * cap, "bucket lists");
-    c->bcount.reserve(W, "bucket counts");
-    ck(cudaMemsetAsync(c->bcount.ptr, 0, W * sizeof(uint32_t), c->stream), "zero bcount");
+    for (int b = 0; b < 2; ++b) {
+      c->bucket[b].reserve(W * cap, "bucket lists");
+      c->bcount[b].reserve(W, "bucket counts");
+      ck(cudaMemsetAsync(c->bcount[b].ptr, 0, W * sizeof(uint32_t), c->stream), "zero bcount");
+    }
   }
   const uint64_t nwin = (nseg + W - 1) / W;
   c->ticket.reserve(nwin, "tickets");
@@ -244,9 +254,9 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   std::vector<uint32_t> run_off(nwin + 1, 0);
   uint64_t piece = W;
   if (buckets) {
-    // runs are cut into 64-segment pieces: short per-thread hit loops and a
+    // runs are cut into 32-segment pieces: short per-thread hit loops and a
     // fill grid that covers the GPU (measured best for c4 and c5)
-    piece = c->piece_override ? c->piece_override : 64;
+    piece = c->piece_override ? c->piece_override : 32;
     piece = std::min<uint64_t>(piece, W);
     size_t j = 0;
     for (uint64_t w = 0; w < nwin; ++w) {
@@ -274,10 +284,16 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
                        cudaMemcpyHostToDevice, c->stream), "upload runs");
     ck(cudaStreamSynchronize(c->stream), "sync runs");  // `runs` is pageable and local
   }
-  if (timed) ck(cudaEventRecord(c->ev[2], c->stream), "event");
+  // ev[2] also orders the fill stream after everything queued so far
+  ck(cudaEventRecord(c->ev[2], c->stream), "event");
+  if (buckets) ck(cudaStreamWaitEvent(c->fstream, c->ev[2], 0), "fill wait");
   for (uint64_t w = 0; w < nwin; ++w) {
     const uint64_t ws = w * W, we = std::min(nseg, ws + W);
+    const int b = static_cast<int>(w & 1);
     if (buckets) {
+      // fill window w into buffer b on the fill stream, once the sieve of
+      // window w-2 has released it; it overlaps the sieve of window w-1
+      if (w >= 2) ck(cudaStreamWaitEvent(c->fstream, c->sieve_done[b], 0), "fill wait");
       wsk::FillParams f{};
       f.runs = c->runs.ptr + run_off[w];
       f.nruns = run_off[w + 1] - run_off[w];
@@ -286,14 +302,16 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
       f.p_begin = p.n_mid;
       f.p_end = c->nprimes;
       f.log2S = static_cast<uint32_t>(__builtin_ctz(c->S));
-      f.bucket = c->bucket.ptr;
-      f.bcount = c->bcount.ptr;
+      f.bucket = c->bucket[b].ptr;
+      f.bcount = c->bcount[b].ptr;
       f.bcap = cap;
       f.max_run_segs = static_cast<uint32_t>(piece);
-      ck(wsk::launch_bucket_fill(f, c->stream), "bucket fill");
+      ck(wsk::launch_bucket_fill(f, c->fstream), "bucket fill");
+      ck(cudaEventRecord(c->fill_done[b], c->fstream), "event");
+      ck(cudaStreamWaitEvent(c->stream, c->fill_done[b], 0), "sieve wait");
       c->timing.launches += 1;
-      p.bucket = c->bucket.ptr;
-      p.bcount = c->bcount.ptr;
+      p.bucket = c->bucket[b].ptr;
+      p.bcount = c->bcount[b].ptr;
       p.bcap = cap;
     }
     p.s_begin = ws;
@@ -301,9 +319,11 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     p.ticket = c->ticket.ptr + w;
     const int grid = static_cast<int>(std::min<uint64_t>(we - ws, max_grid));
     ck(wsk::launch_sieve(mode, p, grid, c->stream), "sieve launch");
+    if (buckets) ck(cudaEventRecord(c->sieve_done[b], c->stream), "event");
     c->timing.launches += 1;
   }
-  if (timed) ck(cudaEventRecord(c->ev[3], c->stream), "event");
+  (void)timed;
+  ck(cudaEventRecord(c->ev[3], c->stream), "event");
   c->timing.segments += nseg;
 }
 
@@ -499,6 +519,14 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
       delete c;
       return WS_CUDA;
     }
+  bool ok = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking) == cudaSuccess;
+  for (int i = 0; i < 2 && ok; ++i)
+    ok = cudaEventCreateWithFlags(&c->fill_done[i], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->sieve_done[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    delete c;
+    return WS_CUDA;
+  }
   *out = c;
   return WS_OK;
 }

@@ -83,7 +83,7 @@ struct FillParams {
   uint32_t max_run_segs;    // histogram size (dynamic shared memory)
 };
 constexpr int kFillThreads = 256;
-constexpr int kFillPrimesPerThread = 4;
+constexpr int kFillPrimesPerThread = 16;
 constexpr int kFillPrimesPerBlock = kFillThreads * kFillPrimesPerThread;
 constexpr uint32_t kMaxWindow = 2048;  // segments per window (<= fill histogram size)
 cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st);

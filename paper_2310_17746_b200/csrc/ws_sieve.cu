@@ -132,7 +132,18 @@ struct SegInfo {
   uint32_t len;    // slots in this segment
   uint32_t lo1, hi1, lo5, hi5;  // valid slot bounds per class
   uint32_t nwords; // words per class actually used (ceil(len / 32), rounded to 32)
+  uint32_t t_lo;   // primes p <= t_lo: p*p below the segment (no activation)
+  uint32_t t_hi;   // primes p > t_hi: p*p beyond the segment (inactive)
 };
+
+// floor(sqrt(n)) for 64-bit n, saturated to 2^32 - 1
+__device__ __forceinline__ uint32_t isqrt64(uint64_t n) {
+  uint64_t r = static_cast<uint64_t>(sqrt(static_cast<double>(n)));
+  if (r > 0xFFFFFFFFull) r = 0xFFFFFFFFull;
+  while (r * r > n) --r;
+  while (r < 0xFFFFFFFFull && (r + 1) * (r + 1) <= n) ++r;
+  return static_cast<uint32_t>(r);
+}
 
 __device__ __forceinline__ uint32_t first_valid(uint64_t ks, uint32_t c, uint64_t L) {
   const uint64_t v0 = 6 * ks + c;
@@ -167,6 +178,10 @@ __device__ void fetch_segment(const SieveParams& P, SegInfo& si) {
   si.hi1 = end_valid(si.ks, 1, J.R, si.len);
   si.hi5 = end_valid(si.ks, 5, J.R, si.len);
   si.nwords = ((si.len + 1023u) / 1024u) * 32u;
+  // activation thresholds: p*p = 6*ksq + 1 is at or past slot ks iff
+  // p > isqrt(6 ks), and before the segment end iff p <= isqrt(6 (ks + len))
+  si.t_lo = isqrt64(6 * si.ks);
+  si.t_hi = isqrt64(6 * (si.ks + si.len));
 }
 
 // Phase 1: stamp primes 5..31 and the [L, R) trim into every word.  The
@@ -203,14 +218,18 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
 // First hits (segment-relative) of prime p in both classes, or false when
 // p is not yet active in this segment (p*p beyond its end; since primes
 // ascend, no later prime is active either).
-__device__ __forceinline__ bool prime_offsets(uint32_t p, uint64_t m, uint64_t ks, uint32_t len,
-                                              uint32_t& rel1, uint32_t& rel5) {
-  const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;  // p*p = 6*ksq + 1
-  if (ksq >= ks + len) return false;
+// First hits (segment-relative) of prime p in both classes, or false when
+// p is not yet active in this segment (p*p beyond its end; since primes
+// ascend, no later prime is active either).  The activation test is two
+// 32-bit compares against the segment's thresholds.
+__device__ __forceinline__ bool prime_offsets(uint32_t p, uint64_t m, uint64_t ks, uint32_t t_lo,
+                                              uint32_t t_hi, uint32_t& rel1, uint32_t& rel5) {
+  if (p > t_hi) return false;
   const uint32_t t1 = target1(p), t5 = target5(p);
-  if (ksq >= ks) {
+  if (p > t_lo) {
     // activation segment: class 1 starts exactly at p*p, class 5 at the
     // first multiple above it (anchor p*(p-1), segment.cpp:182)
+    const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;
     rel1 = static_cast<uint32_t>(ksq - ks);
     rel5 = rel1 + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
   } else {
@@ -249,12 +268,12 @@ __device__ __forceinline__ void mark_strided(uint32_t a0, uint32_t h0, uint32_t 
 
 // Phase 2: medium and large primes.
 __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo& si,
-                                             uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr,
-                                             uint32_t* lp_ctr) {
+                                             uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t len = si.len;
   const uint64_t ks = si.ks;
   const uint32_t a1 = smem_addr(bm1), a5 = smem_addr(bm5);
+  const uint32_t t_lo = si.t_lo, t_hi = si.t_hi;
   // warp-cooperative primes, handed out dynamically (largest work first)
   for (;;) {
     uint32_t i = 0;
@@ -263,30 +282,24 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     if (i >= P.n_wc) break;
     const uint32_t p = P.prime_p[i];
     uint32_t rel1, rel5;
-    if (!prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5)) break;
+    if (!prime_offsets(p, P.prime_m[i], ks, t_lo, t_hi, rel1, rel5)) break;
     mark_strided(a1, rel1, p, len, lane);
     mark_strided(a5, rel5, p, len, lane);
   }
-  // one thread per prime, in warp-sized chunks handed out dynamically; both
-  // classes advance together (their hits are the same stride p apart)
   // large primes come from the window's bucket list unless it overflowed
   const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;
   const uint32_t lp_end = use_bucket ? P.n_mid : P.nprimes;
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(lp_ctr, 32u);
-    base = __shfl_sync(kFull, base, 0) + P.n_wc;
-    if (base >= lp_end) break;
+  const uint32_t warp = threadIdx.x >> 5;
+  // p < S: one thread per prime, static warp-sized chunks; both classes
+  // advance together (their hits are the same stride p apart)
+  const uint32_t mid_end = P.n_mid < lp_end ? P.n_mid : lp_end;
+  for (uint32_t base = P.n_wc + 32 * warp; base < mid_end; base += 32 * kWarps) {
+    if (P.prime_p[base] > t_hi) break;  // primes ascend: the rest is inactive
     const uint32_t i = base + lane;
-    uint32_t p = 0, rel1 = 0, rel5 = 0;
-    bool active = false;
-    if (i < lp_end) {
-      p = P.prime_p[i];
-      active = prime_offsets(p, P.prime_m[i], ks, len, rel1, rel5);
-    }
-    if (!__any_sync(kFull, active)) break;  // primes ascend: later chunks are inactive too
-    if (!active) continue;
-    // both classes share the stride: h5 = h1 + d with |d| < p
+    if (i >= mid_end) continue;
+    const uint32_t p = P.prime_p[i];
+    uint32_t rel1, rel5;
+    if (!prime_offsets(p, P.prime_m[i], ks, t_lo, t_hi, rel1, rel5)) continue;
     const int32_t d = static_cast<int32_t>(rel5 - rel1);
     const uint32_t dpos = d > 0 ? static_cast<uint32_t>(d) : 0u;
     uint32_t h = rel1;
@@ -298,12 +311,32 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     const uint32_t h5 = h + d;
     if (d < 0 && h5 < len) mark(a5, h5);
   }
+  // p >= S (no bucket list): at most one hit per class, no loop
+  for (uint32_t base = mid_end + 32 * warp; base < lp_end; base += 32 * kWarps) {
+    if (P.prime_p[base] > t_hi) break;
+    const uint32_t i = base + lane;
+    if (i >= lp_end) continue;
+    const uint32_t p = P.prime_p[i];
+    uint32_t rel1, rel5;
+    if (!prime_offsets(p, P.prime_m[i], ks, t_lo, t_hi, rel1, rel5)) continue;
+    if (rel1 < len) mark(a1, rel1);
+    if (rel5 < len) mark(a5, rel5);
+  }
   if (use_bucket) {
     const uint64_t ls = si.s - P.s_begin;
     const uint32_t n = P.bcount[ls];
     const uint32_t* list = P.bucket + ls * P.bcap;
-    for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
-      const uint32_t e = __ldcs(list + i);  // streamed once
+    uint32_t i = threadIdx.x;
+    for (; i + 3 * kThreads < n; i += 4 * kThreads) {  // 4 streamed loads in flight
+      const uint32_t e0 = __ldcs(list + i), e1 = __ldcs(list + i + kThreads);
+      const uint32_t e2 = __ldcs(list + i + 2 * kThreads), e3 = __ldcs(list + i + 3 * kThreads);
+      mark((e0 >> 18) ? a5 : a1, e0 & 0x3FFFFu);
+      mark((e1 >> 18) ? a5 : a1, e1 & 0x3FFFFu);
+      mark((e2 >> 18) ? a5 : a1, e2 & 0x3FFFFu);
+      mark((e3 >> 18) ? a5 : a1, e3 & 0x3FFFFu);
+    }
+    for (; i < n; i += kThreads) {
+      const uint32_t e = __ldcs(list + i);
       mark((e >> 18) ? a5 : a1, e & 0x3FFFFu);
     }
   }
@@ -403,7 +436,7 @@ constexpr size_t mode_smem_extra() {
 
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P) {
+__global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_kernel(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bm1 = smem;
   uint32_t* bm5 = smem + P.S / 32;
@@ -412,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
   __shared__ SegInfo si;
   __shared__ unsigned long long red_a[kWarps], red_b[kWarps], red_c[kWarps];
   __shared__ uint32_t red_n[kWarps];
-  __shared__ uint32_t wc_ctr, lp_ctr;
+  __shared__ uint32_t wc_ctr;
   __shared__ unsigned long long seg_base;
   __shared__ uint32_t seg_total;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -423,13 +456,12 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
     if (threadIdx.x == 0) {
       fetch_segment(P, si);
       wc_ctr = 0;
-      lp_ctr = 0;
     }
     __syncthreads();
     if (si.s == ~0ull) break;
     init_words(si, tab, bm1, bm5);
     __syncthreads();
-    sieve_primes(P, si, bm1, bm5, &wc_ctr, &lp_ctr);
+    sieve_primes(P, si, bm1, bm5, &wc_ctr);
     __syncthreads();
     if (P.bucket != nullptr && threadIdx.x == 0) P.bcount[si.s - P.s_begin] = 0;
 
@@ -633,57 +665,64 @@ __global__ void __launch_bounds__(kThreads, 2) sieve_kernel(const SieveParams P)
 // (block, segment) reserves a contiguous slice of that segment's list, then
 // every hit is written into it.  First hits use the same Barrett offsets and
 // p*p activation rule as the sieve kernel.
-template <bool kWrite>
-__device__ __forceinline__ void fill_pass(const FillParams& F, const Run& run, uint32_t* hist) {
+__global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillParams F) {
+  extern __shared__ uint32_t fill_smem[];
+  uint32_t* hist = fill_smem;                       // max_run_segs counters
+  uint32_t* first1 = fill_smem + F.max_run_segs;    // per prime: first hit (run-relative)
+  uint32_t* first5 = first1 + kFillPrimesPerBlock;  // UINT32_MAX = no hit in this run
+  const Run run = F.runs[blockIdx.y];
   const uint32_t S = 1u << F.log2S;
-  const uint32_t first = F.p_begin + blockIdx.x * (kFillThreads * kFillPrimesPerThread);
+  const uint32_t span = static_cast<uint32_t>(run.k_hi - run.k_lo);  // <= kMaxWindow * S
+  // activation thresholds of the run (see fetch_segment)
+  const uint32_t t_lo = isqrt64(6 * run.k_lo), t_hi = isqrt64(6 * run.k_hi);
+  for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) hist[i] = 0;
+  __syncthreads();
+  const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
+  // pass 1: first hits (Barrett, p*p activation) + per-segment histogram
 #pragma unroll 1
   for (int j = 0; j < kFillPrimesPerThread; ++j) {
-    const uint32_t i = first + j * kFillThreads + threadIdx.x;
-    if (i >= F.p_end) break;
-    const uint32_t p = F.prime_p[i];
-    const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;
-    if (ksq >= run.k_hi) break;  // inactive here, and so is every later prime
-    const uint32_t t1 = target1(p), t5 = target5(p);
-    uint64_t k1, k5;
-    if (ksq >= run.k_lo) {
-      k1 = ksq;
-      k5 = ksq + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
-    } else {
-      const uint32_t r = mod_barrett(run.k_lo, p, F.prime_m[i]);
-      k1 = run.k_lo + (t1 >= r ? t1 - r : t1 + p - r);
-      k5 = run.k_lo + (t5 >= r ? t5 - r : t5 + p - r);
+    const uint32_t li = j * kFillThreads + threadIdx.x;
+    const uint32_t i = first + li;
+    uint32_t r1 = 0xFFFFFFFFu, r5 = 0xFFFFFFFFu;
+    if (i < F.p_end) {
+      const uint32_t p = F.prime_p[i];
+      uint32_t q1, q5;
+      if (prime_offsets(p, F.prime_m[i], run.k_lo, t_lo, t_hi, q1, q5)) {
+        if (q1 < span) r1 = q1;
+        if (q5 < span) r5 = q5;
+        for (uint32_t h = r1; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+        for (uint32_t h = r5; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+      }
     }
+    first1[li] = r1;
+    first5[li] = r5;
+  }
+  __syncthreads();
+  // reserve one contiguous slice per (block, segment)
+  for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) {
+    const uint32_t c = hist[i];
+    hist[i] = c ? atomicAdd(F.bcount + run.seg0 + i, c) : 0u;
+  }
+  __syncthreads();
+  // pass 2: write the entries
+#pragma unroll 1
+  for (int j = 0; j < kFillPrimesPerThread; ++j) {
+    const uint32_t li = j * kFillThreads + threadIdx.x;
+    const uint32_t i = first + li;
+    if (i >= F.p_end) break;
+    const uint32_t r1 = first1[li], r5 = first5[li];
+    if (r1 == 0xFFFFFFFFu && r5 == 0xFFFFFFFFu) continue;
+    const uint32_t p = F.prime_p[i];
     for (int c = 0; c < 2; ++c) {
-      for (uint64_t k = c ? k5 : k1; k < run.k_hi; k += p) {
-        const uint32_t rel = static_cast<uint32_t>(k - run.k_lo);
-        const uint32_t seg = rel >> F.log2S;
-        if (!kWrite) {
-          atomicAdd(hist + seg, 1u);
-        } else {
-          const uint32_t pos = atomicAdd(hist + seg, 1u);
-          if (pos < F.bcap)
-            F.bucket[static_cast<uint64_t>(run.seg0 + seg) * F.bcap + pos] =
-                (rel & (S - 1)) | (static_cast<uint32_t>(c) << 18);
-        }
+      for (uint32_t h = c ? r5 : r1; h < span; h += p) {
+        const uint32_t seg = h >> F.log2S;
+        const uint32_t pos = atomicAdd(hist + seg, 1u);
+        if (pos < F.bcap)
+          F.bucket[static_cast<uint64_t>(run.seg0 + seg) * F.bcap + pos] =
+              (h & (S - 1)) | (static_cast<uint32_t>(c) << 18);
       }
     }
   }
-}
-
-__global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillParams F) {
-  extern __shared__ uint32_t hist[];  // max_run_segs counters
-  const Run run = F.runs[blockIdx.y];
-  for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) hist[i] = 0;
-  __syncthreads();
-  fill_pass<false>(F, run, hist);
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) {
-    const uint32_t c = hist[i];
-    hist[i] = c ? atomicAdd(F.bcount + run.seg0 + i, c) : 0u;  // slice start
-  }
-  __syncthreads();
-  fill_pass<true>(F, run, hist);
 }
 
 // ---------------------------------------------------------------------------
@@ -779,7 +818,8 @@ cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st) {
   const uint32_t nb = (f.p_end - f.p_begin + per_block - 1) / per_block;
   if (nb == 0 || f.nruns == 0) return cudaSuccess;
   dim3 grid(nb, f.nruns);
-  bucket_fill_kernel<<<grid, kFillThreads, f.max_run_segs * sizeof(uint32_t), st>>>(f);
+  const size_t smem = (f.max_run_segs + 2 * kFillPrimesPerBlock) * sizeof(uint32_t);
+  bucket_fill_kernel<<<grid, kFillThreads, smem, st>>>(f);
   return cudaGetLastError();
 }
 
