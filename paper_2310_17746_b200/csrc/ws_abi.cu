@@ -96,6 +96,7 @@ struct ws_ctx {
   DevBuf<unsigned long long> tab_m;
 
   uint32_t n_below_S = 0;  // table primes (>= 37) below S: in-kernel; the rest bucketed
+  uint32_t n_wc = 161;     // table primes below the warp-cooperative limit (1024)
   size_t bucket_budget = 1ull << 30;  // bytes of bucket lists per window
   uint32_t cap_override = 0;           // test knob (WHEELSIEVE_BUCKET_CAP)
   uint32_t piece_override = 0;         // tuning knob (WHEELSIEVE_FILL_PIECE)
@@ -217,7 +218,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.nprimes = c->nprimes;
   // warp-cooperative loop for primes below 1024 (>= 256 hits per class per
   // 2^18-slot segment): 161 table entries; one thread per prime above
-  p.n_wc = std::min<uint32_t>(161, c->nprimes);
+  p.n_wc = std::min<uint32_t>(c->n_wc, c->nprimes);
   p.n_mid = std::min<uint32_t>(std::max(c->n_below_S, p.n_wc), c->nprimes);
   p.acc = c->acc.ptr;
   p.per_seg = per_seg_dev;
@@ -491,15 +492,21 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   if (!c) return WS_OUT_OF_MEMORY;
   c->device = dev;
   c->S = S;
-  {  // primes in [37, S): the in-kernel share of the table
-    std::vector<uint8_t> comp(S, 0);
-    uint32_t n = 0;
-    for (uint32_t i = 2; i < S; ++i) {
+  {  // primes in [37, S): the in-kernel share of the table; and the warp-
+     // cooperative share [37, wc_limit)
+    uint32_t wc_limit = 1024;
+    if (const char* e = std::getenv("WHEELSIEVE_WC_LIMIT")) wc_limit = std::strtoul(e, nullptr, 10);
+    const uint32_t n_max = std::max(S, wc_limit);
+    std::vector<uint8_t> comp(n_max, 0);
+    uint32_t n = 0, nw = 0;
+    for (uint32_t i = 2; i < n_max; ++i) {
       if (comp[i]) continue;
-      if (i >= wsk::kFirstTablePrime) ++n;
-      for (uint64_t j = static_cast<uint64_t>(i) * i; j < S; j += i) comp[j] = 1;
+      if (i >= wsk::kFirstTablePrime && i < S) ++n;
+      if (i >= wsk::kFirstTablePrime && i < wc_limit) ++nw;
+      for (uint64_t j = static_cast<uint64_t>(i) * i; j < n_max; j += i) comp[j] = 1;
     }
     c->n_below_S = n;
+    c->n_wc = nw;
   }
   // test / tuning knobs: bucket-list capacity per segment and window budget
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CAP")) c->cap_override = std::strtoul(e, nullptr, 10);

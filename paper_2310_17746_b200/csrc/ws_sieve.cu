@@ -577,11 +577,12 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
         if (rtotal == 0) continue;
         if (rtotal <= kStage) {
           // 1) each lane drops its survivor positions (64*lane + bit) into the stage
-          uint32_t o = incl - c;
+          uint16_t* sp = stage + (incl - c);
           const uint32_t eb = lane << 6;
-          for (uint32_t x = lo; x; x &= x - 1) stage[o++] = static_cast<uint16_t>(eb | (__ffs(x) - 1));
-          for (uint32_t x = hi; x; x &= x - 1)
-            stage[o++] = static_cast<uint16_t>(eb | 32u | (__ffs(x) - 1));
+#pragma unroll 1
+          for (uint32_t x = lo; x; x &= x - 1) *sp++ = static_cast<uint16_t>(eb | (__ffs(x) - 1));
+#pragma unroll 1
+          for (uint32_t x = hi; x; x &= x - 1) *sp++ = static_cast<uint16_t>(eb | 31u + __ffs(x));
           __syncwarp();
           // 2) coalesced: lane i writes survivors i, i+32, ... of the round
           unsigned long long* dst = P.out + pos;
@@ -690,8 +691,10 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
       if (prime_offsets(p, F.prime_m[i], run.k_lo, t_lo, t_hi, q1, q5)) {
         if (q1 < span) r1 = q1;
         if (q5 < span) r5 = q5;
-        for (uint32_t h = r1; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
-        for (uint32_t h = r5; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+        // 64-bit stepping: p can be within `span` of 2^32 near the top of
+        // the 64-bit value range, where a 32-bit h + p would wrap
+        for (uint64_t h = r1; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+        for (uint64_t h = r5; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
       }
     }
     first1[li] = r1;
@@ -714,12 +717,12 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
     if (r1 == 0xFFFFFFFFu && r5 == 0xFFFFFFFFu) continue;
     const uint32_t p = F.prime_p[i];
     for (int c = 0; c < 2; ++c) {
-      for (uint32_t h = c ? r5 : r1; h < span; h += p) {
-        const uint32_t seg = h >> F.log2S;
+      for (uint64_t h = c ? r5 : r1; h < span; h += p) {
+        const uint32_t seg = static_cast<uint32_t>(h >> F.log2S);
         const uint32_t pos = atomicAdd(hist + seg, 1u);
         if (pos < F.bcap)
           F.bucket[static_cast<uint64_t>(run.seg0 + seg) * F.bcap + pos] =
-              (h & (S - 1)) | (static_cast<uint32_t>(c) << 18);
+              (static_cast<uint32_t>(h) & (S - 1)) | (static_cast<uint32_t>(c) << 18);
       }
     }
   }

@@ -198,3 +198,41 @@ print("ok")
                                  {}])
 def test_bucket_windows_and_overflow(env):
     assert "ok" in _run_isolated(BUCKET_CODE, env)
+
+
+def _is_prime_mr(n):
+    """Deterministic Miller-Rabin for n < 3.3e24 (independent checker for
+    ranges above the reference's 1e16 naive-sieve cap, wheel.hpp:40)."""
+    if n < 2:
+        return False
+    for p in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        if n % p == 0:
+            return n == p
+    d, s = n - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        s += 1
+    for a in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        x = pow(a, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(s - 1):
+            x = x * x % n
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
+
+
+@pytest.mark.parametrize("L,W", [(10**18, 40_000), (2**63 - 20_000, 40_000),
+                                 (18446744073709551612 - 30_000, 30_000)])
+def test_top_of_64bit_range_vs_miller_rabin(sieve, L, W):
+    R = L + W
+    vals, n, c = sieve.enumerate_range(L, R)
+    expected = [v for v in range(L | 1, R, 2) if v % 3 and _is_prime_mr(v)]
+    assert [int(x) for x in vals] == expected
+    cc = sieve.count_range(L, R, checks=True)
+    assert cc.count == len(expected) == n
+    assert cc.sum == sum(expected) % 2**64 and cc.xor == c.xor
+    assert cc.largest == (expected[-1] if expected else 0)
