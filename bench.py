@@ -55,6 +55,15 @@ CONFIGS = {
 }
 
 
+L2_NOTE = {
+    "enumerate": "output (3.64 GB per step at c2) far larger than the 126 MB L2; no flush",
+    "count": "inputs are two scalars; the work is on-chip (shared memory); per-segment "
+             "counts written each step; no flush needed",
+    "checks": "bucket lists (~1 GB per window) far larger than L2; no flush",
+    "intervals": "bucket lists far larger than L2; no flush",
+}
+
+
 # ----------------------------------------------------------------------------
 def splitmix_starts(seed: int, n: int, lo: int, hi: int) -> np.ndarray:
     out = np.empty(n, np.uint64)
@@ -196,19 +205,27 @@ def run_ours(args, cfg, world, rank, local):
     import paper_2310_17746_b200 as ws
     from paper_2310_17746_b200 import dist as wsdist
 
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev = local % ndev  # ranks > GPUs only in the gloo smoke mode below
+    torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    sv = ws.Sieve(device=local)
-    stream = torch.cuda.ExternalStream(sv.stream, device=torch.device("cuda", local))
+        # WS_DIST_BACKEND=gloo lets the N>1 host path be exercised with several
+        # ranks on one GPU (NCCL rejects duplicate GPUs); production is nccl.
+        backend = os.environ.get("WS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            tdist.init_process_group(backend)
+    sv = ws.Sieve(device=dev)
+    stream = torch.cuda.ExternalStream(sv.stream, device=torch.device("cuda", dev))
     kind = cfg["kind"]
     lo, hi, scaling = rank_range(cfg, rank, world)
 
     # ---- per-config step functions (device-resident outputs) ----------------
     if kind == "enumerate":
         cap = ws.prime_count_bound(lo, hi)
-        out_dev = torch.empty(cap, dtype=torch.int64, device=f"cuda:{local}")
+        out_dev = torch.empty(cap, dtype=torch.int64, device=f"cuda:{dev}")
 
         def step():
             _, n, c = sv.enumerate_range(lo, hi, out=out_dev, fresh_base=True)
@@ -216,7 +233,7 @@ def run_ours(args, cfg, world, rank, local):
         units_local = None  # primes, known after the first step
     elif kind in ("count", "checks"):
         nseg = sv.num_segments(lo, hi)
-        ps_dev = torch.zeros(max(1, nseg), dtype=torch.int32, device=f"cuda:{local}")
+        ps_dev = torch.zeros(max(1, nseg), dtype=torch.int32, device=f"cuda:{dev}")
 
         def step():
             return sv.count_range(lo, hi, checks=(kind == "checks"), per_seg=ps_dev,
@@ -246,7 +263,7 @@ def run_ours(args, cfg, world, rank, local):
     sieve_ms, launches = [], 0
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             c = step()
@@ -313,7 +330,7 @@ def run_ours(args, cfg, world, rank, local):
     if rank != 0:
         return None
     peaks, peak_src = load_peaks()
-    props = torch.cuda.get_device_properties(local)
+    props = torch.cuda.get_device_properties(dev)
     avg_sieve_ms = float(np.mean(sieve_ms))
     clocks = clk.summary()
     traffic = None
@@ -354,14 +371,16 @@ def run_ours(args, cfg, world, rank, local):
         "data": "synthetic (deterministic ranges; c5 seeded splitmix64)",
         "config": {"workload": cfg["workload"], "L": lo if world == 1 else cfg.get("L"),
                    "R": hi if world == 1 else cfg.get("R"), "segment_slots": SEG,
-                   "l2": "outputs/ranges far larger than the 126 MB L2 (c2 writes 3.64 GB per "
-                         "step); no flush", "parallelism": f"dp{world}",
+                   "l2": L2_NOTE[kind], "parallelism": f"dp{world}",
                    "base_primes": "re-sieved on device every step (WS_FRESH_BASE)"},
-        "result": {"count": checks.count, "sum": checks.sum, "xor": checks.xor,
-                   "largest": checks.largest},
+        "result": {"count": checks.count,
+                   "sum": checks.sum if kind != "count" else None,
+                   "xor": checks.xor if kind != "count" else None,
+                   "largest": checks.largest if kind != "intervals" else None},
         "e2e": e2e, "roofline": roof, "roofline_smem": roof_smem,
         "gpu_launches": launches, "clocks": clocks,
-        "integers_per_s": (hi - lo) * world / (ms_per_step / 1e3) if lo is not None else None,
+        "integers_per_s": (total_units if kind != "enumerate" else (hi - lo) * world)
+                          / (ms_per_step / 1e3),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
