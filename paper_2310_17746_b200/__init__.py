@@ -4,5 +4,6 @@ Importing loads libwheelsieve_cuda.so (the C ABI of include/wheelsieve/gpu.h);
 there is no CPU fallback."""
 from .wheelsieve import (  # noqa: F401
     CountSink, Checks, Errc, Error, MemorySink, PrimeSink, Sieve, SieveConfig, SieveReport,
-    SinkFailure, isqrt, partition, prime_count_bound, round_segment_span, run, start_offsets,
+    SinkFailure, isqrt, partition, prime_count_bound, round_segment_span, run, run_unbounded,
+    start_offsets,
 )

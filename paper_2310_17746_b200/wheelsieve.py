@@ -342,7 +342,7 @@ def round_segment_span(span: int, threads: int) -> int:  # engine.cpp:311-320
     return (span // align + 1) * align
 
 
-def _validate(config: SieveConfig) -> None:  # engine.cpp:119-143 (bounded)
+def _validate(config: SieveConfig, bounded: bool = True) -> None:  # engine.cpp:119-143
     if config.sink is None:
         raise Error(Errc.BadConfig, "config has no sink")
     if config.threads == 0:
@@ -354,12 +354,15 @@ def _validate(config: SieveConfig) -> None:  # engine.cpp:119-143 (bounded)
         raise Error(Errc.BadConfig, f"segment span {config.segment_span} is not a positive multiple of {align}")
     if config.segment_span > K_MAX_SEGMENT_END:
         raise Error(Errc.BadConfig, "segment span exceeds the 64-bit value range")
-    if config.limit is None:
-        raise Error(Errc.BadConfig, "bounded run requires a limit")
-    if config.limit < 2:
-        raise Error(Errc.EmptyRange, "no primes below 2")
-    if config.limit > K_MAX_SEGMENT_END - 1:
-        raise Error(Errc.Overflow, "limit exceeds the sievable 64-bit range")
+    if bounded:
+        if config.limit is None:
+            raise Error(Errc.BadConfig, "bounded run requires a limit")
+        if config.limit < 2:
+            raise Error(Errc.EmptyRange, "no primes below 2")
+        if config.limit > K_MAX_SEGMENT_END - 1:
+            raise Error(Errc.Overflow, "limit exceeds the sievable 64-bit range")
+    elif config.limit is not None:
+        raise Error(Errc.BadConfig, "unbounded run cannot take a limit")
 
 
 _default_sieve: Optional[Sieve] = None
@@ -372,48 +375,91 @@ def _sieve() -> Sieve:
     return _default_sieve
 
 
-def run(config: SieveConfig, sieve: Optional[Sieve] = None) -> SieveReport:
-    """engine.hpp:83 on the GPU: every prime <= limit into config.sink, 2 and
-    3 first, then ascending batches (one per iteration of segment_span)."""
-    _validate(config)
-    sv = sieve or _sieve()
-    t0 = time.perf_counter()
-    limit = config.limit
-    span = config.segment_span
-    limit_end = (limit // 6 + 1) * 6                  # engine.cpp:160
-    iters = limit_end // span + (limit_end % span != 0)
-    rep = SieveReport()
-    sub = span // config.threads
-    # analytic flag accounting (engine.cpp:218-230): the widest iteration
-    ent = 0
+_WIDTH_BYTES = {0: lambda n: (n + 7) // 8, 1: lambda n: n, 2: lambda n: 4 * n}
+_CHUNK_INTEGERS = 1 << 28  # integers sieved per device call for value sinks
+
+
+def _account(config: SieveConfig, seg_lo: int, seg_hi: int, rep: SieveReport) -> None:
+    """Analytic flag-storage accounting of one iteration (engine.cpp:218-230)."""
+    sub = config.segment_span // config.threads
+    ent = byt = 0
     for j in range(config.threads):
-        lo = j * sub
-        if lo >= min(span, limit_end):
+        lo = seg_lo + j * sub
+        if lo >= seg_hi:
             break
-        hi = min(lo + sub, min(span, limit_end))
-        ent += 2 * ((hi - lo) // 6)
-    rep.peak_flag_entries = ent
-    widths = {0: lambda n: (n + 7) // 8, 1: lambda n: n, 2: lambda n: 4 * n}
-    rep.peak_flag_bytes = sum(2 * widths[config.flag_width]((min(j * sub + sub, min(span, limit_end)) - j * sub) // 6)
-                              for j in range(config.threads) if j * sub < min(span, limit_end))
+        hi = min(lo + sub, seg_hi)
+        n = (hi - lo) // 6
+        ent += 2 * n
+        byt += 2 * _WIDTH_BYTES[config.flag_width](n)
+    rep.peak_flag_entries = max(rep.peak_flag_entries, ent)
+    rep.peak_flag_bytes = max(rep.peak_flag_bytes, byt)
+
+
+def _run_loop(config: SieveConfig, stop, sv: Sieve) -> SieveReport:
+    """engine.cpp:149-307 on the device: the same iteration structure and
+    emission (2 and 3 first, one ascending batch per segment_span iteration),
+    with many iterations sieved per device call and batches cut on the host."""
+    bounded = stop is None
+    _validate(config, bounded)
     sink = config.sink
+    t0 = time.perf_counter()
+    span = config.segment_span
+    limit = config.limit if bounded else 0
+    limit_end = (limit // 6 + 1) * 6 if bounded else K_MAX_SEGMENT_END
+    total_iters = limit_end // span + (limit_end % span != 0) if bounded else None
+    rep = SieveReport()
+    want_values = sink.wants_values()
+    per_call = max(1, _CHUNK_INTEGERS // span)
+    vals = np.zeros(0, np.uint64)
+    vpos = 0
+    count_total = count_largest = 0
+    if bounded and not want_values:
+        c = sv.count_range(0, limit + 1)
+        count_total, count_largest = c.count, c.largest
+    i = 0
+    seg_lo = 0
     try:
-        if not sink.wants_values():
-            c = sv.count_range(0, limit + 1)
-            pre = 2 if limit >= 3 else 1
-            sink.emit_count(pre, 3 if limit >= 3 else 2)
-            if c.count > pre:
-                sink.emit_count(c.count - pre, c.largest)
-        else:
-            sink.emit(np.array([2, 3][: 2 if limit >= 3 else 1], np.uint64))
-            for i in range(iters):
-                lo = max(i * span, 4)
-                hi = min((i + 1) * span, limit + 1)
-                if hi <= lo:
-                    continue
-                vals, n, _ = sv.enumerate_range(lo, hi)
-                if n:
-                    sink.emit(vals)
+        while True:
+            if bounded and i >= total_iters:
+                break
+            if stop is not None and stop():
+                rep.stopped = True
+                break
+            if not bounded and seg_lo > K_MAX_SEGMENT_END - span:
+                rep.overflowed = True
+                break
+            seg_hi = limit_end if (bounded and span > limit_end - seg_lo) else seg_lo + span
+            _account(config, seg_lo, seg_hi, rep)
+            if i == 0:  # engine.cpp:268-276
+                n = 2 if (not bounded or limit >= 3) else 1
+                if want_values:
+                    sink.emit(np.array([2, 3][:n], np.uint64))
+                else:
+                    sink.emit_count(n, 3 if n == 2 else 2)
+            if want_values:
+                if i % per_call == 0:
+                    blo = max(seg_lo, 4)
+                    bhi = seg_lo + min(per_call, (K_MAX_SEGMENT_END - seg_lo) // span) * span
+                    if bounded:
+                        bhi = min(bhi, limit + 1)
+                    vals = sv.enumerate_range(blo, bhi)[0] if blo < bhi else np.zeros(0, np.uint64)
+                    vpos = 0
+                top = min(seg_hi, limit + 1) if bounded else seg_hi
+                end = int(np.searchsorted(vals, np.uint64(top), side="left"))
+                if end > vpos:
+                    sink.emit(vals[vpos:end])
+                vpos = end
+            elif bounded:
+                if i + 1 == total_iters and count_total > 2:
+                    sink.emit_count(count_total - 2, count_largest)
+            else:
+                c = sv.count_range(max(seg_lo, 4), seg_hi)
+                if c.count:
+                    sink.emit_count(c.count, c.largest)
+            rep.iterations = i + 1
+            rep.sieved_to = seg_hi
+            i += 1
+            seg_lo += span
     except Error as e:
         if isinstance(e, SinkFailure) or e.code in (Errc.Cuda, Errc.NoDevice, Errc.OutOfMemory):
             raise
@@ -421,9 +467,21 @@ def run(config: SieveConfig, sieve: Optional[Sieve] = None) -> SieveReport:
         rep.largest_prime = sink.largest()
         rep.wall_ms = (time.perf_counter() - t0) * 1e3
         raise SinkFailure(e.code, str(e), rep) from e
-    rep.iterations = iters
-    rep.sieved_to = limit + 1
+    if bounded:
+        rep.sieved_to = limit + 1
     rep.prime_count = sink.count()
     rep.largest_prime = sink.largest()
     rep.wall_ms = (time.perf_counter() - t0) * 1e3
     return rep
+
+
+def run(config: SieveConfig, sieve: Optional[Sieve] = None) -> SieveReport:
+    """engine.hpp:83 on the GPU: every prime <= limit into config.sink."""
+    return _run_loop(config, None, sieve or _sieve())
+
+
+def run_unbounded(config: SieveConfig, stop, sieve: Optional[Sieve] = None) -> SieveReport:
+    """engine.hpp:89 on the GPU.  `stop` is a zero-argument callable (or an
+    object with is_set(), e.g. threading.Event) checked between iterations."""
+    fn = stop.is_set if hasattr(stop, "is_set") else stop
+    return _run_loop(config, fn, sieve or _sieve())

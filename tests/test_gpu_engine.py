@@ -108,3 +108,48 @@ def test_sink_failure_partial(port):  # test_engine.cpp:227-238
 
 def test_back_to_back():  # test_engine.cpp:274-280
     assert run_collect(100, 1, 6000) == run_collect(100, 1, 6000)
+
+
+class StopRequestingSink(MemorySink):  # test_engine.cpp:22-34
+    def __init__(self, flag):
+        super().__init__()
+        self.flag = flag
+
+    def accept(self, batch):
+        super().accept(batch)
+        self.flag.set()
+
+
+def test_unbounded_stop(port):  # test_engine.cpp:240-272
+    import threading
+    from paper_2310_17746_b200 import run_unbounded
+    ev = threading.Event()
+    ev.set()
+    rep = run_unbounded(SieveConfig(None, 1, 6000, 0, CountSink()), ev)
+    assert rep.stopped and not rep.overflowed and rep.prime_count == 0 and rep.iterations == 0
+    ev = threading.Event()
+    sink = StopRequestingSink(ev)
+    rep = run_unbounded(SieveConfig(None, 1, 6000, 0, sink), ev)
+    assert rep.stopped and rep.iterations == 1 and rep.prime_count == 783
+    assert rep.largest_prime == 5987 and rep.sieved_to == 6000
+    assert np.array_equal(sink.primes(), port.naive_sieve(5999))
+    with pytest.raises(Error) as e:
+        run_unbounded(SieveConfig(1000, 1, 6000, 0, MemorySink()), threading.Event())
+    assert e.value.code == Errc.BadConfig
+
+
+def test_large_run_values_match_checksums(sieve):  # config-2 style through run()
+    class ChecksumSink(ws.PrimeSink):
+        def __init__(self):
+            super().__init__()
+            self.s = 0
+            self.x = 0
+
+        def accept(self, batch):
+            self.s = (self.s + int(batch.sum(dtype=np.uint64))) % 2**64
+            self.x ^= int(np.bitwise_xor.reduce(batch))
+
+    sink = ChecksumSink()
+    rep = run(SieveConfig(10**9, 1, 6 * (1 << 18), 0, sink), sieve)
+    assert rep.prime_count == 50_847_534 and rep.largest_prime == 999_999_937
+    assert sink.s == 24_739_512_092_254_535 and sink.x == 6_213_527
