@@ -68,6 +68,24 @@ struct DevBuf {
   }
 };
 
+// Growable page-locked host staging (async H2D/D2H without staging copies).
+struct PinnedBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* reserve(size_t n, const char* what) {
+    if (n <= bytes) return ptr;
+    release();
+    ck(cudaMallocHost(&ptr, std::max<size_t>(n, 64)), what);
+    bytes = n;
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
 uint64_t small_primes_upto(uint64_t B) {  // |{5,7,...,31} ∩ [5, B]|
   static const uint32_t sp[] = {5, 7, 11, 13, 17, 19, 23, 29, 31};
   uint64_t c = 0;
@@ -87,13 +105,19 @@ struct ws_ctx {
   ws_timing timing{};
   cudaEvent_t ev[4] = {};
 
+  PinnedBuf pin_jobs, pin_runs, pin_out;  // async staging for uploads / results
+  DevBuf<uint32_t> d_tabn;  // exact base-table size, written on device by prepare_table
+  DevBuf<uint32_t> small_tab;  // small-prime pattern tables
+
   // resident base-prime table: every prime in [37, base_B]
   bool base_valid = false;
   bool base_built = false;  // the last call (re)built the table
   uint64_t base_B = 0;
-  uint32_t nprimes = 0;
+  uint32_t nprimes = 0;              // upper bound on the table size (host)
+  const uint32_t* nprimes_dev = nullptr;  // exact size on device (nullable)
   DevBuf<uint32_t> tab_p;
   DevBuf<unsigned long long> tab_m;
+  DevBuf<double> tab_inv;
 
   uint32_t n_below_S = 0;  // table primes (>= 37) below S: in-kernel; the rest bucketed
   uint32_t n_wc = 161;     // table primes below the warp-cooperative limit (1024)
@@ -116,6 +140,7 @@ struct ws_ctx {
   DevBuf<unsigned long long> vals;  // enumeration scratch (base primes / host-bound output)
   DevBuf<uint32_t> l0_p;
   DevBuf<unsigned long long> l0_m;
+  DevBuf<double> l0_inv;
   DevBuf<uint32_t> l0_n;
   std::vector<wsk::Job> h_jobs;
 
@@ -124,6 +149,13 @@ struct ws_ctx {
     for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n, &bucket[0], &bucket[1], &bcount[0], &bcount[1]})
       b->release();
     runs.release();
+    tab_inv.release();
+    l0_inv.release();
+    d_tabn.release();
+    small_tab.release();
+    pin_jobs.release();
+    pin_runs.release();
+    pin_out.release();
     for (int i = 0; i < 2; ++i) {
       if (fill_done[i]) cudaEventDestroy(fill_done[i]);
       if (sieve_done[i]) cudaEventDestroy(sieve_done[i]);
@@ -199,8 +231,10 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   const size_t nj = c->h_jobs.size();
   c->jobs.reserve(nj, "jobs");
   c->acc.reserve(nj, "acc");
-  ck(cudaMemcpyAsync(c->jobs.ptr, c->h_jobs.data(), nj * sizeof(wsk::Job),
-                     cudaMemcpyHostToDevice, c->stream), "upload jobs");
+  void* hj = c->pin_jobs.reserve(nj * sizeof(wsk::Job), "pinned jobs");
+  std::memcpy(hj, c->h_jobs.data(), nj * sizeof(wsk::Job));
+  ck(cudaMemcpyAsync(c->jobs.ptr, hj, nj * sizeof(wsk::Job), cudaMemcpyHostToDevice, c->stream),
+     "upload jobs");
   ck(cudaMemsetAsync(c->acc.ptr, 0, nj * sizeof(wsk::JobAcc), c->stream), "zero acc");
   if (mode == wsk::kEnumerate) {
     c->status.reserve(nseg, "status");
@@ -209,13 +243,16 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   }
   if (nseg == 0) return;
   wsk::SieveParams p{};
+  p.small_tab = c->small_tab.ptr;
   p.jobs = c->jobs.ptr;
   p.njobs = static_cast<uint32_t>(nj);
   p.nseg_total = nseg;
   p.S = c->S;
   p.prime_p = c->tab_p.ptr;
   p.prime_m = c->tab_m.ptr;
+  p.prime_inv = c->tab_inv.ptr;
   p.nprimes = c->nprimes;
+  p.nprimes_dev = c->nprimes_dev;
   // warp-cooperative loop for primes below 1024 (>= 256 hits per class per
   // 2^18-slot segment): 161 table entries; one thread per prime above
   p.n_wc = std::min<uint32_t>(c->n_wc, c->nprimes);
@@ -281,9 +318,10 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
       run_off[w + 1] = static_cast<uint32_t>(runs.size());
     }
     c->runs.reserve(runs.size(), "runs");
-    ck(cudaMemcpyAsync(c->runs.ptr, runs.data(), runs.size() * sizeof(wsk::Run),
-                       cudaMemcpyHostToDevice, c->stream), "upload runs");
-    ck(cudaStreamSynchronize(c->stream), "sync runs");  // `runs` is pageable and local
+    void* hr = c->pin_runs.reserve(runs.size() * sizeof(wsk::Run), "pinned runs");
+    std::memcpy(hr, runs.data(), runs.size() * sizeof(wsk::Run));
+    ck(cudaMemcpyAsync(c->runs.ptr, hr, runs.size() * sizeof(wsk::Run), cudaMemcpyHostToDevice,
+                       c->stream), "upload runs");
   }
   // ev[2] also orders the fill stream after everything queued so far
   ck(cudaEventRecord(c->ev[2], c->stream), "event");
@@ -300,6 +338,8 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
       f.nruns = run_off[w + 1] - run_off[w];
       f.prime_p = c->tab_p.ptr;
       f.prime_m = c->tab_m.ptr;
+      f.prime_inv = c->tab_inv.ptr;
+      f.nprimes_dev = c->nprimes_dev;
       f.p_begin = p.n_mid;
       f.p_end = c->nprimes;
       f.log2S = static_cast<uint32_t>(__builtin_ctz(c->S));
@@ -328,7 +368,9 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   c->timing.segments += nseg;
 }
 
-// Make the resident table cover every prime in [37, B].
+// Make the resident table cover every prime in [37, B].  No host round
+// trip: the level-0 count and the table size stay on the device and the
+// kernels read them (SieveParams::nprimes_dev); the host keeps upper bounds.
 void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
   c->base_built = false;
   if (c->base_valid && c->base_B >= B && !fresh) return;
@@ -337,47 +379,76 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
   c->base_valid = false;
   if (B < wsk::kFirstTablePrime) {
     c->nprimes = 0;
+    c->nprimes_dev = nullptr;
     c->base_B = B;
     c->base_valid = true;
     ck(cudaEventRecord(c->ev[1], c->stream), "event");
     return;
   }
   if (B > 0xFFFFFFFFull) throw Fail{WS_OVERFLOW, "base bound exceeds 2^32"};
-  // level 0: primes in [37, isqrt(B)] (isqrt(B) < 2^16)
+  // level 0: primes in [37, isqrt(B)] (isqrt(B) < 2^16: at most 6542 - 11)
   const uint64_t B0 = isqrt_u64(B);
   c->l0_p.reserve(7000, "l0");
   c->l0_m.reserve(7000, "l0");
+  c->l0_inv.reserve(7000, "l0");
   c->l0_n.reserve(1, "l0");
-  ck(wsk::launch_tiny_primes(static_cast<uint32_t>(B0), c->l0_p.ptr, c->l0_m.ptr, c->l0_n.ptr,
-                             c->stream), "tiny primes");
-  uint32_t n0 = 0;
-  ck(cudaMemcpyAsync(&n0, c->l0_n.ptr, 4, cudaMemcpyDeviceToHost, c->stream), "n0");
-  ck(cudaStreamSynchronize(c->stream), "sync");
+  ck(wsk::launch_tiny_primes(static_cast<uint32_t>(B0), c->l0_p.ptr, c->l0_m.ptr, c->l0_inv.ptr,
+                             c->l0_n.ptr, c->stream), "tiny primes");
   c->timing.launches += 1;
   // level 1: enumerate [0, B + 1) with the level-0 table
   const uint64_t cap = prime_count_bound(0, B + 1);
   c->vals.reserve(cap, "base values");
   c->tab_p.reserve(cap, "base table");
   c->tab_m.reserve(cap, "base table");
+  c->tab_inv.reserve(cap, "base table");
+  c->d_tabn.reserve(1, "table size");
   std::swap(c->tab_p, c->l0_p);  // run_sieve reads the table from tab_*
   std::swap(c->tab_m, c->l0_m);
-  c->nprimes = n0;
+  std::swap(c->tab_inv, c->l0_inv);
+  c->nprimes = 7000;
+  c->nprimes_dev = c->l0_n.ptr;
+  // small segments so the (short) base range spreads over many CTAs
+  const uint32_t S_main = c->S;
+  uint32_t S_base = 1u << 12;
+  while (S_base < S_main && (B / 6) / S_base > 4ull * c->sms) S_base <<= 1;
+  c->S = S_base;
   c->h_jobs.assign(1, make_job(0, B + 1, c->S, 0));
-  run_sieve(c, wsk::kEnumerate, nullptr, c->vals.ptr, cap, false);
+  try {
+    run_sieve(c, wsk::kEnumerate, nullptr, c->vals.ptr, cap, false);
+  } catch (...) {
+    c->S = S_main;
+    throw;
+  }
+  c->S = S_main;
   std::swap(c->tab_p, c->l0_p);
   std::swap(c->tab_m, c->l0_m);
-  wsk::JobAcc a{};
-  ck(cudaMemcpyAsync(&a, c->acc.ptr, sizeof a, cudaMemcpyDeviceToHost, c->stream), "acc");
-  ck(cudaStreamSynchronize(c->stream), "sync");
-  if (a.count > cap) throw Fail{WS_CAPACITY, "base prime bound too small"};
+  std::swap(c->tab_inv, c->l0_inv);
   const uint64_t skip = small_primes_upto(B);
-  ck(wsk::launch_prepare_table(c->vals.ptr, skip, a.count, c->tab_p.ptr, c->tab_m.ptr,
-                               c->stream), "prepare table");
+  ck(wsk::launch_prepare_table(c->vals.ptr, skip, &c->acc.ptr[0].count, cap, c->tab_p.ptr,
+                               c->tab_m.ptr, c->tab_inv.ptr, c->d_tabn.ptr, c->stream),
+     "prepare table");
   c->timing.launches += 1;
-  c->nprimes = static_cast<uint32_t>(a.count - skip);
+  c->nprimes = static_cast<uint32_t>(cap > skip ? cap - skip : 0);
+  c->nprimes_dev = c->d_tabn.ptr;
   c->base_B = B;
   c->base_valid = true;
   ck(cudaEventRecord(c->ev[1], c->stream), "event");
+}
+
+// Copy the n job accumulators (and the exact table size) to pinned host
+// memory and wait: the one synchronisation of a call.
+const wsk::JobAcc* fetch_results(ws_ctx* c, size_t n) {
+  char* h = static_cast<char*>(c->pin_out.reserve(n * sizeof(wsk::JobAcc) + 16, "pinned out"));
+  ck(cudaMemcpyAsync(h, c->acc.ptr, n * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost, c->stream),
+     "results");
+  uint32_t* tabn = reinterpret_cast<uint32_t*>(h + n * sizeof(wsk::JobAcc));
+  *tabn = c->nprimes;
+  if (c->nprimes_dev)
+    ck(cudaMemcpyAsync(tabn, c->nprimes_dev, 4, cudaMemcpyDeviceToHost, c->stream), "table size");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  ck(cudaGetLastError(), "kernel");
+  c->timing.base_primes = *tabn + small_primes_upto(c->base_B);
+  return reinterpret_cast<const wsk::JobAcc*>(h);
 }
 
 float event_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -527,6 +598,17 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
       return WS_CUDA;
     }
   bool ok = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking) == cudaSuccess;
+  if (ok) {
+    std::vector<uint32_t> tab(wsk::small_table_words());
+    wsk::build_small_tables(tab.data());
+    try {
+      c->small_tab.reserve(tab.size(), "small tables");
+    } catch (const Fail&) {
+      ok = false;
+    }
+    ok = ok && cudaMemcpy(c->small_tab.ptr, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) ==
+                   cudaSuccess;
+  }
   for (int i = 0; i < 2 && ok; ++i)
     ok = cudaEventCreateWithFlags(&c->fill_done[i], cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&c->sieve_done[i], cudaEventDisableTiming) == cudaSuccess;
@@ -618,14 +700,10 @@ ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws
     }
     const int mode = (flags & WS_WANT_CHECKS) ? wsk::kCountChecks : wsk::kCount;
     run_sieve(ctx, mode, dps, nullptr, 0, true);
-    wsk::JobAcc a{};
-    ck(cudaMemcpyAsync(&a, ctx->acc.ptr, sizeof a, cudaMemcpyDeviceToHost, ctx->stream),
-       "acc");
     if (per_seg && !dev_out)
       ck(cudaMemcpyAsync(per_seg, dps, std::min(nseg, per_seg_cap) * sizeof(uint32_t),
                          cudaMemcpyDeviceToHost, ctx->stream), "per_seg");
-    ck(cudaStreamSynchronize(ctx->stream), "sync");
-    ck(cudaGetLastError(), "kernel");
+    const wsk::JobAcc a = *fetch_results(ctx, 1);
     out->count = a.count;
     out->sum = a.sum;
     out->xor_ = a.xr;
@@ -634,7 +712,6 @@ ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws
     if (n_seg) *n_seg = nseg;
     ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
     ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
-    ctx->timing.base_primes = ctx->nprimes + small_primes_upto(ctx->base_B);
   });
 }
 
@@ -673,11 +750,7 @@ ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags
       for (uint64_t i = 0; i < npre && i < cap; ++i) out[i] = pre[i];
     }
     run_sieve(ctx, wsk::kEnumerate, nullptr, dst, dcap, true);
-    wsk::JobAcc a{};
-    ck(cudaMemcpyAsync(&a, ctx->acc.ptr, sizeof a, cudaMemcpyDeviceToHost, ctx->stream),
-       "acc");
-    ck(cudaStreamSynchronize(ctx->stream), "sync");
-    ck(cudaGetLastError(), "kernel");
+    const wsk::JobAcc a = *fetch_results(ctx, 1);
     if (!dev_out) {
       const uint64_t n = std::min<uint64_t>(a.count, dcap);
       if (n)
@@ -693,7 +766,6 @@ ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags
     if (checks) *checks = chk;
     ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
     ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
-    ctx->timing.base_primes = ctx->nprimes + small_primes_upto(ctx->base_B);
     if (chk.count > cap) throw Fail{WS_CAPACITY, "output capacity below the prime count"};
   });
   return st;
@@ -733,11 +805,7 @@ ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64
     }
     const bool checks = sums || xors;
     run_sieve(ctx, checks ? wsk::kCountChecks : wsk::kCount, nullptr, nullptr, 0, true);
-    std::vector<wsk::JobAcc> acc(n);
-    ck(cudaMemcpyAsync(acc.data(), ctx->acc.ptr, n * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost,
-                       ctx->stream), "acc");
-    ck(cudaStreamSynchronize(ctx->stream), "sync");
-    ck(cudaGetLastError(), "kernel");
+    const wsk::JobAcc* acc = fetch_results(ctx, n);
     std::vector<uint32_t> hc(n);
     std::vector<uint64_t> hs(n), hx(n);
     for (uint64_t i = 0; i < n; ++i) {
@@ -758,7 +826,6 @@ ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64
     }
     ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
     ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
-    ctx->timing.base_primes = ctx->nprimes + small_primes_upto(ctx->base_B);
   });
 }
 

@@ -42,6 +42,7 @@ struct Run {             // a maximal run of window segments of one job
 };
 
 struct SieveParams {
+  const uint32_t* small_tab;  // small-prime pattern tables (built once per context)
   const Job* jobs;
   uint32_t njobs;
   uint64_t nseg_total;   // segments of all jobs
@@ -49,8 +50,10 @@ struct SieveParams {
   uint64_t s_count;
   uint32_t S;                        // wheel slots per class per segment (power of two)
   const uint32_t* prime_p;           // sieving primes >= 37, ascending
-  const unsigned long long* prime_m; // floor((2^64-1)/p), Barrett reciprocal
-  uint32_t nprimes;
+  const unsigned long long* prime_m; // floor((2^64-1)/p), Barrett reciprocal (ks >= 2^53)
+  const double* prime_inv;           // fl(1/p), FP64 quotient estimate (ks < 2^53)
+  uint32_t nprimes;                  // host-side upper bound on the table size
+  const uint32_t* nprimes_dev;       // nullable: exact table size, written on device
   uint32_t n_wc;                     // primes [0, n_wc) use the warp-cooperative loop
   uint32_t n_mid;                    // primes [n_wc, n_mid) one thread per prime; [n_mid,
                                      // nprimes) from buckets (or directly if bucket == null)
@@ -66,6 +69,8 @@ struct SieveParams {
 };
 
 size_t sieve_smem_bytes(uint32_t S, int mode);
+uint32_t small_table_words();
+void build_small_tables(uint32_t* out);  // host
 // blocks_per_sm[mode] for the three modes
 cudaError_t sieve_configure(int* blocks_per_sm);
 cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st);
@@ -75,6 +80,8 @@ struct FillParams {
   uint32_t nruns;
   const uint32_t* prime_p;
   const unsigned long long* prime_m;
+  const double* prime_inv;
+  const uint32_t* nprimes_dev;  // exact table size (p_end is an upper bound)
   uint32_t p_begin, p_end;  // large primes [p_begin, p_end) of the table
   uint32_t log2S;
   uint32_t* bucket;
@@ -90,10 +97,13 @@ cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st);
 
 // Level-0 base primes: all primes in [37, n] (n <= 65536 + 1) in one block.
 cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
-                               uint32_t* out_count, cudaStream_t st);
+                               double* out_inv, uint32_t* out_count, cudaStream_t st);
 // Table preparation: vals[i] (uint64 primes, ascending) -> p / Barrett m for
 // i in [skip, n).
-cudaError_t launch_prepare_table(const unsigned long long* vals, uint64_t skip, uint64_t n,
-                                 uint32_t* out_p, unsigned long long* out_m, cudaStream_t st);
+// n_dev: number of values (device); out_n = n - skip (device).  cap bounds n.
+cudaError_t launch_prepare_table(const unsigned long long* vals, uint64_t skip,
+                                 const unsigned long long* n_dev, uint64_t cap, uint32_t* out_p,
+                                 unsigned long long* out_m, double* out_inv, uint32_t* out_n,
+                                 cudaStream_t st);
 
 }  // namespace wsk

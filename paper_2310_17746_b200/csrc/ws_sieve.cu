@@ -62,6 +62,39 @@ __device__ __forceinline__ uint32_t mod_barrett(uint64_t x, uint32_t p, uint64_t
   return static_cast<uint32_t>(r);
 }
 
+// ks mod p for every sieving prime of a segment.  For ks < 2^53 (values
+// below 5.4e16, every BASELINE config) one FP64 FMA gives the quotient:
+// fma(ks, 1/p, 1.5*2^52) holds round(ks/p) in its low mantissa word; with
+// |ks * fl(1/p) - ks/p| < 1/37 the estimate is q or q+1, so one conditional
+// add of p fixes the 32-bit remainder.  Larger ks use the 64-bit Barrett.
+struct ModCtx {
+  uint64_t ks;
+  double ksd;
+  uint32_t kslo;
+  bool fast;
+};
+
+__device__ __forceinline__ ModCtx mod_ctx(uint64_t ks) {
+  ModCtx c;
+  c.ks = ks;
+  c.fast = ks < (1ull << 53);
+  c.ksd = static_cast<double>(ks);
+  c.kslo = static_cast<uint32_t>(ks);
+  return c;
+}
+
+__device__ __forceinline__ uint32_t mod_p(const ModCtx& c, uint32_t p, const double* inv,
+                                          const unsigned long long* m, uint32_t i) {
+  if (c.fast) {
+    const double t = __fma_rn(c.ksd, __ldg(inv + i), 6755399441055744.0);
+    const uint32_t q = static_cast<uint32_t>(__double2loint(t));
+    uint32_t r = c.kslo - q * p;
+    if (static_cast<int32_t>(r) < 0) r += p;
+    return r;
+  }
+  return mod_barrett(c.ks, p, __ldg(m + i));
+}
+
 // 32-bit shared-window address of a shared-memory pointer
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -98,25 +131,25 @@ constexpr uint32_t kTabPerClass = kTabW0 + kTabW1 + kTabW2;
 constexpr uint32_t kTabWords = 2 * kTabPerClass;
 constexpr uint32_t kTabOff1 = kTabW0, kTabOff2 = kTabW0 + kTabW1;
 
-__device__ void build_tables(uint32_t* tab) {
-  for (uint32_t idx = threadIdx.x; idx < kTabWords; idx += blockDim.x) {
-    const uint32_t cls = idx / kTabPerClass;  // 0 -> 6k+1, 1 -> 6k+5
-    const uint32_t rem = idx % kTabPerClass;
-    const int g = rem < kTabOff1 ? 0 : (rem < kTabOff2 ? 1 : 2);
-    const uint32_t i = rem - (g == 0 ? 0u : g == 1 ? kTabOff1 : kTabOff2);
-    uint32_t word = 0;
-    for (uint32_t b = 0; b < 32; ++b) {
-      const uint32_t pos = 32 * i + b;
-      bool keep = true;
-      for (int j = 0; j < group_size(g); ++j) {
-        const uint32_t q = group_prime(g, j);
-        const uint32_t t = cls ? target5(q) : target1(q);
-        keep = keep && (pos % q != t);
-      }
-      word |= static_cast<uint32_t>(keep) << b;
+// One table word (class cls, group g, word i): bit b set when index
+// 32 i + b is not a multiple-position of any prime of the group.
+__host__ __device__ uint32_t table_word(uint32_t idx) {
+  const uint32_t cls = idx / kTabPerClass;  // 0 -> 6k+1, 1 -> 6k+5
+  const uint32_t rem = idx % kTabPerClass;
+  const int g = rem < kTabOff1 ? 0 : (rem < kTabOff2 ? 1 : 2);
+  const uint32_t i = rem - (g == 0 ? 0u : g == 1 ? kTabOff1 : kTabOff2);
+  uint32_t word = 0;
+  for (uint32_t b = 0; b < 32; ++b) {
+    const uint32_t pos = 32 * i + b;
+    bool keep = true;
+    for (int j = 0; j < group_size(g); ++j) {
+      const uint32_t q = group_prime(g, j);
+      const uint32_t t = cls ? target5(q) : target1(q);
+      keep = keep && (pos % q != t);
     }
-    tab[idx] = word;
+    word |= static_cast<uint32_t>(keep) << b;
   }
+  return word;
 }
 
 __device__ __forceinline__ uint32_t tab_read(const uint32_t* t, uint32_t off) {
@@ -222,18 +255,20 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
 // p is not yet active in this segment (p*p beyond its end; since primes
 // ascend, no later prime is active either).  The activation test is two
 // 32-bit compares against the segment's thresholds.
-__device__ __forceinline__ bool prime_offsets(uint32_t p, uint64_t m, uint64_t ks, uint32_t t_lo,
-                                              uint32_t t_hi, uint32_t& rel1, uint32_t& rel5) {
+__device__ __forceinline__ bool prime_offsets(uint32_t p, uint32_t i, const double* inv,
+                                              const unsigned long long* m, const ModCtx& mc,
+                                              uint32_t t_lo, uint32_t t_hi, uint32_t& rel1,
+                                              uint32_t& rel5) {
   if (p > t_hi) return false;
   const uint32_t t1 = target1(p), t5 = target5(p);
   if (p > t_lo) {
     // activation segment: class 1 starts exactly at p*p, class 5 at the
     // first multiple above it (anchor p*(p-1), segment.cpp:182)
     const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;
-    rel1 = static_cast<uint32_t>(ksq - ks);
+    rel1 = static_cast<uint32_t>(ksq - mc.ks);
     rel5 = rel1 + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
   } else {
-    const uint32_t r = mod_barrett(ks, p, m);
+    const uint32_t r = mod_p(mc, p, inv, m, i);
     rel1 = t1 >= r ? t1 - r : t1 + p - r;
     rel5 = t5 >= r ? t5 - r : t5 + p - r;
   }
@@ -243,6 +278,14 @@ __device__ __forceinline__ bool prime_offsets(uint32_t p, uint64_t m, uint64_t k
 // cross off bit h of the bitmap at shared address a0
 __device__ __forceinline__ void mark(uint32_t a0, uint32_t h) {
   atom_or_shared(a0 + ((h >> 5) << 2), 1u << (h & 31u));
+}
+
+// ... only if h < len, as a predicated atomic (no branch / reconvergence)
+__device__ __forceinline__ void mark_if(uint32_t a0, uint32_t h, uint32_t len) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %2, %3;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
+      ::"r"(a0 + ((h >> 5) << 2)), "r"(1u << (h & 31u)), "r"(h), "r"(len)
+      : "memory");
 }
 
 // Warp-cooperative strided marking of one class: lane l takes hits
@@ -268,38 +311,41 @@ __device__ __forceinline__ void mark_strided(uint32_t a0, uint32_t h0, uint32_t 
 
 // Phase 2: medium and large primes.
 __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo& si,
-                                             uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr) {
+                                             uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr,
+                                             uint32_t nprimes) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t len = si.len;
   const uint64_t ks = si.ks;
   const uint32_t a1 = smem_addr(bm1), a5 = smem_addr(bm5);
   const uint32_t t_lo = si.t_lo, t_hi = si.t_hi;
+  const ModCtx mc = mod_ctx(ks);
+  const uint32_t n_wc = min(P.n_wc, nprimes), n_mid = min(P.n_mid, nprimes);
   // warp-cooperative primes, handed out dynamically (largest work first)
   for (;;) {
     uint32_t i = 0;
     if (lane == 0) i = atomicAdd(wc_ctr, 1u);
     i = __shfl_sync(kFull, i, 0);
-    if (i >= P.n_wc) break;
+    if (i >= n_wc) break;
     const uint32_t p = P.prime_p[i];
     uint32_t rel1, rel5;
-    if (!prime_offsets(p, P.prime_m[i], ks, t_lo, t_hi, rel1, rel5)) break;
+    if (!prime_offsets(p, i, P.prime_inv, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
     mark_strided(a1, rel1, p, len, lane);
     mark_strided(a5, rel5, p, len, lane);
   }
   // large primes come from the window's bucket list unless it overflowed
   const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;
-  const uint32_t lp_end = use_bucket ? P.n_mid : P.nprimes;
+  const uint32_t lp_end = use_bucket ? n_mid : nprimes;
   const uint32_t warp = threadIdx.x >> 5;
   // p < S: one thread per prime, static warp-sized chunks; both classes
   // advance together (their hits are the same stride p apart)
-  const uint32_t mid_end = P.n_mid < lp_end ? P.n_mid : lp_end;
-  for (uint32_t base = P.n_wc + 32 * warp; base < mid_end; base += 32 * kWarps) {
+  const uint32_t mid_end = n_mid < lp_end ? n_mid : lp_end;
+  for (uint32_t base = n_wc + 32 * warp; base < mid_end; base += 32 * kWarps) {
     if (P.prime_p[base] > t_hi) break;  // primes ascend: the rest is inactive
     const uint32_t i = base + lane;
     if (i >= mid_end) continue;
     const uint32_t p = P.prime_p[i];
     uint32_t rel1, rel5;
-    if (!prime_offsets(p, P.prime_m[i], ks, t_lo, t_hi, rel1, rel5)) continue;
+    if (!prime_offsets(p, i, P.prime_inv, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) continue;
     const int32_t d = static_cast<int32_t>(rel5 - rel1);
     const uint32_t dpos = d > 0 ? static_cast<uint32_t>(d) : 0u;
     uint32_t h = rel1;
@@ -307,20 +353,18 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       mark(a1, h);
       mark(a5, h + d);
     }
-    if (h < len) mark(a1, h);
-    const uint32_t h5 = h + d;
-    if (d < 0 && h5 < len) mark(a5, h5);
+    mark_if(a1, h, len);
+    mark_if(a5, h + d, d < 0 ? len : 0u);
   }
-  // p >= S (no bucket list): at most one hit per class, no loop
+  // p >= S (no bucket list): at most one hit per class -- no loop, no branch
   for (uint32_t base = mid_end + 32 * warp; base < lp_end; base += 32 * kWarps) {
-    if (P.prime_p[base] > t_hi) break;
+    if (__ldg(P.prime_p + base) > t_hi) break;
     const uint32_t i = base + lane;
-    if (i >= lp_end) continue;
-    const uint32_t p = P.prime_p[i];
-    uint32_t rel1, rel5;
-    if (!prime_offsets(p, P.prime_m[i], ks, t_lo, t_hi, rel1, rel5)) continue;
-    if (rel1 < len) mark(a1, rel1);
-    if (rel5 < len) mark(a5, rel5);
+    const uint32_t p = i < lp_end ? __ldg(P.prime_p + i) : 0xFFFFFFFFu;
+    uint32_t rel1 = len, rel5 = len;
+    prime_offsets(p, i, P.prime_inv, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
+    mark_if(a1, rel1, len);
+    mark_if(a5, rel5, len);
   }
   if (use_bucket) {
     const uint64_t ls = si.s - P.s_begin;
@@ -450,7 +494,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
   __shared__ uint32_t seg_total;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 
-  build_tables(tab);
+  for (uint32_t i = threadIdx.x; i < kTabWords; i += blockDim.x) tab[i] = __ldg(P.small_tab + i);
+  const uint32_t nprimes = P.nprimes_dev ? min(P.nprimes, *P.nprimes_dev) : P.nprimes;
   for (;;) {
     __syncthreads();  // bitmap / si reuse guard
     if (threadIdx.x == 0) {
@@ -461,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
     if (si.s == ~0ull) break;
     init_words(si, tab, bm1, bm5);
     __syncthreads();
-    sieve_primes(P, si, bm1, bm5, &wc_ctr);
+    sieve_primes(P, si, bm1, bm5, &wc_ctr, nprimes);
     __syncthreads();
     if (P.bucket != nullptr && threadIdx.x == 0) P.bcount[si.s - P.s_begin] = 0;
 
@@ -676,19 +721,21 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
   const uint32_t span = static_cast<uint32_t>(run.k_hi - run.k_lo);  // <= kMaxWindow * S
   // activation thresholds of the run (see fetch_segment)
   const uint32_t t_lo = isqrt64(6 * run.k_lo), t_hi = isqrt64(6 * run.k_hi);
+  const ModCtx mc = mod_ctx(run.k_lo);
   for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) hist[i] = 0;
   __syncthreads();
   const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
+  const uint32_t p_end = F.nprimes_dev ? min(F.p_end, *F.nprimes_dev) : F.p_end;
   // pass 1: first hits (Barrett, p*p activation) + per-segment histogram
 #pragma unroll 1
   for (int j = 0; j < kFillPrimesPerThread; ++j) {
     const uint32_t li = j * kFillThreads + threadIdx.x;
     const uint32_t i = first + li;
     uint32_t r1 = 0xFFFFFFFFu, r5 = 0xFFFFFFFFu;
-    if (i < F.p_end) {
+    if (i < p_end) {
       const uint32_t p = F.prime_p[i];
       uint32_t q1, q5;
-      if (prime_offsets(p, F.prime_m[i], run.k_lo, t_lo, t_hi, q1, q5)) {
+      if (prime_offsets(p, i, F.prime_inv, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
         if (q1 < span) r1 = q1;
         if (q5 < span) r5 = q5;
         // 64-bit stepping: p can be within `span` of 2^32 near the top of
@@ -712,7 +759,7 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
   for (int j = 0; j < kFillPrimesPerThread; ++j) {
     const uint32_t li = j * kFillThreads + threadIdx.x;
     const uint32_t i = first + li;
-    if (i >= F.p_end) break;
+    if (i >= p_end) break;
     const uint32_t r1 = first1[li], r5 = first5[li];
     if (r1 == 0xFFFFFFFFu && r5 == 0xFFFFFFFFu) continue;
     const uint32_t p = F.prime_p[i];
@@ -733,6 +780,7 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
 // writing the primes >= 37 in ascending order with their Barrett constants.
 __global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t* out_p,
                                                            unsigned long long* out_m,
+                                                           double* out_inv,
                                                            uint32_t* out_count) {
   __shared__ uint32_t comp[(65536 + 64) / 32 + 1];
   __shared__ uint32_t scan[1024];
@@ -766,22 +814,33 @@ __global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t*
     if (x >= kFirstTablePrime && !((comp[x >> 5] >> (x & 31)) & 1u)) {
       out_p[pos] = x;
       out_m[pos] = ~0ull / x;
+      out_inv[pos] = 1.0 / static_cast<double>(x);
       ++pos;
     }
   if (threadIdx.x == blockDim.x - 1) *out_count = scan[threadIdx.x];
 }
 
-__global__ void prepare_table_kernel(const unsigned long long* vals, uint64_t skip, uint64_t n,
-                                     uint32_t* out_p, unsigned long long* out_m) {
+__global__ void prepare_table_kernel(const unsigned long long* vals, uint64_t skip,
+                                     const unsigned long long* n_dev, uint64_t cap,
+                                     uint32_t* out_p, unsigned long long* out_m, double* out_inv,
+                                     uint32_t* out_n) {
+  const uint64_t n = *n_dev < cap ? static_cast<uint64_t>(*n_dev) : cap;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_n = static_cast<uint32_t>(n > skip ? n - skip : 0);
   for (uint64_t i = skip + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t p = static_cast<uint32_t>(vals[i]);
     out_p[i - skip] = p;
     out_m[i - skip] = ~0ull / p;
+    out_inv[i - skip] = 1.0 / static_cast<double>(p);
   }
 }
 
 }  // namespace
+
+uint32_t small_table_words() { return kTabWords; }
+void build_small_tables(uint32_t* out) {
+  for (uint32_t i = 0; i < kTabWords; ++i) out[i] = table_word(i);
+}
 
 size_t sieve_smem_bytes(uint32_t S, int mode) {
   const size_t base = (2 * (S / 32) + kTabWords) * sizeof(uint32_t);
@@ -827,17 +886,18 @@ cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st) {
 }
 
 cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
-                               uint32_t* out_count, cudaStream_t st) {
-  tiny_primes_kernel<<<1, 1024, 0, st>>>(n, out_p, out_m, out_count);
+                               double* out_inv, uint32_t* out_count, cudaStream_t st) {
+  tiny_primes_kernel<<<1, 1024, 0, st>>>(n, out_p, out_m, out_inv, out_count);
   return cudaGetLastError();
 }
 
-cudaError_t launch_prepare_table(const unsigned long long* vals, uint64_t skip, uint64_t n,
-                                 uint32_t* out_p, unsigned long long* out_m, cudaStream_t st) {
-  if (n <= skip) return cudaSuccess;
-  const uint64_t cnt = n - skip;
+cudaError_t launch_prepare_table(const unsigned long long* vals, uint64_t skip,
+                                 const unsigned long long* n_dev, uint64_t cap, uint32_t* out_p,
+                                 unsigned long long* out_m, double* out_inv, uint32_t* out_n,
+                                 cudaStream_t st) {
+  const uint64_t cnt = cap > skip ? cap - skip : 1;
   const int grid = static_cast<int>(cnt / 256 + 1 < 4096 ? cnt / 256 + 1 : 4096);
-  prepare_table_kernel<<<grid, 256, 0, st>>>(vals, skip, n, out_p, out_m);
+  prepare_table_kernel<<<grid, 256, 0, st>>>(vals, skip, n_dev, cap, out_p, out_m, out_inv, out_n);
   return cudaGetLastError();
 }
 
