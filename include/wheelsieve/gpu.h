@@ -14,6 +14,8 @@
  *   engine tiling plan_iteration / round_segment_span  engine.cpp:311-342
  *       -> ws_partition (contiguous per-GPU super-ranges)
  *   start_offsets (paper Table 1)                 wheel.cpp:96-106  -> ws_start_offsets
+ *   BasePrimeStore::bootstrap / naive_sieve       base_store.cpp:34, wheel.cpp:40 -> ws_base_primes
+ *   SegmentBitmap + sieve_segment (flag arrays)   segment.cpp:93-188 -> ws_sieve_segment
  *   isqrt                                         wheel.cpp:25-33   -> ws_isqrt
  *
  * Conventions (mirroring the reference):
@@ -124,13 +126,30 @@ ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags
 ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64_t width,
                              uint32_t flags, uint32_t* counts, uint64_t* sums, uint64_t* xors);
 
+/* BasePrimeStore::bootstrap / entries (base_store.cpp:34-42, naive_sieve
+ * wheel.cpp:40-54): the wheel primes 5 <= p <= B, ascending, sieved on the
+ * device (B <= 2^32).  *n = count; WS_CAPACITY if cap is too small. */
+ws_status ws_base_primes(ws_ctx* ctx, uint64_t B, uint32_t flags, uint64_t* out, uint64_t cap,
+                         uint64_t* n);
+
+/* SegmentBitmap(start, len) + sieve_segment (segment.hpp:90-168,
+ * segment.cpp:93-188): the two flag arrays after sieving, in FlagArray's Bit
+ * layout -- bit i of words[i / 64], LSB-first, tail bits zero -- for the 6k+1
+ * class (r1_words) and the 6k+5 class (r5_words), ceil(len / 64) words each.
+ * As in the reference the value 1 is left set (callers clear it,
+ * engine.cpp:244).  Errors: WS_ALIGNMENT (start % 6), WS_DOMAIN (len == 0),
+ * WS_OVERFLOW (end beyond the 64-bit range). */
+ws_status ws_sieve_segment(ws_ctx* ctx, uint64_t start, uint64_t len, uint32_t flags,
+                           uint64_t* r1_words, uint64_t* r5_words);
+
 /* Upper bound on the number of primes in [L, R) (capacity helper). */
 uint64_t ws_prime_count_bound(uint64_t L, uint64_t R);
 
 /* Multi-GPU partitioner: rank's contiguous share [*lo, *hi) of [L, R), with
  * interior boundaries on multiples of 6 * segment_slots values counted from
  * floor(L / 6) * 6 (so every rank's segments coincide with the single-GPU
- * segmentation); the last rank absorbs the remainder.  Pure function. */
+ * segmentation); rank r gets segments [floor(r n / world), floor((r+1) n / world))
+ * of the n segments, clipped to [L, R).  Pure function. */
 ws_status ws_partition(uint64_t L, uint64_t R, uint32_t segment_slots, uint32_t rank,
                        uint32_t world, uint64_t* lo, uint64_t* hi);
 

@@ -9,7 +9,10 @@
 //                       contract, count-only emit_count)  -> same semantics
 //   engine.hpp:13-89    SieveConfig, WorkerAssignment, SieveReport, SinkFailure,
 //                       round_segment_span, plan_iteration, run, run_unbounded
-//   wheel.hpp:50-81     isqrt, start_offsets
+//   wheel.hpp:13-81     ResidueClass, WheelCoord, value_of, coord_of, isqrt,
+//                       ceil_sqrt, start_offsets
+//   segment.hpp:90-168  SegmentBitmap + sieve_segment -> Device::sieve_segment
+//   base_store.hpp:25   BasePrimeStore::bootstrap     -> Device::base_primes
 //   (new)               Device::count_range / enumerate_range / count_intervals
 //                       for [L, R) (the SURVEY §3.3 composition as one call)
 //
@@ -75,6 +78,35 @@ inline constexpr uint64_t kMaxWheelIndex = (UINT64_MAX - 5) / 6;        // wheel
 inline constexpr uint64_t kMaxSegmentEnd = 6 * (kMaxWheelIndex + 1);    // wheel.hpp:37
 
 inline uint64_t isqrt(uint64_t n) { return ws_isqrt(n); }
+
+inline uint64_t ceil_sqrt(uint64_t n) {  // wheel.cpp:35-38
+  const uint64_t r = isqrt(n);
+  return r * r == n ? r : r + 1;
+}
+
+enum class ResidueClass : uint8_t { R1, R5 };  // wheel.hpp:13
+
+struct WheelCoord {  // wheel.hpp:17-22
+  uint64_t index;
+  ResidueClass residue;
+  bool operator==(const WheelCoord&) const = default;
+};
+
+inline uint64_t value_of(WheelCoord c) {  // wheel.cpp:8-13
+  if (c.index > kMaxWheelIndex)
+    throw Error(Errc::Overflow, "wheel index " + std::to_string(c.index) +
+                                    " exceeds the 64-bit value range");
+  return 6 * c.index + (c.residue == ResidueClass::R1 ? 1 : 5);
+}
+
+inline WheelCoord coord_of(uint64_t n) {  // wheel.cpp:15-23
+  switch (n % 6) {
+    case 1: return {n / 6, ResidueClass::R1};
+    case 5: return {n / 6, ResidueClass::R5};
+    default:
+      throw Error(Errc::NotOnWheel, std::to_string(n) + " is divisible by 2 or 3, not on the wheel");
+  }
+}
 
 struct StartOffsets {  // wheel.hpp:26-30
   uint64_t id1;
@@ -157,6 +189,35 @@ struct Checks {
   uint64_t count = 0, sum = 0, xr = 0, largest = 0;
 };
 
+// Flag arrays of one sieved segment in FlagArray's Bit layout (segment.hpp:34-84):
+// bit i of words[i >> 6], LSB-first, tail bits zero; the value 1 left set.
+struct SegmentFlags {
+  uint64_t start = 0, len = 0;
+  std::vector<uint64_t> r1, r5;
+  bool test(ResidueClass r, uint64_t i) const {
+    const auto& w = r == ResidueClass::R1 ? r1 : r5;
+    return (w[i >> 6] >> (i & 63)) & 1;
+  }
+  bool flag_for(uint64_t value) const {  // segment.cpp:112-124 (unchecked range)
+    const WheelCoord c = coord_of(value);
+    return test(c.residue, c.index - start / 6);
+  }
+  std::vector<uint64_t> surviving() const {  // segment.hpp:123-146 order
+    std::vector<uint64_t> v;
+    for (size_t wi = 0; wi < r1.size(); ++wi) {
+      uint64_t m1 = r1[wi], m5 = r5[wi], both = m1 | m5;
+      while (both) {
+        const int bit = __builtin_ctzll(both);
+        both &= both - 1;
+        const uint64_t k = (uint64_t{wi} << 6) | static_cast<uint64_t>(bit);
+        if ((m1 >> bit) & 1) v.push_back(start + 6 * k + 1);
+        if ((m5 >> bit) & 1) v.push_back(start + 6 * k + 5);
+      }
+    }
+    return v;
+  }
+};
+
 // One GPU context (device buffers, stream, resident base-prime table).  Not
 // reentrant: one Device per host thread.
 class Device {
@@ -201,6 +262,30 @@ class Device {
     out.resize(n);
     if (checks) *checks = {c.count, c.sum, c.xor_, c.largest};
     return out;
+  }
+
+  // BasePrimeStore::bootstrap entries: the wheel primes 5 <= p <= B.
+  std::vector<uint64_t> base_primes(uint64_t B) {
+    std::vector<uint64_t> out(std::max<uint64_t>(1, ws_prime_count_bound(0, B + 1)));
+    uint64_t n = 0;
+    check(ws_base_primes(ctx_, B, 0u, out.data(), out.size(), &n), ctx_, "ws_base_primes");
+    out.resize(n);
+    return out;
+  }
+
+  // SegmentBitmap(start, len) + sieve_segment (segment.cpp:93-188).
+  SegmentFlags sieve_segment(uint64_t start, uint64_t len) {
+    SegmentFlags f;
+    f.start = start;
+    f.len = len;
+    const uint64_t nw = (len + 63) / 64;
+    f.r1.assign(std::max<uint64_t>(nw, 1), 0);
+    f.r5.assign(std::max<uint64_t>(nw, 1), 0);
+    check(ws_sieve_segment(ctx_, start, len, 0u, f.r1.data(), f.r5.data()), ctx_,
+          "ws_sieve_segment");
+    f.r1.resize(nw);
+    f.r5.resize(nw);
+    return f;
   }
 
   void count_intervals(std::span<const uint64_t> Ls, uint64_t width, std::vector<uint32_t>& counts,

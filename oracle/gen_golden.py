@@ -20,7 +20,7 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle.oracle import Reference, Port  # noqa: E402
+from oracle.oracle import Reference, Port, fnv1a64  # noqa: E402
 
 GOLDEN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
 SEG = 1 << 18
@@ -42,6 +42,10 @@ WINDOWS = [
     (999_999_999_989 - 6, 999_999_999_989 + 7),
     (10**16 - 10**6 - 12, 10**16 - 12),  # naive_sieve cap (wheel.hpp:40) bounds R at 1e16
 ]
+
+SEGMENTS = [(12_000, 1000), (0, 1000), (10_200, 1), (168, 1), (594_000, 1000), (6, 77),
+            (0, 1 << 18), (6 * 10**14, 300_000), (6 * 123_456_789, (1 << 18) + 5),
+            (10**16 - 6 * 4000 - 4, 4000)]
 
 PREFIXES = [2, 3, 4, 5, 29, 30, 96, 100, 1000, 5999, 10_000, 99_991, 100_000, 123_456, 10**6,
             10**7, 10**8, 10**9]
@@ -108,6 +112,26 @@ def main() -> None:
             start = 6 * int(rng.integers(p // 6 + 1, 166_666))
             i1, i5 = ref.start_offsets(p, start)
             offs.append(dict(p=p, start=start, id1=i1, id5=i5))
+
+    # SegmentBitmap + sieve_segment (segment.cpp:93-188): raw flag words
+    segs = []
+    for start, length in SEGMENTS:
+        w1, w5 = ref.sieve_segment(start, length)
+        segs.append(dict(start=start, len=length, r1=[int(x) for x in w1] if length <= 4096 else None,
+                         r5=[int(x) for x in w5] if length <= 4096 else None,
+                         fnv_r1=fnv1a64(w1.astype("<u8").tobytes()),
+                         fnv_r5=fnv1a64(w5.astype("<u8").tobytes()),
+                         pop_r1=int(sum(bin(int(x)).count("1") for x in w1)),
+                         pop_r5=int(sum(bin(int(x)).count("1") for x in w5))))
+    boots = []
+    for hint in (25, 1000, 18000, 10**6, 10**10, 10**12 + 7):
+        e, f = ref.bootstrap(hint)
+        boots.append(dict(hint=hint, frontier=f, n=int(e.size), first=[int(x) for x in e[:5]],
+                          last=int(e[-1]), fnv=fnv1a64(e.astype("<u8").tobytes())))
+    with open(os.path.join(GOLDEN, "reference_segments.json"), "w") as f:
+        json.dump(dict(meta=dict(source="reference", entry="SegmentBitmap + sieve_segment, "
+                                 "BasePrimeStore::bootstrap", generator="oracle/gen_golden.py"),
+                       segments=segs, bootstrap=boots), f)
 
     big = {}
     if a.big:

@@ -157,9 +157,10 @@ class Reference:
         L.wsref_naive_sieve.argtypes = [u64, P64, u64, P64]
         L.wsref_bootstrap.argtypes = [u64, P64, u64, P64, P64]
         L.wsref_hw_threads.restype = C.c_uint
+        L.wsref_sieve_segment.argtypes = [u64, u64, P64, P64]
         for f in ("wsref_run_count", "wsref_run_checks", "wsref_run_values", "wsref_range",
                   "wsref_range_values", "wsref_intervals", "wsref_start_offsets",
-                  "wsref_naive_sieve", "wsref_bootstrap"):
+                  "wsref_naive_sieve", "wsref_bootstrap", "wsref_sieve_segment"):
             getattr(L, f).restype = C.c_int
 
     @staticmethod
@@ -224,6 +225,13 @@ class Reference:
         self._ok(self.lib.wsref_intervals(_p64(Ls), n, width, threads, seg_slots, _p32(counts),
                                           _p64(sums), _p64(xors), C.byref(ms)), "intervals")
         return counts, sums, xors, ms.value
+
+    def sieve_segment(self, start: int, length: int):
+        nw = (length + 63) // 64
+        r1 = np.zeros(nw, np.uint64)
+        r5 = np.zeros(nw, np.uint64)
+        self._ok(self.lib.wsref_sieve_segment(start, length, _p64(r1), _p64(r5)), "sieve_segment")
+        return r1, r5
 
     def start_offsets(self, p: int, start: int):
         a, b = u64(), u64()

@@ -322,6 +322,21 @@ int wsref_bootstrap(uint64_t hint, uint64_t* out, uint64_t cap, uint64_t* n, uin
   });
 }
 
+// SegmentBitmap(start, len) + sieve_segment with a store bootstrapped past
+// the segment end: the raw FlagArray words of both classes (segment.hpp:75).
+int wsref_sieve_segment(uint64_t start, uint64_t len, uint64_t* r1, uint64_t* r5) {
+  return guarded([&] {
+    const BasePrimeStore base =
+        BasePrimeStore::bootstrap(std::max<uint64_t>(25, start + 6 * len));
+    SegmentBitmap seg(start, len);
+    sieve_segment(seg, base);
+    auto w1 = seg.marks(ResidueClass::R1).bit_words();
+    auto w5 = seg.marks(ResidueClass::R5).bit_words();
+    std::memcpy(r1, w1.data(), w1.size() * 8);
+    std::memcpy(r5, w5.data(), w5.size() * 8);
+  });
+}
+
 unsigned wsref_hw_threads(void) { return static_cast<unsigned>(nthreads_or_hw(0)); }
 
 }  // extern "C"

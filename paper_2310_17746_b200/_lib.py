@@ -19,7 +19,7 @@ EXPORTS = (
     "ws_opts_default", "ws_status_name", "ws_ctx_create", "ws_ctx_destroy", "ws_last_error",
     "ws_ctx_stream", "ws_last_timing", "ws_count_range", "ws_enumerate_range",
     "ws_count_intervals", "ws_prime_count_bound", "ws_partition", "ws_start_offsets",
-    "ws_isqrt", "ws_version",
+    "ws_isqrt", "ws_version", "ws_base_primes", "ws_sieve_segment",
 )
 
 WS_WANT_CHECKS = 0x1
@@ -68,6 +68,8 @@ def _load(path: str = LIB_PATH) -> C.CDLL:
         "ws_partition": (C.c_int, [u64, u64, u32, u32, u32, P64, P64]),
         "ws_start_offsets": (C.c_int, [u64, u64, P64, P64]),
         "ws_isqrt": (u64, [u64]),
+        "ws_base_primes": (C.c_int, [vp, u64, u32, vp, u64, P64]),
+        "ws_sieve_segment": (C.c_int, [vp, u64, u64, u32, vp, vp]),
         "ws_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():

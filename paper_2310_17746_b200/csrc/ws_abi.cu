@@ -119,6 +119,7 @@ struct ws_ctx {
   DevBuf<unsigned long long> tab_m;
   DevBuf<double> tab_inv;
 
+  uint32_t* words_out[2] = {nullptr, nullptr};  // SegmentBitmap export (ws_sieve_segment)
   uint32_t n_below_S = 0;  // table primes (>= 37) below S: in-kernel; the rest bucketed
   uint32_t n_wc = 161;     // table primes below the warp-cooperative limit (1024)
   size_t bucket_budget = 1ull << 30;  // bytes of bucket lists per window
@@ -262,6 +263,8 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.status = c->status.ptr;
   p.out = out;
   p.out_cap = out_cap;
+  p.words1 = c->words_out[0];
+  p.words5 = c->words_out[1];
   const uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps[mode];
   // Buckets pay off only when most large primes are far above S (c4: up to
   // 120 S, c5: 16 S); up to a few S (c3: 3.8 S) the per-(prime, segment)
@@ -769,6 +772,72 @@ ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags
     if (chk.count > cap) throw Fail{WS_CAPACITY, "output capacity below the prime count"};
   });
   return st;
+}
+
+ws_status ws_base_primes(ws_ctx* ctx, uint64_t B, uint32_t flags, uint64_t* out, uint64_t cap,
+                         uint64_t* n) {
+  return guarded(ctx, [&] {
+    if (!n) throw Fail{WS_BAD_CONFIG, "null n"};
+    *n = 0;
+    if (B < 2) throw Fail{WS_EMPTY_RANGE, "no primes below 2"};  // wheel.cpp:41
+    if (B > 0xFFFFFFFFull) throw Fail{WS_CAPACITY, "base bound above 2^32"};
+    // the store's entries are the wheel primes 5 <= p <= B (base_store.cpp:34-42):
+    // enumerate [5, B + 1) on the device
+    if (B < 5) return;
+    ws_checks chk{};
+    const uint32_t f = (flags & (WS_OUT_DEVICE | WS_FRESH_BASE));
+    const ws_status st = ws_enumerate_range(ctx, 5, B + 1, f, out, cap, n, &chk);
+    if (st != WS_OK) throw Fail{st, ctx->err};
+  });
+}
+
+ws_status ws_sieve_segment(ws_ctx* ctx, uint64_t start, uint64_t len, uint32_t flags,
+                           uint64_t* r1_words, uint64_t* r5_words) {
+  return guarded(ctx, [&] {
+    // SegmentBitmap checks, segment.cpp:101-110
+    if (start % 6 != 0) throw Fail{WS_ALIGNMENT, "segment start is not a multiple of 6"};
+    if (len == 0) throw Fail{WS_DOMAIN, "segment must span at least one wheel index"};
+    if (len > (kMaxSegmentEnd - start) / 6)
+      throw Fail{WS_OVERFLOW, "segment end exceeds the 64-bit value range"};
+    if (!r1_words || !r5_words) throw Fail{WS_BAD_CONFIG, "null output"};
+    const uint64_t end = start + 6 * len;
+    ensure_base(ctx, isqrt_u64(end - 1), flags & WS_FRESH_BASE);
+    ctx->h_jobs.assign(1, make_job(start, end, ctx->S, 0));
+    const uint64_t nseg = ctx->h_jobs[0].nseg;
+    const uint64_t words32 = nseg * (ctx->S / 32);
+    const uint64_t out64 = (len + 63) / 64;
+    const bool dev_out = flags & WS_OUT_DEVICE;
+    DevBuf<uint32_t> tmp;
+    tmp.reserve(2 * words32 + 2, "bitmap words");
+    ctx->words_out[0] = tmp.ptr;
+    ctx->words_out[1] = tmp.ptr + words32;
+    try {
+      run_sieve(ctx, wsk::kCount, nullptr, nullptr, 0, true);
+    } catch (...) {
+      ctx->words_out[0] = ctx->words_out[1] = nullptr;
+      tmp.release();
+      throw;
+    }
+    ctx->words_out[0] = ctx->words_out[1] = nullptr;
+    // uint32 LSB-first words are byte-identical to FlagArray's uint64 words
+    const cudaMemcpyKind k = dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    ck(cudaMemcpyAsync(r1_words, tmp.ptr, out64 * 8, k, ctx->stream), "r1 words");
+    ck(cudaMemcpyAsync(r5_words, tmp.ptr + words32, out64 * 8, k, ctx->stream), "r5 words");
+    fetch_results(ctx, 1);
+    tmp.release();
+    // sieve_segment leaves the value 1 set; callers clear it (engine.cpp:244)
+    if (start == 0) {
+      if (dev_out) {
+        uint64_t w0 = 0;
+        ck(cudaMemcpy(&w0, r1_words, 8, cudaMemcpyDeviceToHost), "w0");
+        w0 |= 1;
+        ck(cudaMemcpy(r1_words, &w0, 8, cudaMemcpyHostToDevice), "w0");
+      } else {
+        r1_words[0] |= 1;
+      }
+    }
+    ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
+  });
 }
 
 ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64_t width,

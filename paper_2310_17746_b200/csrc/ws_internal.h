@@ -66,6 +66,8 @@ struct SieveParams {
   unsigned long long* status;        // enumeration look-back words (zeroed)
   unsigned long long* out;           // enumeration output (after 2 and 3)
   unsigned long long out_cap;
+  uint32_t* words1;                  // nullable (count modes): survivor flag words of
+  uint32_t* words5;                  // each class, segment s at word s * S / 32
 };
 
 size_t sieve_smem_bytes(uint32_t S, int mode);

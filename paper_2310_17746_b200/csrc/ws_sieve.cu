@@ -511,6 +511,14 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
     if (P.bucket != nullptr && threadIdx.x == 0) P.bcount[si.s - P.s_begin] = 0;
 
     const uint64_t vbase = 6 * si.ks;
+    if (MODE != kEnumerate && P.words1 != nullptr) {  // SegmentBitmap export
+      const uint64_t wb = si.s * (P.S / 32);  // single-job launches
+      const uint32_t nw = (si.len + 63) / 64 * 2;  // whole uint64 FlagArray words
+      for (uint32_t w = threadIdx.x; w < nw; w += kThreads) {
+        P.words1[wb + w] = ~bm1[w];
+        P.words5[wb + w] = ~bm5[w];
+      }
+    }
     if (MODE != kEnumerate) {
       uint32_t cnt = 0;
       unsigned long long lg = 0, sum = 0, xr = 0;

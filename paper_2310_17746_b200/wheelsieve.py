@@ -81,6 +81,26 @@ def isqrt(n: int) -> int:
     return int(lib.ws_isqrt(n))
 
 
+def ceil_sqrt(n: int) -> int:  # wheel.cpp:35-38
+    r = isqrt(n)
+    return r if r * r == n else r + 1
+
+
+R1, R5 = 1, 5  # ResidueClass (wheel.hpp:13) as the residue itself
+
+
+def value_of(index: int, residue: int) -> int:  # wheel.cpp:8-13
+    if index > K_MAX_WHEEL_INDEX:
+        raise Error(Errc.Overflow, f"wheel index {index} exceeds the 64-bit value range")
+    return 6 * index + residue
+
+
+def coord_of(n: int):  # wheel.cpp:15-23 -> (index, residue)
+    if n % 6 not in (1, 5):
+        raise Error(Errc.NotOnWheel, f"{n} is divisible by 2 or 3, not on the wheel")
+    return n // 6, n % 6
+
+
 def start_offsets(p: int, segment_start: int):
     """wheel.cpp:96-106 -> (id1, id5)."""
     a, b = C.c_uint64(), C.c_uint64()
@@ -221,6 +241,24 @@ class Sieve:
                                       xors.ctypes.data if xors is not None else None),
                self._h, "count_intervals")
         return counts, sums, xors
+
+    def base_primes(self, B: int, fresh_base: bool = False) -> np.ndarray:
+        """BasePrimeStore::bootstrap entries: wheel primes 5 <= p <= B (device-sieved)."""
+        out = np.empty(max(1, prime_count_bound(0, B + 1)), np.uint64)
+        n = C.c_uint64()
+        _check(lib.ws_base_primes(self._h, B, WS_FRESH_BASE if fresh_base else 0,
+                                  out.ctypes.data, out.size, C.byref(n)), self._h, "base_primes")
+        return out[: n.value].copy()
+
+    def sieve_segment(self, start: int, length: int):
+        """SegmentBitmap(start, length) after sieve_segment: (r1_words, r5_words),
+        uint64 FlagArray Bit layout, value 1 left set like the reference."""
+        nw = (length + 63) // 64
+        r1 = np.zeros(max(1, nw), np.uint64)
+        r5 = np.zeros(max(1, nw), np.uint64)
+        _check(lib.ws_sieve_segment(self._h, start, length, 0, r1.ctypes.data, r5.ctypes.data),
+               self._h, "sieve_segment")
+        return r1[:nw], r5[:nw]
 
     def num_segments(self, L: int, R: int) -> int:
         if R <= L:

@@ -244,6 +244,34 @@ int main() {
     CHECK(counts[0] == 628'905 && sums[0] == 238'210'012'871'732'589ull);
   }
 
+  {  // test_segment.cpp:135-184 against the SegmentBitmap mirror
+    const SegmentFlags seg = dev.sieve_segment(12000, 1000);
+    CHECK(!seg.flag_for(14443) && !seg.flag_for(14417) && seg.flag_for(12007));
+    const auto all = textbook(18000);
+    std::vector<uint64_t> sl;
+    for (uint64_t p : all)
+      if (p >= 12000) sl.push_back(p);
+    CHECK(seg.surviving() == sl);
+    const SegmentFlags first = dev.sieve_segment(0, 1000);
+    CHECK(first.flag_for(1));  // not a multiple of anything; callers clear it
+    const SegmentFlags one = dev.sieve_segment(10200, 1);
+    CHECK(!one.flag_for(10201) && !one.flag_for(10205));
+    const SegmentFlags sq = dev.sieve_segment(168, 1);
+    CHECK(!sq.flag_for(169) && sq.flag_for(173));
+    EXPECT_ERROR(Errc::Alignment, dev.sieve_segment(10, 5));
+    EXPECT_ERROR(Errc::Domain, dev.sieve_segment(12, 0));
+    EXPECT_ERROR(Errc::Overflow, dev.sieve_segment(kMaxSegmentEnd, 1));
+  }
+
+  {  // test_base_store.cpp:29-38 and test_wheel.cpp:30-74
+    const auto b = dev.base_primes(ceil_sqrt(1'000'000));
+    CHECK(b.size() == 166 && b.front() == 5 && b.back() == 997);
+    CHECK(value_of({0, ResidueClass::R1}) == 1 && value_of({0, ResidueClass::R5}) == 5);
+    CHECK((coord_of(25) == WheelCoord{4, ResidueClass::R1}));
+    EXPECT_ERROR(Errc::NotOnWheel, coord_of(4));
+    EXPECT_ERROR(Errc::Overflow, value_of({kMaxWheelIndex + 1, ResidueClass::R1}));
+  }
+
   std::printf(g_fail ? "[FAIL] %d failures\n" : "[PASS] all checks\n", g_fail);
   return g_fail;
 }

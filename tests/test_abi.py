@@ -84,3 +84,23 @@ def test_prime_count_bound_is_upper_bound(golden):
     for rec in golden["windows"] + [dict(L=0, R=p["limit"] + 1, count=p["count"])
                                     for p in golden["prefixes"]]:
         assert ws.prime_count_bound(rec["L"], rec["R"]) >= rec["count"]
+
+
+def test_wheel_coordinates():  # test_wheel.cpp:30-74
+    import numpy as np
+    import paper_2310_17746_b200 as ws
+    assert ws.value_of(0, ws.R1) == 1 and ws.value_of(0, ws.R5) == 5
+    assert ws.coord_of(25) == (4, 1) and ws.coord_of(35) == (5, 5)
+    rng = np.random.default_rng(42)
+    for _ in range(2000):
+        k = int(rng.integers(0, ws.wheelsieve.K_MAX_WHEEL_INDEX))
+        for r in (ws.R1, ws.R5):
+            assert ws.coord_of(ws.value_of(k, r)) == (k, r)
+    for bad in (0, 2, 3, 4, 6):
+        with pytest.raises(ws.Error) as e:
+            ws.coord_of(bad)
+        assert e.value.code == ws.Errc.NotOnWheel
+    with pytest.raises(ws.Error) as e:
+        ws.value_of(ws.wheelsieve.K_MAX_WHEEL_INDEX + 1, ws.R1)
+    assert e.value.code == ws.Errc.Overflow
+    assert [ws.ceil_sqrt(n) for n in (0, 1, 2, 4, 5, 24, 25, 26)] == [0, 1, 2, 2, 3, 5, 5, 6]

@@ -236,3 +236,47 @@ def test_top_of_64bit_range_vs_miller_rabin(sieve, L, W):
     assert cc.count == len(expected) == n
     assert cc.sum == sum(expected) % 2**64 and cc.xor == c.xor
     assert cc.largest == (expected[-1] if expected else 0)
+
+
+def test_sieve_segment_flag_words_match_reference():
+    """ws_sieve_segment returns exactly the reference's FlagArray words after
+    SegmentBitmap + sieve_segment (segment.cpp:93-188), golden from the
+    reference library (tests/golden/reference_segments.json)."""
+    import paper_2310_17746_b200 as ws
+    from oracle.oracle import fnv1a64
+    g = load_golden("reference_segments.json")
+    for sv in (ws.Sieve(), ws.Sieve(segment_slots=1 << 12)):
+        for rec in g["segments"]:
+            r1, r5 = sv.sieve_segment(rec["start"], rec["len"])
+            if rec["r1"] is not None:
+                assert [int(x) for x in r1] == rec["r1"], (rec["start"], rec["len"])
+                assert [int(x) for x in r5] == rec["r5"], (rec["start"], rec["len"])
+            assert fnv1a64(r1.astype("<u8").tobytes()) == rec["fnv_r1"]
+            assert fnv1a64(r5.astype("<u8").tobytes()) == rec["fnv_r5"]
+        sv.close()
+
+
+def test_sieve_segment_errors(sieve):
+    import paper_2310_17746_b200 as ws
+    for args, code in (((10, 5), ws.Errc.Alignment), ((12, 0), ws.Errc.Domain),
+                       ((ws.wheelsieve.K_MAX_SEGMENT_END, 1), ws.Errc.Overflow)):
+        with pytest.raises(ws.Error) as e:
+            sieve.sieve_segment(*args)
+        assert e.value.code == code  # test_segment.cpp:100-120
+
+
+def test_base_primes_match_bootstrap(sieve):
+    """ws_base_primes(B) == BasePrimeStore::bootstrap(hint).entries with
+    B = ceil_sqrt(hint) (base_store.cpp:34-42)."""
+    import paper_2310_17746_b200 as ws
+    from oracle.oracle import fnv1a64
+    g = load_golden("reference_segments.json")
+    for rec in g["bootstrap"]:
+        assert ws.ceil_sqrt(rec["hint"]) == rec["frontier"]
+        e = sieve.base_primes(rec["frontier"])
+        assert e.size == rec["n"] and [int(x) for x in e[:5]] == rec["first"]
+        assert int(e[-1]) == rec["last"] and fnv1a64(e.astype("<u8").tobytes()) == rec["fnv"]
+    assert sieve.base_primes(4).size == 0
+    with pytest.raises(ws.Error) as e:
+        sieve.base_primes(1)
+    assert e.value.code == ws.Errc.EmptyRange
