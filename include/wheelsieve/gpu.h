@@ -16,6 +16,8 @@
  *   start_offsets (paper Table 1)                 wheel.cpp:96-106  -> ws_start_offsets
  *   BasePrimeStore::bootstrap / naive_sieve       base_store.cpp:34, wheel.cpp:40 -> ws_base_primes
  *   SegmentBitmap + sieve_segment (flag arrays)   segment.cpp:93-188 -> ws_sieve_segment
+ *   ChunkedFileSink / read_back / verify_store    sink.cpp:39-344 -> ws_store_range,
+ *                                                 ws_read_back, ws_verify_store
  *   isqrt                                         wheel.cpp:25-33   -> ws_isqrt
  *
  * Conventions (mirroring the reference):
@@ -141,6 +143,25 @@ ws_status ws_base_primes(ws_ctx* ctx, uint64_t B, uint32_t flags, uint64_t* out,
  * WS_OVERFLOW (end beyond the 64-bit range). */
 ws_status ws_sieve_segment(ws_ctx* ctx, uint64_t start, uint64_t len, uint32_t flags,
                            uint64_t* r1_words, uint64_t* r5_words);
+
+/* Chunked prime store (ChunkedFileSink, sink.hpp:68-141):
+ * enumerate [L, R) on the device and write primes_%05llu.{txt,bin} chunk
+ * files of primes_per_file values plus manifest.json (count/min/max/crc32 per
+ * file, format, total_count, frontier = R), byte-identical to the reference
+ * CLI's `sieve --out` for [0, limit + 1).  Binary chunks' CRC-32s are
+ * computed on the device.  WS_DOMAIN if primes_per_file == 0, WS_IO on
+ * filesystem errors. */
+#define WS_STORE_TEXT 0u
+#define WS_STORE_BINARY 1u
+ws_status ws_store_range(ws_ctx* ctx, uint64_t L, uint64_t R, const char* dir, uint32_t format,
+                         uint64_t primes_per_file, uint64_t* n_out);
+/* read_back (sink.cpp:306-321): primes in [lo, hi) of a store, every touched
+ * file verified against its crc32 and count; WS_BEYOND_FRONTIER if hi exceeds
+ * the recorded frontier, WS_CHECKSUM_MISMATCH / WS_BAD_MANIFEST / WS_IO. */
+ws_status ws_read_back(const char* dir, uint64_t lo, uint64_t hi, uint64_t* out, uint64_t cap,
+                       uint64_t* n_out);
+/* verify_store (sink.cpp:323-342): every file vs the manifest, global order. */
+ws_status ws_verify_store(const char* dir);
 
 /* Upper bound on the number of primes in [L, R) (capacity helper). */
 uint64_t ws_prime_count_bound(uint64_t L, uint64_t R);

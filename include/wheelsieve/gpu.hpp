@@ -288,6 +288,16 @@ class Device {
     return f;
   }
 
+  // ChunkedFileSink-format store of the primes of [L, R) (frontier R).
+  uint64_t store_range(uint64_t L, uint64_t R, const std::string& dir, bool binary,
+                       uint64_t primes_per_file = 125'000'000) {
+    uint64_t n = 0;
+    check(ws_store_range(ctx_, L, R, dir.c_str(), binary ? WS_STORE_BINARY : WS_STORE_TEXT,
+                         primes_per_file, &n),
+          ctx_, "ws_store_range");
+    return n;
+  }
+
   void count_intervals(std::span<const uint64_t> Ls, uint64_t width, std::vector<uint32_t>& counts,
                        std::vector<uint64_t>* sums = nullptr,
                        std::vector<uint64_t>* xors = nullptr) {
@@ -302,6 +312,77 @@ class Device {
  private:
   ws_ctx* ctx_ = nullptr;
   uint32_t slots_ = 0;
+};
+
+// read_back / verify_store (sink.cpp:306-342) over a chunked store.
+inline std::vector<uint64_t> read_back(const std::string& dir, uint64_t lo, uint64_t hi) {
+  uint64_t n = 0;
+  const ws_status s = ws_read_back(dir.c_str(), lo, hi, nullptr, 0, &n);
+  if (s != WS_OK && s != WS_CAPACITY) check(s, nullptr, "read_back");
+  std::vector<uint64_t> v(n);
+  check(ws_read_back(dir.c_str(), lo, hi, v.data(), v.size(), &n), nullptr, "read_back");
+  return v;
+}
+inline void verify_store(const std::string& dir) {
+  check(ws_verify_store(dir.c_str()), nullptr, "verify_store");
+}
+
+// Unbounded incremental enumerator (stream.hpp:16-46): 2, 3, then every wheel
+// prime ascending; the device sieves `block` values per refill (a multiple of
+// 6 * segment_wheel_len) and the base primes grow with it (the store's
+// incremental growth, base_store.cpp:44-76).  nullopt once the 64-bit range
+// is exhausted (overflowed() then stays true).
+class PrimeStream {
+ public:
+  explicit PrimeStream(uint64_t segment_wheel_len, Device& dev,
+                       uint64_t segments_per_refill = 64)
+      : dev_(dev), wheel_len_(segment_wheel_len) {
+    if (segment_wheel_len == 0)
+      throw Error(Errc::Domain, "segment must span at least one wheel index");
+    if (segment_wheel_len > kMaxSegmentEnd / 6)
+      throw Error(Errc::Overflow, "segment span exceeds the 64-bit value range");
+    span_ = 6 * segment_wheel_len * std::max<uint64_t>(1, segments_per_refill);
+    if (span_ / 6 / segments_per_refill != segment_wheel_len) span_ = 6 * segment_wheel_len;
+  }
+
+  std::optional<uint64_t> next() {
+    if (prelude_ < 2) return prelude_++ == 0 ? 2 : 3;
+    while (pos_ == buf_.size()) {
+      if (overflowed_) return std::nullopt;
+      refill();
+    }
+    return buf_[pos_++];
+  }
+  bool overflowed() const { return overflowed_; }
+  uint64_t segment_wheel_len() const { return wheel_len_; }
+
+  static bool segment_would_overflow(uint64_t start, uint64_t wheel_len) {  // stream.cpp:24-26
+    return start >= kMaxSegmentEnd || wheel_len > (kMaxSegmentEnd - start) / 6;
+  }
+
+ private:
+  void refill() {
+    if (segment_would_overflow(next_start_, wheel_len_)) {
+      overflowed_ = true;
+      return;
+    }
+    uint64_t end = next_start_ + span_;
+    if (segment_would_overflow(next_start_, span_ / 6)) {
+      end = next_start_ + 6 * wheel_len_ * ((kMaxSegmentEnd - next_start_) / (6 * wheel_len_));
+    }
+    buf_ = dev_.enumerate_range(std::max<uint64_t>(next_start_, 4), end);
+    pos_ = 0;
+    next_start_ = end;
+  }
+
+  Device& dev_;
+  uint64_t wheel_len_;
+  uint64_t span_ = 0;
+  uint64_t next_start_ = 0;
+  std::vector<uint64_t> buf_;
+  size_t pos_ = 0;
+  uint8_t prelude_ = 0;
+  bool overflowed_ = false;
 };
 
 // --------------------------------------------------------------- engine ----

@@ -158,9 +158,13 @@ class Reference:
         L.wsref_bootstrap.argtypes = [u64, P64, u64, P64, P64]
         L.wsref_hw_threads.restype = C.c_uint
         L.wsref_sieve_segment.argtypes = [u64, u64, P64, P64]
+        L.wsref_store_run.argtypes = [u64, C.c_uint, C.c_char_p, C.c_int, u64]
+        L.wsref_read_back.argtypes = [C.c_char_p, u64, u64, P64, u64, P64]
+        L.wsref_verify_store.argtypes = [C.c_char_p]
         for f in ("wsref_run_count", "wsref_run_checks", "wsref_run_values", "wsref_range",
                   "wsref_range_values", "wsref_intervals", "wsref_start_offsets",
-                  "wsref_naive_sieve", "wsref_bootstrap", "wsref_sieve_segment"):
+                  "wsref_naive_sieve", "wsref_bootstrap", "wsref_sieve_segment",
+                  "wsref_store_run", "wsref_read_back", "wsref_verify_store"):
             getattr(L, f).restype = C.c_int
 
     @staticmethod
@@ -232,6 +236,23 @@ class Reference:
         r5 = np.zeros(nw, np.uint64)
         self._ok(self.lib.wsref_sieve_segment(start, length, _p64(r1), _p64(r5)), "sieve_segment")
         return r1, r5
+
+    def store_run(self, limit: int, dir: str, binary: bool, primes_per_file: int,
+                  threads: int = 0):
+        self._ok(self.lib.wsref_store_run(limit, threads, dir.encode(), int(binary),
+                                          primes_per_file), "store_run")
+
+    def read_back(self, dir: str, lo: int, hi: int):
+        """Returns (status, values): status 0 ok, else 1 + Errc."""
+        cap = max(16, hi - lo)
+        cap = min(cap, 1 << 26)
+        out = np.empty(cap, np.uint64)
+        n = u64()
+        rc = self.lib.wsref_read_back(dir.encode(), lo, hi, _p64(out), cap, C.byref(n))
+        return rc, out[: min(cap, n.value)].copy()
+
+    def verify_store(self, dir: str) -> int:
+        return self.lib.wsref_verify_store(dir.encode())
 
     def start_offsets(self, p: int, start: int):
         a, b = u64(), u64()

@@ -337,6 +337,34 @@ int wsref_sieve_segment(uint64_t start, uint64_t len, uint64_t* r1, uint64_t* r5
   });
 }
 
+// The reference CLI's store path (tools/wheelsieve.cpp:139-168): run() over
+// [0, limit] into a ChunkedFileSink, set_frontier(sieved_to), flush.
+int wsref_store_run(uint64_t limit, unsigned threads, const char* dir, int binary,
+                    uint64_t primes_per_file) {
+  return guarded([&] {
+    ChunkedFileSink sink(ChunkedFileOptions{dir, primes_per_file,
+                                            binary ? FileFormat::Binary : FileFormat::Text});
+    const unsigned t = static_cast<unsigned>(nthreads_or_hw(threads));
+    SieveConfig cfg{limit, t, round_segment_span(6 * (1u << 18) * t, t), FlagWidth::Bit, &sink};
+    const SieveReport r = run(cfg);
+    sink.set_frontier(r.sieved_to);
+    sink.flush();
+  });
+}
+
+int wsref_read_back(const char* dir, uint64_t lo, uint64_t hi, uint64_t* out, uint64_t cap,
+                    uint64_t* n) {
+  return guarded([&] {
+    const std::vector<uint64_t> v = read_back(dir, lo, hi);
+    *n = v.size();
+    std::memcpy(out, v.data(), std::min<uint64_t>(cap, v.size()) * 8);
+  });
+}
+
+int wsref_verify_store(const char* dir) {
+  return guarded([&] { verify_store(dir); });
+}
+
 unsigned wsref_hw_threads(void) { return static_cast<unsigned>(nthreads_or_hw(0)); }
 
 }  // extern "C"

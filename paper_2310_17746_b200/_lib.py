@@ -19,7 +19,8 @@ EXPORTS = (
     "ws_opts_default", "ws_status_name", "ws_ctx_create", "ws_ctx_destroy", "ws_last_error",
     "ws_ctx_stream", "ws_last_timing", "ws_count_range", "ws_enumerate_range",
     "ws_count_intervals", "ws_prime_count_bound", "ws_partition", "ws_start_offsets",
-    "ws_isqrt", "ws_version", "ws_base_primes", "ws_sieve_segment",
+    "ws_isqrt", "ws_version", "ws_base_primes", "ws_sieve_segment", "ws_store_range",
+    "ws_read_back", "ws_verify_store",
 )
 
 WS_WANT_CHECKS = 0x1
@@ -70,6 +71,9 @@ def _load(path: str = LIB_PATH) -> C.CDLL:
         "ws_isqrt": (u64, [u64]),
         "ws_base_primes": (C.c_int, [vp, u64, u32, vp, u64, P64]),
         "ws_sieve_segment": (C.c_int, [vp, u64, u64, u32, vp, vp]),
+        "ws_store_range": (C.c_int, [vp, u64, u64, C.c_char_p, u32, u64, P64]),
+        "ws_read_back": (C.c_int, [C.c_char_p, u64, u64, vp, u64, P64]),
+        "ws_verify_store": (C.c_int, [C.c_char_p]),
         "ws_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():

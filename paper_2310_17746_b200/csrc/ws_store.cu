@@ -1,0 +1,453 @@
+// Chunked prime store: the reference's ChunkedFileSink on-disk
+// format (sink.hpp:68-141, sink.cpp:39-344) written from device-enumerated
+// primes, byte-identical to what the reference CLI writes for the same range
+// (`wheelsieve sieve --out`, tools/wheelsieve.cpp:139-168):
+//   primes_%05llu.txt  one decimal value per line        (sink.cpp:66-73)
+//   primes_%05llu.bin  8-byte little-endian words        (sink.cpp:74-78)
+//   manifest.json      nlohmann dump(2), sorted keys, crc32 as 8 hex digits,
+//                      written to manifest.json.tmp then renamed (sink.cpp:242-277)
+// The binary chunks' CRC-32s are computed on the device (ws_crc.cu) over the
+// enumerated words and combined per file with zlib's crc32_combine.
+// read_back / verify_store (sink.cpp:306-342) read either implementation's stores.
+#include <cuda_runtime.h>
+#include <zlib.h>
+
+#include <algorithm>
+#include <charconv>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include "wheelsieve/gpu.h"
+#include "ws_internal.h"
+
+namespace fs = std::filesystem;
+
+namespace {
+
+struct StoreFail {
+  ws_status code;
+  std::string msg;
+};
+
+struct FileEntry {
+  std::string name;
+  uint64_t count = 0, min = 0, max = 0;
+  uint32_t crc32 = 0;
+};
+
+struct Manifest {
+  int format = 0;  // 0 text, 1 binary
+  uint64_t primes_per_file = 0, frontier = 0, total_count = 0;
+  std::vector<FileEntry> files;
+};
+
+std::string chunk_name(uint64_t seq, int format) {  // sink.cpp:48-53
+  char buf[48];
+  std::snprintf(buf, sizeof buf, "primes_%05llu.%s", static_cast<unsigned long long>(seq),
+                format ? "bin" : "txt");
+  return buf;
+}
+
+std::string crc_hex(uint32_t crc) {  // sink.cpp:55-59
+  char buf[16];
+  std::snprintf(buf, sizeof buf, "%08x", crc);
+  return buf;
+}
+
+// nlohmann::json::dump(2) of the manifest object (keys sorted), plus '\n'.
+std::string manifest_text(const Manifest& m) {
+  std::string s = "{\n  \"files\": [";
+  for (size_t i = 0; i < m.files.size(); ++i) {
+    const FileEntry& f = m.files[i];
+    s += i ? ",\n    {\n" : "\n    {\n";
+    s += "      \"count\": " + std::to_string(f.count) + ",\n";
+    s += "      \"crc32\": \"" + crc_hex(f.crc32) + "\",\n";
+    s += "      \"max\": " + std::to_string(f.max) + ",\n";
+    s += "      \"min\": " + std::to_string(f.min) + ",\n";
+    s += "      \"name\": \"" + f.name + "\"\n    }";
+  }
+  s += m.files.empty() ? "],\n" : "\n  ],\n";
+  s += std::string("  \"format\": \"") + (m.format ? "binary" : "text") + "\",\n";
+  s += "  \"frontier\": " + std::to_string(m.frontier) + ",\n";
+  s += "  \"primes_per_file\": " + std::to_string(m.primes_per_file) + ",\n";
+  s += "  \"total_count\": " + std::to_string(m.total_count) + "\n}\n";
+  return s;
+}
+
+// ---- minimal JSON reader for the manifest schema --------------------------
+struct Json {
+  enum Kind { Null, Num, Str, Arr, Obj } kind = Null;
+  uint64_t num = 0;
+  std::string str;
+  std::vector<Json> arr;
+  std::vector<std::pair<std::string, Json>> obj;
+  const Json* get(const char* k) const {
+    for (const auto& kv : obj)
+      if (kv.first == k) return &kv.second;
+    return nullptr;
+  }
+};
+
+struct Parser {
+  const char* p;
+  const char* e;
+  void ws() {
+    while (p < e && (*p == ' ' || *p == '\n' || *p == '\r' || *p == '\t')) ++p;
+  }
+  [[noreturn]] void bad() { throw StoreFail{WS_BAD_MANIFEST, "manifest.json unreadable"}; }
+  std::string string() {
+    if (p >= e || *p != '"') bad();
+    std::string s;
+    for (++p; p < e && *p != '"'; ++p) {
+      if (*p == '\\') {
+        if (++p >= e) bad();
+      }
+      s.push_back(*p);
+    }
+    if (p >= e) bad();
+    ++p;
+    return s;
+  }
+  Json value() {
+    ws();
+    if (p >= e) bad();
+    Json j;
+    if (*p == '{') {
+      j.kind = Json::Obj;
+      ++p;
+      ws();
+      if (p < e && *p == '}') {
+        ++p;
+        return j;
+      }
+      for (;;) {
+        ws();
+        std::string k = string();
+        ws();
+        if (p >= e || *p != ':') bad();
+        ++p;
+        j.obj.emplace_back(std::move(k), value());
+        ws();
+        if (p < e && *p == ',') {
+          ++p;
+          continue;
+        }
+        if (p < e && *p == '}') {
+          ++p;
+          return j;
+        }
+        bad();
+      }
+    }
+    if (*p == '[') {
+      j.kind = Json::Arr;
+      ++p;
+      ws();
+      if (p < e && *p == ']') {
+        ++p;
+        return j;
+      }
+      for (;;) {
+        j.arr.push_back(value());
+        ws();
+        if (p < e && *p == ',') {
+          ++p;
+          continue;
+        }
+        if (p < e && *p == ']') {
+          ++p;
+          return j;
+        }
+        bad();
+      }
+    }
+    if (*p == '"') {
+      j.kind = Json::Str;
+      j.str = string();
+      return j;
+    }
+    if (*p >= '0' && *p <= '9') {
+      j.kind = Json::Num;
+      auto [n, ec] = std::from_chars(p, e, j.num);
+      if (ec != std::errc{}) bad();
+      p = n;
+      return j;
+    }
+    bad();
+  }
+};
+
+Manifest load_manifest(const fs::path& dir) {  // sink.cpp:113-159
+  std::ifstream in(dir / "manifest.json", std::ios::binary);
+  if (!in) throw StoreFail{WS_BAD_MANIFEST, "no manifest.json under " + dir.string()};
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  Parser ps{text.data(), text.data() + text.size()};
+  const Json j = ps.value();
+  auto need = [&](const Json* v, Json::Kind k, const char* what) {
+    if (!v || v->kind != k)
+      throw StoreFail{WS_BAD_MANIFEST, std::string("manifest.json incomplete: ") + what};
+    return v;
+  };
+  Manifest m;
+  const std::string fmt = need(j.get("format"), Json::Str, "format")->str;
+  if (fmt == "text")
+    m.format = 0;
+  else if (fmt == "binary")
+    m.format = 1;
+  else
+    throw StoreFail{WS_BAD_MANIFEST, "unknown format '" + fmt + "' in manifest"};
+  m.primes_per_file = need(j.get("primes_per_file"), Json::Num, "primes_per_file")->num;
+  m.frontier = need(j.get("frontier"), Json::Num, "frontier")->num;
+  m.total_count = need(j.get("total_count"), Json::Num, "total_count")->num;
+  for (const Json& f : need(j.get("files"), Json::Arr, "files")->arr) {
+    FileEntry fe;
+    fe.name = need(f.get("name"), Json::Str, "name")->str;
+    fe.count = need(f.get("count"), Json::Num, "count")->num;
+    fe.min = need(f.get("min"), Json::Num, "min")->num;
+    fe.max = need(f.get("max"), Json::Num, "max")->num;
+    const std::string crc = need(f.get("crc32"), Json::Str, "crc32")->str;
+    char* endp = nullptr;
+    fe.crc32 = static_cast<uint32_t>(std::strtoul(crc.c_str(), &endp, 16));
+    if (crc.empty() || *endp) throw StoreFail{WS_BAD_MANIFEST, "manifest.json malformed crc32"};
+    m.files.push_back(std::move(fe));
+  }
+  return m;
+}
+
+void encode_text(std::string& out, const uint64_t* v, uint64_t n) {  // sink.cpp:66-73
+  char digits[24];
+  for (uint64_t i = 0; i < n; ++i) {
+    auto [end, ec] = std::to_chars(digits, digits + sizeof digits, v[i]);
+    out.append(digits, end);
+    out.push_back('\n');
+  }
+}
+
+std::vector<uint64_t> load_and_verify(const fs::path& dir, const FileEntry& f, int format) {
+  std::ifstream in(dir / f.name, std::ios::binary);  // sink.cpp:161-183
+  if (!in) throw StoreFail{WS_BAD_MANIFEST, "manifest lists missing chunk file " + f.name};
+  std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  uLong c = ::crc32(0, Z_NULL, 0);
+  for (size_t off = 0; off < bytes.size(); off += (1u << 30))
+    c = ::crc32(c, reinterpret_cast<const Bytef*>(bytes.data() + off),
+                static_cast<uInt>(std::min<size_t>(1u << 30, bytes.size() - off)));
+  const uint32_t crc = static_cast<uint32_t>(c);
+  if (crc != f.crc32)
+    throw StoreFail{WS_CHECKSUM_MISMATCH, "chunk file " + f.name +
+                                              " does not match its recorded crc32 " +
+                                              crc_hex(f.crc32)};
+  std::vector<uint64_t> v;
+  if (format == 0) {
+    const char* p = bytes.data();
+    const char* e = p + bytes.size();
+    while (p < e) {
+      uint64_t x = 0;
+      auto [next, ec] = std::from_chars(p, e, x);
+      if (ec != std::errc{} || next == e || *next != '\n')
+        throw StoreFail{WS_BAD_MANIFEST, "chunk file " + f.name + " is not well-formed text"};
+      v.push_back(x);
+      p = next + 1;
+    }
+  } else {
+    if (bytes.size() % 8)
+      throw StoreFail{WS_BAD_MANIFEST, "chunk file " + f.name + " is not a whole number of words"};
+    v.resize(bytes.size() / 8);
+    std::memcpy(v.data(), bytes.data(), bytes.size());  // little-endian host
+  }
+  if (v.size() != f.count)
+    throw StoreFail{WS_BAD_MANIFEST, "chunk file " + f.name + " holds " + std::to_string(v.size()) +
+                                         " values, manifest says " + std::to_string(f.count)};
+  return v;
+}
+
+void write_file(const fs::path& path, const void* data, size_t bytes) {
+  std::FILE* fp = std::fopen(path.c_str(), "wb");
+  if (!fp) throw StoreFail{WS_IO, "cannot open chunk file " + path.filename().string()};
+  const size_t w = bytes ? std::fwrite(data, 1, bytes, fp) : 0;
+  const bool ok = std::fclose(fp) == 0 && w == bytes;
+  if (!ok) throw StoreFail{WS_IO, "write to " + path.filename().string() + " failed"};
+}
+
+void write_manifest(const fs::path& dir, const Manifest& m) {  // sink.cpp:242-277
+  const std::string text = manifest_text(m);
+  const fs::path tmp = dir / "manifest.json.tmp";
+  write_file(tmp, text.data(), text.size());
+  std::error_code ec;
+  fs::rename(tmp, dir / "manifest.json", ec);
+  if (ec) throw StoreFail{WS_IO, "replacing manifest failed: " + ec.message()};
+}
+
+}  // namespace
+
+// Device half of the store, called with the values of [L, R) resident on the
+// device (dev, n values): CRC-32 of every file's bytes (binary format).
+namespace wsk {
+cudaError_t launch_crc32_ranges(const void* data, const uint64_t* begin, const uint64_t* len,
+                                uint32_t n, uint32_t* out, cudaStream_t st);
+}
+
+extern "C" {
+
+ws_status ws_store_range(ws_ctx* ctx, uint64_t L, uint64_t R, const char* dir, uint32_t format,
+                         uint64_t primes_per_file, uint64_t* n_out) {
+  if (!ctx || !dir || !n_out) return WS_BAD_CONFIG;
+  *n_out = 0;
+  if (primes_per_file == 0) return WS_DOMAIN;  // sink.cpp:189-190
+  if (format > 1) return WS_BAD_CONFIG;
+  const uint64_t cap = std::max<uint64_t>(1, ws_prime_count_bound(L, R));
+  uint64_t* dev = nullptr;
+  uint64_t* host = nullptr;
+  uint64_t* d_rng = nullptr;
+  uint32_t* d_crc = nullptr;
+  auto cleanup = [&] {
+    if (dev) cudaFree(dev);
+    if (host) cudaFreeHost(host);
+    if (d_rng) cudaFree(d_rng);
+    if (d_crc) cudaFree(d_crc);
+  };
+  try {
+    std::error_code ec;
+    fs::create_directories(dir, ec);
+    if (ec) throw StoreFail{WS_IO, std::string("cannot create output directory ") + dir};
+    if (cudaMalloc(&dev, cap * 8) != cudaSuccess)
+      throw StoreFail{WS_OUT_OF_MEMORY, "store buffer"};
+    uint64_t n = 0;
+    ws_checks chk{};
+    const ws_status st = ws_enumerate_range(ctx, L, R, WS_OUT_DEVICE, dev, cap, &n, &chk);
+    if (st != WS_OK) throw StoreFail{st, ws_last_error(ctx)};
+    cudaStream_t s = static_cast<cudaStream_t>(ws_ctx_stream(ctx));
+    const uint64_t nfiles = (n + primes_per_file - 1) / primes_per_file;
+    std::vector<uint32_t> file_crc(nfiles, 0);
+    if (format == 1 && n) {
+      // ranges of <= 64 KiB inside each file, CRC'd on the device
+      constexpr uint64_t kPiece = 8192;  // values per range
+      std::vector<uint64_t> begin, len;
+      std::vector<uint64_t> first(nfiles + 1, 0);
+      for (uint64_t f = 0; f < nfiles; ++f) {
+        first[f] = begin.size();
+        const uint64_t a = f * primes_per_file, b = std::min(n, a + primes_per_file);
+        for (uint64_t x = a; x < b; x += kPiece) {
+          begin.push_back(8 * x);
+          len.push_back(8 * (std::min(b, x + kPiece) - x));
+        }
+      }
+      first[nfiles] = begin.size();
+      const uint64_t nr = begin.size();
+      if (cudaMalloc(&d_rng, 2 * nr * 8) != cudaSuccess || cudaMalloc(&d_crc, nr * 4) != cudaSuccess)
+        throw StoreFail{WS_OUT_OF_MEMORY, "crc ranges"};
+      if (cudaMemcpyAsync(d_rng, begin.data(), nr * 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+          cudaMemcpyAsync(d_rng + nr, len.data(), nr * 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+          wsk::launch_crc32_ranges(dev, d_rng, d_rng + nr, static_cast<uint32_t>(nr), d_crc, s) !=
+              cudaSuccess)
+        throw StoreFail{WS_CUDA, "crc kernel"};
+      std::vector<uint32_t> crc(nr);
+      if (cudaMemcpyAsync(crc.data(), d_crc, nr * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        throw StoreFail{WS_CUDA, "crc readback"};
+      for (uint64_t f = 0; f < nfiles; ++f) {
+        uLong c = ::crc32(0, Z_NULL, 0);
+        for (uint64_t r = first[f]; r < first[f + 1]; ++r)
+          c = ::crc32_combine(c, crc[r], static_cast<z_off_t>(len[r]));
+        file_crc[f] = static_cast<uint32_t>(c);
+      }
+    }
+    if (cudaMallocHost(&host, std::max<uint64_t>(n, 1) * 8) != cudaSuccess)
+      throw StoreFail{WS_OUT_OF_MEMORY, "host staging"};
+    if (n && (cudaMemcpyAsync(host, dev, n * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+              cudaStreamSynchronize(s) != cudaSuccess))
+      throw StoreFail{WS_CUDA, "values readback"};
+    Manifest m;
+    m.format = static_cast<int>(format);
+    m.primes_per_file = primes_per_file;
+    m.frontier = R;  // the CLI sets the sieved-through bound (wheelsieve.cpp:167)
+    const fs::path d(dir);
+    std::string text;
+    for (uint64_t f = 0; f < nfiles; ++f) {
+      const uint64_t a = f * primes_per_file, b = std::min(n, a + primes_per_file);
+      FileEntry fe;
+      fe.name = chunk_name(f, m.format);
+      fe.count = b - a;
+      fe.min = host[a];
+      fe.max = host[b - 1];
+      if (format == 1) {
+        write_file(d / fe.name, host + a, (b - a) * 8);
+        fe.crc32 = file_crc[f];
+      } else {
+        text.clear();
+        encode_text(text, host + a, b - a);
+        write_file(d / fe.name, text.data(), text.size());
+        uLong c = ::crc32(0, Z_NULL, 0);
+        for (size_t off = 0; off < text.size(); off += (1u << 30))
+          c = ::crc32(c, reinterpret_cast<const Bytef*>(text.data() + off),
+                      static_cast<uInt>(std::min<size_t>(1u << 30, text.size() - off)));
+        fe.crc32 = static_cast<uint32_t>(c);
+      }
+      m.total_count += fe.count;
+      m.files.push_back(std::move(fe));
+    }
+    write_manifest(d, m);
+    *n_out = n;
+  } catch (const StoreFail& e) {
+    cleanup();
+    return e.code;
+  } catch (...) {
+    cleanup();
+    return WS_IO;
+  }
+  cleanup();
+  return WS_OK;
+}
+
+ws_status ws_read_back(const char* dir, uint64_t lo, uint64_t hi, uint64_t* out, uint64_t cap,
+                       uint64_t* n_out) {  // sink.cpp:306-321
+  if (!dir || !n_out) return WS_BAD_CONFIG;
+  *n_out = 0;
+  if (lo >= hi) return WS_OK;
+  try {
+    const Manifest m = load_manifest(dir);
+    if (hi > m.frontier) return WS_BEYOND_FRONTIER;
+    uint64_t n = 0;
+    for (const FileEntry& f : m.files) {
+      if (f.count == 0 || f.max < lo || f.min >= hi) continue;
+      for (uint64_t v : load_and_verify(dir, f, m.format))
+        if (lo <= v && v < hi) {
+          if (out && n < cap) out[n] = v;
+          ++n;
+        }
+    }
+    *n_out = n;
+    return n > cap ? WS_CAPACITY : WS_OK;
+  } catch (const StoreFail& e) {
+    return e.code;
+  } catch (...) {
+    return WS_IO;
+  }
+}
+
+ws_status ws_verify_store(const char* dir) {  // sink.cpp:323-342
+  if (!dir) return WS_BAD_CONFIG;
+  try {
+    const Manifest m = load_manifest(dir);
+    uint64_t total = 0, prev = 0;
+    for (const FileEntry& f : m.files) {
+      const std::vector<uint64_t> v = load_and_verify(dir, f, m.format);
+      if (!v.empty() && (v.front() != f.min || v.back() != f.max)) return WS_BAD_MANIFEST;
+      for (uint64_t x : v) {
+        if (x <= prev) return WS_BAD_MANIFEST;
+        prev = x;
+      }
+      total += v.size();
+    }
+    return total == m.total_count ? WS_OK : WS_BAD_MANIFEST;
+  } catch (const StoreFail& e) {
+    return e.code;
+  } catch (...) {
+    return WS_IO;
+  }
+}
+
+}  // extern "C"

@@ -108,6 +108,25 @@ def start_offsets(p: int, segment_start: int):
     return a.value, b.value
 
 
+def read_back(dir: str, lo: int, hi: int) -> np.ndarray:
+    """sink.cpp:306-321: primes in [lo, hi) of a chunked store, CRC-verified."""
+    if hi <= lo:
+        return np.zeros(0, np.uint64)
+    n = C.c_uint64()
+    st = lib.ws_read_back(str(dir).encode(), lo, hi, None, 0, C.byref(n))
+    if st not in (0, 4):  # 4 = Capacity: just sizing
+        _check(st, what="read_back")
+    out = np.empty(max(1, n.value), np.uint64)
+    _check(lib.ws_read_back(str(dir).encode(), lo, hi, out.ctypes.data, out.size, C.byref(n)),
+           what="read_back")
+    return out[: n.value].copy()
+
+
+def verify_store(dir: str) -> None:
+    """sink.cpp:323-342; raises Error on the first mismatch."""
+    _check(lib.ws_verify_store(str(dir).encode()), what="verify_store")
+
+
 def prime_count_bound(L: int, R: int) -> int:
     return int(lib.ws_prime_count_bound(L, R))
 
@@ -259,6 +278,14 @@ class Sieve:
         _check(lib.ws_sieve_segment(self._h, start, length, 0, r1.ctypes.data, r5.ctypes.data),
                self._h, "sieve_segment")
         return r1[:nw], r5[:nw]
+
+    def store_range(self, L: int, R: int, dir: str, binary: bool = True,
+                    primes_per_file: int = 125_000_000) -> int:
+        """ChunkedFileSink-format store of the primes of [L, R) (frontier R)."""
+        n = C.c_uint64()
+        _check(lib.ws_store_range(self._h, L, R, str(dir).encode(), 1 if binary else 0,
+                                  primes_per_file, C.byref(n)), self._h, "store_range")
+        return n.value
 
     def num_segments(self, L: int, R: int) -> int:
         if R <= L:
@@ -523,3 +550,64 @@ def run_unbounded(config: SieveConfig, stop, sieve: Optional[Sieve] = None) -> S
     object with is_set(), e.g. threading.Event) checked between iterations."""
     fn = stop.is_set if hasattr(stop, "is_set") else stop
     return _run_loop(config, fn, sieve or _sieve())
+
+
+class PrimeStream:
+    """stream.hpp:16-46 on the GPU: 2, 3, then every wheel prime ascending;
+    each refill sieves `segments_per_refill` segments of segment_wheel_len
+    slots on the device.  next() returns None once the 64-bit range is
+    exhausted (overflowed() then stays true)."""
+
+    def __init__(self, segment_wheel_len: int, sieve: Optional[Sieve] = None,
+                 segments_per_refill: int = 64):
+        if segment_wheel_len == 0:
+            raise Error(Errc.Domain, "segment must span at least one wheel index")
+        if segment_wheel_len > K_MAX_SEGMENT_END // 6:
+            raise Error(Errc.Overflow, "segment span exceeds the 64-bit value range")
+        self._sv = sieve or _sieve()
+        self._len = segment_wheel_len
+        self._span = 6 * segment_wheel_len * max(1, segments_per_refill)
+        self._next = 0
+        self._buf = np.zeros(0, np.uint64)
+        self._pos = 0
+        self._prelude = 0
+        self._overflowed = False
+
+    @staticmethod
+    def segment_would_overflow(start: int, wheel_len: int) -> bool:  # stream.cpp:24-26
+        return start >= K_MAX_SEGMENT_END or wheel_len > (K_MAX_SEGMENT_END - start) // 6
+
+    def overflowed(self) -> bool:
+        return self._overflowed
+
+    def _refill(self):
+        if self.segment_would_overflow(self._next, self._len):
+            self._overflowed = True
+            return
+        end = self._next + self._span
+        if self.segment_would_overflow(self._next, self._span // 6):
+            end = self._next + 6 * self._len * ((K_MAX_SEGMENT_END - self._next) // (6 * self._len))
+        self._buf = self._sv.enumerate_range(max(self._next, 4), end)[0]
+        self._pos = 0
+        self._next = end
+
+    def next(self):
+        if self._prelude < 2:
+            self._prelude += 1
+            return 2 if self._prelude == 1 else 3
+        while self._pos == self._buf.size:
+            if self._overflowed:
+                return None
+            self._refill()
+        v = int(self._buf[self._pos])
+        self._pos += 1
+        return v
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        v = self.next()
+        if v is None:
+            raise StopIteration
+        return v

@@ -5,6 +5,7 @@
 // wheel.cpp:40-54) and from known answers in the reference tests.
 // Prints "[PASS]"/"[FAIL]" lines; exit code = number of failures.
 #include <atomic>
+#include <filesystem>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -270,6 +271,36 @@ int main() {
     CHECK((coord_of(25) == WheelCoord{4, ResidueClass::R1}));
     EXPECT_ERROR(Errc::NotOnWheel, coord_of(4));
     EXPECT_ERROR(Errc::Overflow, value_of({kMaxWheelIndex + 1, ResidueClass::R1}));
+  }
+
+  {  // test_stream.cpp:12-51, acceptance.cpp:363-400
+    PrimeStream st(1000, dev);
+    std::vector<uint64_t> first;
+    for (int i = 0; i < 10; ++i) first.push_back(*st.next());
+    CHECK((first == std::vector<uint64_t>{2, 3, 5, 7, 11, 13, 17, 19, 23, 29}));
+    PrimeStream s2(7, dev);
+    const auto ref = textbook(1'000'000);
+    bool same = true;
+    for (uint64_t p : ref) same = same && (*s2.next() == p);
+    CHECK(same);
+    PrimeStream s3(1 << 12, dev);
+    uint64_t v = 0;
+    for (int i = 0; i < 100'000; ++i) v = *s3.next();
+    CHECK(v == 1'299'709);
+    EXPECT_ERROR(Errc::Domain, PrimeStream(0, dev));
+    CHECK(PrimeStream::segment_would_overflow(kMaxSegmentEnd, 1));
+    CHECK(!PrimeStream::segment_would_overflow(0, 1));
+  }
+
+  {  // chunked store round trip through the C++ mirror (sink.hpp:68-141)
+    const std::string d = "/tmp/wheelsieve_gpu_cpp_store";
+    std::filesystem::remove_all(d);
+    const uint64_t n = dev.store_range(0, 1'000'001, d, true, 10'000);
+    CHECK(n == 78'498);
+    verify_store(d);
+    CHECK(read_back(d, 0, 1'000'001) == textbook(1'000'000));
+    EXPECT_ERROR(Errc::BeyondFrontier, read_back(d, 0, 1'000'002));
+    std::filesystem::remove_all(d);
   }
 
   std::printf(g_fail ? "[FAIL] %d failures\n" : "[PASS] all checks\n", g_fail);

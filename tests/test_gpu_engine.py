@@ -153,3 +153,20 @@ def test_large_run_values_match_checksums(sieve):  # config-2 style through run(
     rep = run(SieveConfig(10**9, 1, 6 * (1 << 18), 0, sink), sieve)
     assert rep.prime_count == 50_847_534 and rep.largest_prime == 999_999_937
     assert sink.s == 24_739_512_092_254_535 and sink.x == 6_213_527
+
+
+def test_prime_stream(port):  # test_stream.cpp:12-69, acceptance.cpp:363-400
+    import itertools
+    from paper_2310_17746_b200 import PrimeStream
+    assert list(itertools.islice(PrimeStream(1000), 10)) == [2, 3, 5, 7, 11, 13, 17, 19, 23, 29]
+    ref = [int(x) for x in port.naive_sieve(1_000_000)]
+    assert list(itertools.islice(PrimeStream(7, segments_per_refill=3), len(ref))) == ref
+    s = PrimeStream(1 << 12)
+    v = None
+    for _ in range(100_000):
+        v = s.next()
+    assert v == 1_299_709
+    with pytest.raises(Error) as e:
+        PrimeStream(0)
+    assert e.value.code == Errc.Domain
+    assert PrimeStream.segment_would_overflow(ws.wheelsieve.K_MAX_SEGMENT_END, 1)
