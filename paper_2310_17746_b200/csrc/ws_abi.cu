@@ -120,7 +120,9 @@ struct ws_ctx {
   DevBuf<double> tab_inv;
 
   uint32_t* words_out[2] = {nullptr, nullptr};  // SegmentBitmap export (ws_sieve_segment)
-  uint32_t n_below_S = 0;  // table primes (>= 37) below S: in-kernel; the rest bucketed
+  uint32_t n_below_S = 0;  // table primes (>= 37) below bucket_pmin: in-kernel; the rest bucketed
+  uint32_t bucket_pmin = 0;
+  uint32_t n_S = 0;        // table primes (>= 37) below S
   uint32_t n_wc = 161;     // table primes below the warp-cooperative limit (1024)
   size_t bucket_budget = 1ull << 30;  // bytes of bucket lists per window
   uint32_t cap_override = 0;           // test knob (WHEELSIEVE_BUCKET_CAP)
@@ -217,9 +219,9 @@ void validate_range(uint64_t L, uint64_t R) {
 
 // Expected large-prime hits per segment: 2 S sum_{S <= p <= P} 1/p, by
 // Mertens' estimate sum 1/p over [a, b] ~ ln(ln b / ln a).
-double expected_large_hits(uint32_t S, double pmax) {
-  if (pmax <= S) return 0;
-  return 2.0 * S * std::log(std::log(pmax) / std::log(static_cast<double>(S)));
+double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
+  if (pmax <= pmin) return 0;
+  return 2.0 * S * std::log(std::log(pmax) / std::log(static_cast<double>(pmin)));
 }
 
 // The segment kernel over every segment of ctx->h_jobs.  Without large
@@ -258,6 +260,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   // 2^18-slot segment): 161 table entries; one thread per prime above
   p.n_wc = std::min<uint32_t>(c->n_wc, c->nprimes);
   p.n_mid = std::min<uint32_t>(std::max(c->n_below_S, p.n_wc), c->nprimes);
+  p.n_S = std::min<uint32_t>(std::max(c->n_S, p.n_wc), p.n_mid);
   p.acc = c->acc.ptr;
   p.per_seg = per_seg_dev;
   p.status = c->status.ptr;
@@ -269,12 +272,12 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   // Buckets pay off only when most large primes are far above S (c4: up to
   // 120 S, c5: 16 S); up to a few S (c3: 3.8 S) the per-(prime, segment)
   // offset check in the kernel is cheaper than fill + apply + windowing.
-  const bool buckets = c->nprimes > p.n_mid &&
+  const bool buckets = c->nprimes > p.n_mid && c->base_B > c->bucket_pmin &&
                        c->base_B >= static_cast<uint64_t>(c->bucket_min_ratio) * c->S;
   uint64_t W = nseg;
   uint32_t cap = 0;
   if (buckets) {
-    const double E = expected_large_hits(c->S, static_cast<double>(c->base_B));
+    const double E = expected_large_hits(c->bucket_pmin, c->S, static_cast<double>(c->base_B));
     cap = static_cast<uint32_t>(1.1 * E + 8.0 * std::sqrt(E) + 1024);
     cap = (cap + 31) / 32 * 32;
     if (c->cap_override) cap = c->cap_override;
@@ -568,19 +571,28 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   c->S = S;
   {  // primes in [37, S): the in-kernel share of the table; and the warp-
      // cooperative share [37, wc_limit)
-    uint32_t wc_limit = 1024;
+    // primes below bucket_pmin = ratio * S stay in the kernel even when the
+    // large ones are bucketed (p in [S, pmin) through the loop-free one-hit
+    // path): a bucketed hit costs ~90 instructions (fill + apply); measured
+    // optimum ratio 2 for c4 and c5 (sweep over 1..8)
+    uint32_t wc_limit = 1024, pmin_ratio = 2;
     if (const char* e = std::getenv("WHEELSIEVE_WC_LIMIT")) wc_limit = std::strtoul(e, nullptr, 10);
-    const uint32_t n_max = std::max(S, wc_limit);
+    if (const char* e = std::getenv("WHEELSIEVE_BUCKET_PMIN")) pmin_ratio = std::strtoul(e, nullptr, 10);
+    const uint32_t pmin = S * std::max<uint32_t>(1, pmin_ratio);
+    const uint32_t n_max = std::max(pmin, wc_limit);
     std::vector<uint8_t> comp(n_max, 0);
-    uint32_t n = 0, nw = 0;
+    uint32_t n = 0, nw = 0, ns = 0;
     for (uint32_t i = 2; i < n_max; ++i) {
       if (comp[i]) continue;
-      if (i >= wsk::kFirstTablePrime && i < S) ++n;
+      if (i >= wsk::kFirstTablePrime && i < pmin) ++n;
+      if (i >= wsk::kFirstTablePrime && i < S) ++ns;
       if (i >= wsk::kFirstTablePrime && i < wc_limit) ++nw;
       for (uint64_t j = static_cast<uint64_t>(i) * i; j < n_max; j += i) comp[j] = 1;
     }
     c->n_below_S = n;
+    c->n_S = ns;
     c->n_wc = nw;
+    c->bucket_pmin = pmin;
   }
   // test / tuning knobs: bucket-list capacity per segment and window budget
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CAP")) c->cap_override = std::strtoul(e, nullptr, 10);

@@ -55,8 +55,9 @@ struct SieveParams {
   uint32_t nprimes;                  // host-side upper bound on the table size
   const uint32_t* nprimes_dev;       // nullable: exact table size, written on device
   uint32_t n_wc;                     // primes [0, n_wc) use the warp-cooperative loop
-  uint32_t n_mid;                    // primes [n_wc, n_mid) one thread per prime; [n_mid,
-                                     // nprimes) from buckets (or directly if bucket == null)
+  uint32_t n_S;                      // primes [n_wc, n_S) (p < S): one thread per prime, loop
+  uint32_t n_mid;                    // [n_S, n_mid): one thread per prime, <= 1 hit per class;
+                                     // [n_mid, nprimes) from buckets (directly if bucket == null)
   const uint32_t* bucket;            // window lists: bucket[(s - s_begin) * bcap + i]
   uint32_t* bcount;                  // entries per window segment (reset after use)
   uint32_t bcap;

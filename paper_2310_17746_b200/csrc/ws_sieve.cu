@@ -320,6 +320,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   const uint32_t t_lo = si.t_lo, t_hi = si.t_hi;
   const ModCtx mc = mod_ctx(ks);
   const uint32_t n_wc = min(P.n_wc, nprimes), n_mid = min(P.n_mid, nprimes);
+  const uint32_t n_S = min(P.n_S, n_mid);
   // warp-cooperative primes, handed out dynamically (largest work first)
   for (;;) {
     uint32_t i = 0;
@@ -338,7 +339,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   const uint32_t warp = threadIdx.x >> 5;
   // p < S: one thread per prime, static warp-sized chunks; both classes
   // advance together (their hits are the same stride p apart)
-  const uint32_t mid_end = n_mid < lp_end ? n_mid : lp_end;
+  const uint32_t mid_end = n_S < lp_end ? n_S : lp_end;
   for (uint32_t base = n_wc + 32 * warp; base < mid_end; base += 32 * kWarps) {
     if (P.prime_p[base] > t_hi) break;  // primes ascend: the rest is inactive
     const uint32_t i = base + lane;
