@@ -382,10 +382,39 @@ def run_ours(args, cfg, world, rank, local):
         "integers_per_s": (total_units if kind != "enumerate" else (hi - lo) * world)
                           / (ms_per_step / 1e3),
     }
+    line["result_check"] = check_result(args.config, world, checks)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     sv.close()
     return line
+
+
+def check_result(config, world, c):
+    """Compare the run's result with the reference goldens committed under
+    tests/golden (produced by the reference library, oracle/gen_golden.py)."""
+    gdir = os.path.join(ROOT, "tests", "golden")
+    try:
+        if config == "c2" and world == 1:
+            g = json.load(open(os.path.join(gdir, "reference_goldens.json")))
+            r = [p for p in g["prefixes"] if p["limit"] == 10**10 - 1][0]
+            ok = (c.count, c.sum, c.xor, c.largest) == (r["count"], r["sum"], r["xor"], r["largest"])
+        elif config == "c1":
+            r = json.load(open(os.path.join(gdir, "c1_per_segment.json")))
+            ok = (c.count, c.largest) == (r["count"], r["largest"])
+        elif config == "c3":
+            r = json.load(open(os.path.join(gdir, "reference_big.json")))["pi_1000000000000"]
+            ok = (c.count, c.largest) == (r["count"], r["largest"])
+        elif config == "c4":
+            r = json.load(open(os.path.join(gdir, "reference_big.json")))["c4"]
+            ok = (c.count, c.sum, c.xor, c.largest) == (r["count"], r["sum"], r["xor"], r["largest"])
+        elif config == "c5":
+            r = json.load(open(os.path.join(gdir, "c5_intervals.json")))
+            ok = (c.count, c.sum, c.xor) == (r["total_count"], r["total_sum"], r["total_xor"])
+        else:
+            return "no golden for this configuration"
+    except Exception as e:  # noqa: BLE001
+        return f"golden unavailable: {e}"
+    return "match reference golden" if ok else "MISMATCH vs reference golden"
 
 
 def cpu_baseline(cfg):

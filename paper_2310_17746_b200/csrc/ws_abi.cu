@@ -86,6 +86,39 @@ struct PinnedBuf {
   }
 };
 
+// Per-call bump arena of pinned staging for async uploads.  A region is
+// never reused within a call (its copy may still be pending); offsets reset
+// at the start of the next call, which is safe because every call ends with
+// a stream synchronisation.
+struct PinnedArena {
+  std::vector<PinnedBuf> blocks;
+  size_t cur = 0, off = 0;
+  void reset() {
+    cur = 0;
+    off = 0;
+  }
+  void* alloc(size_t n, const char* what) {
+    n = (n + 255) / 256 * 256;
+    while (cur < blocks.size() && off + n > blocks[cur].bytes) {
+      ++cur;
+      off = 0;
+    }
+    if (cur == blocks.size()) {
+      blocks.emplace_back();
+      blocks.back().reserve(std::max<size_t>(n, 1 << 20), what);
+      off = 0;
+    }
+    void* p = static_cast<char*>(blocks[cur].ptr) + off;
+    off += n;
+    return p;
+  }
+  void release() {
+    for (auto& b : blocks) b.release();
+    blocks.clear();
+    reset();
+  }
+};
+
 uint64_t small_primes_upto(uint64_t B) {  // |{5,7,...,31} ∩ [5, B]|
   static const uint32_t sp[] = {5, 7, 11, 13, 17, 19, 23, 29, 31};
   uint64_t c = 0;
@@ -105,7 +138,8 @@ struct ws_ctx {
   ws_timing timing{};
   cudaEvent_t ev[4] = {};
 
-  PinnedBuf pin_jobs, pin_runs, pin_out;  // async staging for uploads / results
+  PinnedArena pin_up;  // async upload staging (jobs, runs), reset per call
+  PinnedBuf pin_out;   // results, read after the call's synchronisation
   DevBuf<uint32_t> d_tabn;  // exact base-table size, written on device by prepare_table
   DevBuf<uint32_t> small_tab;  // small-prime pattern tables
 
@@ -156,8 +190,7 @@ struct ws_ctx {
     l0_inv.release();
     d_tabn.release();
     small_tab.release();
-    pin_jobs.release();
-    pin_runs.release();
+    pin_up.release();
     pin_out.release();
     for (int i = 0; i < 2; ++i) {
       if (fill_done[i]) cudaEventDestroy(fill_done[i]);
@@ -234,7 +267,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   const size_t nj = c->h_jobs.size();
   c->jobs.reserve(nj, "jobs");
   c->acc.reserve(nj, "acc");
-  void* hj = c->pin_jobs.reserve(nj * sizeof(wsk::Job), "pinned jobs");
+  void* hj = c->pin_up.alloc(nj * sizeof(wsk::Job), "pinned jobs");
   std::memcpy(hj, c->h_jobs.data(), nj * sizeof(wsk::Job));
   ck(cudaMemcpyAsync(c->jobs.ptr, hj, nj * sizeof(wsk::Job), cudaMemcpyHostToDevice, c->stream),
      "upload jobs");
@@ -324,7 +357,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
       run_off[w + 1] = static_cast<uint32_t>(runs.size());
     }
     c->runs.reserve(runs.size(), "runs");
-    void* hr = c->pin_runs.reserve(runs.size() * sizeof(wsk::Run), "pinned runs");
+    void* hr = c->pin_up.alloc(runs.size() * sizeof(wsk::Run), "pinned runs");
     std::memcpy(hr, runs.data(), runs.size() * sizeof(wsk::Run));
     ck(cudaMemcpyAsync(c->runs.ptr, hr, runs.size() * sizeof(wsk::Run), cudaMemcpyHostToDevice,
                        c->stream), "upload runs");
@@ -469,6 +502,7 @@ ws_status guarded(ws_ctx* c, F&& f) {
   Timer t;
   c->err.clear();
   c->timing = ws_timing{};
+  c->pin_up.reset();
   try {
     if (cudaSetDevice(c->device) != cudaSuccess) throw Fail{WS_NO_DEVICE, "cudaSetDevice"};
     f();

@@ -280,3 +280,28 @@ def test_base_primes_match_bootstrap(sieve):
     with pytest.raises(ws.Error) as e:
         sieve.base_primes(1)
     assert e.value.code == ws.Errc.EmptyRange
+
+
+def test_repeated_fresh_base_with_buckets():
+    """Regression: repeated WS_FRESH_BASE calls on a bucketed range (the base
+    sieve and the main launch stage their uploads through pinned memory)."""
+    import paper_2310_17746_b200 as ws
+    g = load_golden("reference_goldens.json")
+    rec = [w for w in g["windows"] if (w["L"], w["R"]) == (10**15, 10**15 + 10**8)][0]
+    with ws.Sieve() as s:
+        for _ in range(4):
+            c = s.count_range(rec["L"], rec["R"], checks=True, fresh_base=True)
+            assert (c.count, c.sum, c.xor) == (rec["count"], rec["sum"], rec["xor"])
+        for _ in range(2):
+            v, n, c = s.enumerate_range(rec["L"], rec["R"], fresh_base=True)
+            assert (n, c.sum, c.xor) == (rec["count"], rec["sum"], rec["xor"])
+
+
+def test_config4_full_window_reference_golden(sieve):
+    """[1e15, 1e15 + 1e11): count, sum, xor, largest from the reference
+    library's --big golden run (oracle/gen_golden.py --big, 262 s on 8 threads)."""
+    big = load_golden("reference_big.json")["c4"]
+    for fresh in (False, True):
+        c = sieve.count_range(big["L"], big["R"], checks=True, fresh_base=fresh)
+        assert (c.count, c.sum, c.xor, c.largest) == (big["count"], big["sum"], big["xor"],
+                                                      big["largest"])
