@@ -119,8 +119,8 @@ struct PinnedArena {
   }
 };
 
-uint64_t small_primes_upto(uint64_t B) {  // |{5,7,...,31} ∩ [5, B]|
-  static const uint32_t sp[] = {5, 7, 11, 13, 17, 19, 23, 29, 31};
+uint64_t small_primes_upto(uint64_t B) {  // |{5,7,...,47} ∩ [5, B]| (the stamped primes)
+  static const uint32_t sp[] = {5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47};
   uint64_t c = 0;
   for (uint32_t q : sp) c += q <= B;
   return c;
@@ -143,7 +143,7 @@ struct ws_ctx {
   DevBuf<uint32_t> d_tabn;  // exact base-table size, written on device by prepare_table
   DevBuf<uint32_t> small_tab;  // small-prime pattern tables
 
-  // resident base-prime table: every prime in [37, base_B]
+  // resident base-prime table: every prime in [53, base_B]
   bool base_valid = false;
   bool base_built = false;  // the last call (re)built the table
   uint64_t base_B = 0;
@@ -167,6 +167,10 @@ struct ws_ctx {
   DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)
   DevBuf<uint32_t> bcount[2];
   cudaStream_t fstream = nullptr;  // bucket-fill stream
+  cudaStream_t cstream = nullptr;  // device->host copy stream (chunked enumeration)
+  cudaEvent_t ev_order = nullptr;
+  static constexpr int kMaxChunks = 16;
+  cudaEvent_t chunk_done[kMaxChunks] = {};
   cudaEvent_t fill_done[2] = {}, sieve_done[2] = {};
   DevBuf<wsk::Run> runs;
   DevBuf<wsk::Job> jobs;
@@ -197,6 +201,10 @@ struct ws_ctx {
       if (sieve_done[i]) cudaEventDestroy(sieve_done[i]);
     }
     if (fstream) cudaStreamDestroy(fstream);
+    if (cstream) cudaStreamDestroy(cstream);
+    if (ev_order) cudaEventDestroy(ev_order);
+    for (cudaEvent_t e : chunk_done)
+      if (e) cudaEventDestroy(e);
     for (auto* b : {&tab_m, &ticket, &status, &vals, &l0_m}) b->release();
     jobs.release();
     acc.release();
@@ -261,17 +269,27 @@ double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
 // primes this is one launch; otherwise the segments are processed in windows
 // of W segments: bucket_fill (large-prime hit lists) then the sieve kernel.
 void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* out,
-               unsigned long long out_cap, bool timed) {
+               unsigned long long out_cap, bool timed, uint32_t acc_base = 0,
+               bool record_start = true) {
   uint64_t nseg = 0;
   for (const auto& j : c->h_jobs) nseg += j.nseg;
   const size_t nj = c->h_jobs.size();
   c->jobs.reserve(nj, "jobs");
-  c->acc.reserve(nj, "acc");
+  if (c->acc.cap < acc_base + nj) {  // grow without losing accumulators of earlier chunks
+    if (acc_base) ck(cudaStreamSynchronize(c->stream), "sync");
+    DevBuf<wsk::JobAcc> bigger;
+    bigger.reserve(std::max<size_t>(acc_base + nj, 16), "acc");
+    if (acc_base)
+      ck(cudaMemcpy(bigger.ptr, c->acc.ptr, acc_base * sizeof(wsk::JobAcc), cudaMemcpyDeviceToDevice),
+         "acc");
+    std::swap(c->acc, bigger);
+    bigger.release();
+  }
   void* hj = c->pin_up.alloc(nj * sizeof(wsk::Job), "pinned jobs");
   std::memcpy(hj, c->h_jobs.data(), nj * sizeof(wsk::Job));
   ck(cudaMemcpyAsync(c->jobs.ptr, hj, nj * sizeof(wsk::Job), cudaMemcpyHostToDevice, c->stream),
      "upload jobs");
-  ck(cudaMemsetAsync(c->acc.ptr, 0, nj * sizeof(wsk::JobAcc), c->stream), "zero acc");
+  ck(cudaMemsetAsync(c->acc.ptr + acc_base, 0, nj * sizeof(wsk::JobAcc), c->stream), "zero acc");
   if (mode == wsk::kEnumerate) {
     c->status.reserve(nseg, "status");
     ck(cudaMemsetAsync(c->status.ptr, 0, nseg * sizeof(unsigned long long), c->stream),
@@ -294,7 +312,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.n_wc = std::min<uint32_t>(c->n_wc, c->nprimes);
   p.n_mid = std::min<uint32_t>(std::max(c->n_below_S, p.n_wc), c->nprimes);
   p.n_S = std::min<uint32_t>(std::max(c->n_S, p.n_wc), p.n_mid);
-  p.acc = c->acc.ptr;
+  p.acc = c->acc.ptr + acc_base;
   p.per_seg = per_seg_dev;
   p.status = c->status.ptr;
   p.out = out;
@@ -362,9 +380,10 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     ck(cudaMemcpyAsync(c->runs.ptr, hr, runs.size() * sizeof(wsk::Run), cudaMemcpyHostToDevice,
                        c->stream), "upload runs");
   }
-  // ev[2] also orders the fill stream after everything queued so far
-  ck(cudaEventRecord(c->ev[2], c->stream), "event");
-  if (buckets) ck(cudaStreamWaitEvent(c->fstream, c->ev[2], 0), "fill wait");
+  // ev[2] (call start) / ev[4] order the fill stream after everything queued so far
+  if (record_start) ck(cudaEventRecord(c->ev[2], c->stream), "event");
+  ck(cudaEventRecord(c->ev_order, c->stream), "event");
+  if (buckets) ck(cudaStreamWaitEvent(c->fstream, c->ev_order, 0), "fill wait");
   for (uint64_t w = 0; w < nwin; ++w) {
     const uint64_t ws = w * W, we = std::min(nseg, ws + W);
     const int b = static_cast<int>(w & 1);
@@ -540,6 +559,55 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Host-output enumeration as a pipeline: [L, R) is cut into up to
+// kMaxChunks chunks on segment borders; every chunk's sieve launch is queued
+// at once on the compute stream, and as each chunk finishes its values are
+// copied device->host on the copy stream while later chunks still sieve, so
+// the PCIe transfer (the bound for large outputs) hides the kernels.
+void enumerate_to_host(ws_ctx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_t cap,
+                       ws_checks* chk) {
+  const wsk::Job whole = make_job(L, R, c->S, 0);
+  const uint64_t nseg = whole.nseg;
+  const uint64_t nch = std::max<uint64_t>(1, std::min<uint64_t>(ws_ctx::kMaxChunks, nseg / 64));
+  std::vector<uint64_t> lo(nch), hi(nch), boff(nch + 1, 0);
+  const uint64_t lo0 = L / 6 * 6;
+  for (uint64_t k = 0; k < nch; ++k) {
+    const uint64_t a = k * nseg / nch, b = (k + 1) * nseg / nch;
+    lo[k] = k == 0 ? L : std::min<uint64_t>(R, lo0 + 6ull * c->S * a);
+    hi[k] = k + 1 == nch ? R : std::min<uint64_t>(R, lo0 + 6ull * c->S * b);
+    boff[k + 1] = boff[k] + prime_count_bound(lo[k], hi[k]);
+  }
+  c->vals.reserve(std::max<uint64_t>(boff[nch], 1), "enumeration buffer");
+  wsk::JobAcc* hacc = static_cast<wsk::JobAcc*>(
+      c->pin_out.reserve(nch * sizeof(wsk::JobAcc) + 16, "pinned out"));
+  for (uint64_t k = 0; k < nch; ++k) {
+    c->h_jobs.assign(1, make_job(lo[k], hi[k], c->S, 0));
+    run_sieve(c, wsk::kEnumerate, nullptr, c->vals.ptr + boff[k], boff[k + 1] - boff[k], true,
+              static_cast<uint32_t>(k), k == 0);
+    ck(cudaMemcpyAsync(hacc + k, c->acc.ptr + k, sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost,
+                       c->stream), "chunk acc");
+    ck(cudaEventRecord(c->chunk_done[k], c->stream), "event");
+  }
+  uint64_t pos = 0;
+  for (uint64_t k = 0; k < nch; ++k) {
+    ck(cudaEventSynchronize(c->chunk_done[k]), "chunk");
+    const uint64_t n = hacc[k].count;
+    const uint64_t take = pos < cap ? std::min(n, cap - pos) : 0;
+    if (take)
+      ck(cudaMemcpyAsync(out + pos, c->vals.ptr + boff[k], take * 8, cudaMemcpyDeviceToHost,
+                         c->cstream), "d2h");
+    pos += n;
+    chk->count += n;
+    chk->sum += hacc[k].sum;
+    chk->xor_ ^= hacc[k].xr;
+    chk->largest = std::max<uint64_t>(chk->largest, hacc[k].largest);
+  }
+  ck(cudaStreamSynchronize(c->cstream), "d2h sync");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  ck(cudaGetLastError(), "kernel");
+  c->timing.base_primes = c->nprimes + small_primes_upto(c->base_B);
+}
+
 }  // namespace
 
 extern "C" {
@@ -646,7 +714,11 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
       delete c;
       return WS_CUDA;
     }
-  bool ok = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking) == cudaSuccess;
+  bool ok = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) == cudaSuccess;
+  for (int i = 0; i < ws_ctx::kMaxChunks && ok; ++i)
+    ok = cudaEventCreateWithFlags(&c->chunk_done[i], cudaEventDisableTiming) == cudaSuccess;
   if (ok) {
     std::vector<uint32_t> tab(wsk::small_table_words());
     wsk::build_small_tables(tab.data());
@@ -792,20 +864,18 @@ ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags
         ck(cudaMemcpyAsync(out, pre, std::min(npre, cap) * 8, cudaMemcpyHostToDevice,
                            ctx->stream), "prelude");
     } else {
-      const uint64_t bound = std::min<uint64_t>(prime_count_bound(L, R), cap > npre ? cap - npre : 0);
-      ctx->vals.reserve(bound, "enumeration buffer");
-      dst = ctx->vals.ptr;
-      dcap = bound;
       for (uint64_t i = 0; i < npre && i < cap; ++i) out[i] = pre[i];
+      enumerate_to_host(ctx, L, R, out + std::min(npre, cap), cap > npre ? cap - npre : 0, &chk);
+      add_prelude(L, R, &chk);
+      *n_out = chk.count;
+      if (checks) *checks = chk;
+      ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
+      ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
+      if (chk.count > cap) throw Fail{WS_CAPACITY, "output capacity below the prime count"};
+      return;
     }
     run_sieve(ctx, wsk::kEnumerate, nullptr, dst, dcap, true);
     const wsk::JobAcc a = *fetch_results(ctx, 1);
-    if (!dev_out) {
-      const uint64_t n = std::min<uint64_t>(a.count, dcap);
-      if (n)
-        ck(cudaMemcpyAsync(out + npre, dst, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
-      ck(cudaStreamSynchronize(ctx->stream), "sync");
-    }
     chk.count = a.count;
     chk.sum = a.sum;
     chk.xor_ = a.xr;

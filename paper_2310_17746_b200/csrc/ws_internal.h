@@ -9,7 +9,7 @@ namespace wsk {
 
 constexpr int kThreads = 512;            // threads per sieve block
 constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kFirstTablePrime = 37; // primes 5..31 are stamped from pattern tables
+constexpr uint32_t kFirstTablePrime = 53; // primes 5..47 are stamped from pattern tables
 
 // One half-open value range [L, R) sieved as nseg segments of S wheel slots
 // per residue class starting at wheel index K0 = floor(L / 6)

@@ -11,12 +11,12 @@
 //                   COMPOSITE bits (the complement of FlagArray), so crossing
 //                   off is one ATOMS.OR.  No bank swizzle: simulated and
 //                   measured conflicts of the strided loop are lower with the
-//                   natural layout (2.4-way vs 2.8-way for p in [37, 1024)).
-//   stamp:          primes 5..31 are never looped: their combined periodic
-//                   patterns (groups 5*7*11*13, 17*19*23, 29*31) live in
-//                   shared tables and each word is initialised by three
+//                   natural layout (2.4-way vs 2.8-way for p in [53, 1024)).
+//   stamp:          primes 5..47 are never looped: their combined periodic
+//                   patterns (5*7*11*13, 17*19*23, 29*31, 37*41, 43*47) live in
+//                   shared tables and each word is initialised by five
 //                   funnel-shifted table reads ANDed with the [L, R) trim mask.
-//   medium primes:  37 <= p < wc_limit: warp-cooperative strided clear (lane l
+//   medium primes:  53 <= p < wc_limit: warp-cooperative strided clear (lane l
 //                   takes hits rel + l*p, rel + (l+32)*p, ...).
 //   other primes:   one thread per prime.
 //   offsets:        the first hit of p in each class is recomputed per
@@ -118,26 +118,35 @@ __device__ __forceinline__ uint32_t range_mask(int64_t a, int64_t b) {
 // c holds bits for wheel indices 32i .. 32i+31 (mod Q_g), bit set when the
 // index is NOT a multiple-position of any prime of the group.  Stored
 // wrap-extended so a funnel shift at any offset < Q_g reads 32 valid bits.
-// group 0: 5*7*11*13 = 5005, group 1: 17*19*23 = 7429, group 2: 29*31 = 899
+// groups: 5*7*11*13 = 5005, 17*19*23 = 7429, 29*31 = 899, 37*41 = 1517,
+// 43*47 = 2021 -- every prime below kFirstTablePrime (53) is stamped
+constexpr int kGroups = 5;
 __host__ __device__ constexpr uint32_t group_prime(int g, int j) {
   return g == 0 ? (j == 0 ? 5 : j == 1 ? 7 : j == 2 ? 11 : 13)
        : g == 1 ? (j == 0 ? 17 : j == 1 ? 19 : 23)
-                : (j == 0 ? 29 : 31);
+       : g == 2 ? (j == 0 ? 29 : 31)
+       : g == 3 ? (j == 0 ? 37 : 41)
+                : (j == 0 ? 43 : 47);
 }
 __host__ __device__ constexpr int group_size(int g) { return g == 0 ? 4 : g == 1 ? 3 : 2; }
+__host__ __device__ constexpr uint32_t group_mod(int g) {
+  return g == 0 ? 5005 : g == 1 ? 7429 : g == 2 ? 899 : g == 3 ? 1517 : 2021;
+}
 constexpr uint32_t tab_words(uint32_t Q) { return (Q + 31) / 32 + 2; }
-constexpr uint32_t kTabW0 = tab_words(5005), kTabW1 = tab_words(7429), kTabW2 = tab_words(899);
-constexpr uint32_t kTabPerClass = kTabW0 + kTabW1 + kTabW2;
+__host__ __device__ constexpr uint32_t tab_off(int g) {
+  return g == 0 ? 0 : tab_off(g - 1) + tab_words(group_mod(g - 1));
+}
+constexpr uint32_t kTabPerClass = tab_off(kGroups);
 constexpr uint32_t kTabWords = 2 * kTabPerClass;
-constexpr uint32_t kTabOff1 = kTabW0, kTabOff2 = kTabW0 + kTabW1;
 
 // One table word (class cls, group g, word i): bit b set when index
 // 32 i + b is not a multiple-position of any prime of the group.
 __host__ __device__ uint32_t table_word(uint32_t idx) {
   const uint32_t cls = idx / kTabPerClass;  // 0 -> 6k+1, 1 -> 6k+5
   const uint32_t rem = idx % kTabPerClass;
-  const int g = rem < kTabOff1 ? 0 : (rem < kTabOff2 ? 1 : 2);
-  const uint32_t i = rem - (g == 0 ? 0u : g == 1 ? kTabOff1 : kTabOff2);
+  int g = 0;
+  while (g + 1 < kGroups && rem >= tab_off(g + 1)) ++g;
+  const uint32_t i = rem - tab_off(g);
   uint32_t word = 0;
   for (uint32_t b = 0; b < 32; ++b) {
     const uint32_t pos = 32 * i + b;
@@ -226,19 +235,26 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
   const uint32_t o0 = static_cast<uint32_t>(si.ks % 5005u);
   const uint32_t o1 = static_cast<uint32_t>(si.ks % 7429u);
   const uint32_t o2 = static_cast<uint32_t>(si.ks % 899u);
+  const uint32_t o3 = static_cast<uint32_t>(si.ks % 1517u);
+  const uint32_t o4 = static_cast<uint32_t>(si.ks % 2021u);
   const uint32_t* t1 = tab;
   const uint32_t* t5 = tab + kTabPerClass;
   for (uint32_t w = threadIdx.x; w < si.nwords; w += kThreads) {
     const uint32_t a0 = (o0 + 32 * w) % 5005u;
     const uint32_t a1 = (o1 + 32 * w) % 7429u;
     const uint32_t a2 = (o2 + 32 * w) % 899u;
-    uint32_t m1 = tab_read(t1, a0) & tab_read(t1 + kTabOff1, a1) & tab_read(t1 + kTabOff2, a2);
-    uint32_t m5 = tab_read(t5, a0) & tab_read(t5 + kTabOff1, a1) & tab_read(t5 + kTabOff2, a2);
-    if (w == 0 && si.ks < 6) {
-      // the small primes themselves survive: 7, 13, 19, 31 at class-1
-      // indices 1, 2, 3, 5 and 5, 11, 17, 23, 29 at class-5 indices 0..4
-      m1 |= 0x2Eu >> si.ks;
-      m5 |= 0x1Fu >> si.ks;
+    const uint32_t a3 = (o3 + 32 * w) % 1517u;
+    const uint32_t a4 = (o4 + 32 * w) % 2021u;
+    uint32_t m1 = tab_read(t1, a0) & tab_read(t1 + tab_off(1), a1) & tab_read(t1 + tab_off(2), a2) &
+                  tab_read(t1 + tab_off(3), a3) & tab_read(t1 + tab_off(4), a4);
+    uint32_t m5 = tab_read(t5, a0) & tab_read(t5 + tab_off(1), a1) & tab_read(t5 + tab_off(2), a2) &
+                  tab_read(t5 + tab_off(3), a3) & tab_read(t5 + tab_off(4), a4);
+    if (w == 0 && si.ks < 8) {
+      // the stamped primes themselves survive: 7, 13, 19, 31, 37, 43 at
+      // class-1 indices 1, 2, 3, 5, 6, 7 and 5, 11, 17, 23, 29, 41, 47 at
+      // class-5 indices 0..4, 6, 7
+      m1 |= 0xEEu >> si.ks;
+      m5 |= 0xDFu >> si.ks;
     }
     const int64_t base = 32 * static_cast<int64_t>(w);
     m1 &= range_mask(static_cast<int64_t>(si.lo1) - base, static_cast<int64_t>(si.hi1) - base);
@@ -786,7 +802,7 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
 
 // ---------------------------------------------------------------------------
 // Level-0 base primes: a dense sieve of [0, n] (n <= 65537) in one block,
-// writing the primes >= 37 in ascending order with their Barrett constants.
+// writing the primes >= 53 in ascending order with their Barrett constants.
 __global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t* out_p,
                                                            unsigned long long* out_m,
                                                            double* out_inv,
