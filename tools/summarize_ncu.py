@@ -53,11 +53,12 @@ def full(path):
                 i = hdr.index(k)
                 print(f"  {k:75s} {r[i]:>20s} {units[i]}")
         if "dram__bytes_read.sum" in hdr:
-            rd = float(r[hdr.index("dram__bytes_read.sum")].replace(",", ""))
-            wr = float(r[hdr.index("dram__bytes_write.sum")].replace(",", ""))
-            ur = units[hdr.index("dram__bytes_read.sum")]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
-            print(f"  traffic (dram read+write) = {(rd + wr) * scale:.4e} bytes per launch")
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                i = hdr.index(k)
+                tot += float(r[i].replace(",", "")) * scale.get(units[i], 1)
+            print(f"  traffic (dram read+write) = {tot:.4e} bytes per launch")
 
 
 if __name__ == "__main__":
