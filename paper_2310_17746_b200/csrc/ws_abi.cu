@@ -162,6 +162,7 @@ struct ws_ctx {
   uint32_t cap_override = 0;           // test knob (WHEELSIEVE_BUCKET_CAP)
   uint32_t piece_override = 0;         // tuning knob (WHEELSIEVE_FILL_PIECE)
   uint32_t bucket_min_ratio = 8;       // buckets iff largest base prime >= ratio * S
+  uint32_t bucket_ctas_per_sm = 0;     // tuning knob (WHEELSIEVE_BUCKET_CTAS)
 
   // scratch
   DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)
@@ -319,7 +320,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.out_cap = out_cap;
   p.words1 = c->words_out[0];
   p.words5 = c->words_out[1];
-  const uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps[mode];
+  uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps[mode];
   // Buckets pay off only when most large primes are far above S (c4: up to
   // 120 S, c5: 16 S); up to a few S (c3: 3.8 S) the per-(prime, segment)
   // offset check in the kernel is cheaper than fill + apply + windowing.
@@ -349,6 +350,9 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   std::vector<uint32_t> run_off(nwin + 1, 0);
   uint64_t piece = W;
   if (buckets) {
+    // optional cap on sieve CTAs per SM to leave room for fill CTAs (measured: no gain)
+    if (c->bucket_ctas_per_sm)
+      max_grid = std::min<uint64_t>(max_grid, static_cast<uint64_t>(c->sms) * c->bucket_ctas_per_sm);
     // runs are cut into 32-segment pieces: short per-thread hit loops and a
     // fill grid that covers the GPU (measured best for c4 and c5)
     piece = c->piece_override ? c->piece_override : 32;
@@ -701,6 +705,7 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_BUDGET")) c->bucket_budget = std::strtoull(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_FILL_PIECE")) c->piece_override = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_RATIO")) c->bucket_min_ratio = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CTAS")) c->bucket_ctas_per_sm = std::strtoul(e, nullptr, 10);
   c->sms = prop.multiProcessorCount;
   if (cudaSetDevice(dev) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
