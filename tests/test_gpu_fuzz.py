@@ -1,0 +1,113 @@
+"""GPU: seeded fuzz of every range entry point against the oracle, across
+segment sizes, bucket policies and ragged interval batches."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2310_17746_b200 as ws
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _t(c):
+    return (c.count, c.sum, c.xor, c.largest)
+
+
+@pytest.mark.parametrize("slots", [1 << 12, 1 << 13, 1 << 15, 1 << 17, 1 << 18])
+def test_fuzz_segment_sizes(port, slots):
+    rng = np.random.default_rng(slots)
+    with ws.Sieve(segment_slots=slots) as sv:
+        for _ in range(12):
+            L = int(rng.choice([rng.integers(0, 10**4), rng.integers(0, 10**10),
+                                rng.integers(10**13, 10**15)]))
+            W = int(rng.integers(1, 3 * slots * 6))
+            ref = port.range(L, L + W, seg_slots=slots, per_seg=True, values=True)
+            c, ps = sv.count_range(L, L + W, checks=True, per_seg=True)
+            assert _t(c) == (ref["count"], ref["sum"], ref["xor"], ref["largest"]), (slots, L, W)
+            assert np.array_equal(ps, ref["per_seg"])
+            v, n, ce = sv.enumerate_range(L, L + W)
+            assert np.array_equal(v, ref["values"]) and _t(ce) == _t(c)
+
+
+def test_fuzz_intervals_ragged(port):
+    rng = np.random.default_rng(99)
+    with ws.Sieve() as sv:
+        for width in (1, 5, 6, 7, 1000, 123_457, 2_000_003):
+            Ls = rng.integers(0, 10**12, size=17).astype(np.uint64)
+            Ls[0] = 0
+            Ls[1] = 1
+            counts, sums, xors = sv.count_intervals(Ls, width)
+            for i, L in enumerate(Ls):
+                r = port.range(int(L), int(L) + width)
+                assert (int(counts[i]), int(sums[i]), int(xors[i])) == (r["count"], r["sum"],
+                                                                         r["xor"]), (width, L)
+
+
+BUCKET_FUZZ = r"""
+import sys
+sys.path.insert(0, '.')
+import numpy as np
+import paper_2310_17746_b200 as ws
+from oracle.oracle import Port
+port = Port()
+rng = np.random.default_rng(5)
+with ws.Sieve() as sv:
+    for _ in range(10):
+        L = int(rng.integers(10**11, 10**15))
+        W = int(rng.integers(10**5, 4 * 10**6))
+        r = port.range(L, L + W, per_seg=True)
+        c, ps = sv.count_range(L, L + W, checks=True, per_seg=True)
+        assert (c.count, c.sum, c.xor, c.largest) == (r["count"], r["sum"], r["xor"], r["largest"]), (L, W)
+        assert np.array_equal(ps, r["per_seg"])
+    Ls = rng.integers(2**32, 2**40, size=9).astype(np.uint64)
+    counts, sums, xors = sv.count_intervals(Ls, 3 * 10**6)
+    for i, L in enumerate(Ls):
+        r = port.range(int(L), int(L) + 3 * 10**6)
+        assert (int(counts[i]), int(sums[i]), int(xors[i])) == (r["count"], r["sum"], r["xor"])
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"WHEELSIEVE_BUCKET_RATIO": "1", "WHEELSIEVE_BUCKET_PMIN": "1"},
+                                 {"WHEELSIEVE_BUCKET_RATIO": "1", "WHEELSIEVE_BUCKET_PMIN": "3",
+                                  "WHEELSIEVE_FILL_PIECE": "7",
+                                  "WHEELSIEVE_BUCKET_BUDGET": str(3 << 20)},
+                                 {"WHEELSIEVE_BUCKET_RATIO": "1", "WHEELSIEVE_BUCKET_CAP": "100",
+                                  "WHEELSIEVE_BUCKET_CTAS": "1"}])
+def test_fuzz_bucket_policies(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", BUCKET_FUZZ], cwd=ROOT, env=e, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_abi_error_paths(sieve, tmp_path):
+    import ctypes as C
+    from paper_2310_17746_b200 import _lib
+    lib = _lib.lib
+    n = C.c_uint64()
+    # null outputs / contexts are rejected, never crash
+    assert lib.ws_count_range(None, 0, 10, 0, None, None, 0, None) == 7
+    assert lib.ws_count_range(sieve._h, 0, 10, 0, None, None, 0, None) == 7
+    assert lib.ws_enumerate_range(sieve._h, 0, 100, 0, None, 5, C.byref(n), None) == 7
+    assert lib.ws_count_intervals(sieve._h, None, 3, 10, 0, None, None, None) == 7
+    Ls = np.array([10, 20], np.uint64)
+    counts = np.zeros(2, np.uint32)
+    assert lib.ws_count_intervals(sieve._h, Ls.ctypes.data, 2, 0, 0, counts.ctypes.data,
+                                  None, None) == 3  # EmptyRange
+    assert lib.ws_count_intervals(sieve._h, Ls.ctypes.data, 0, 10, 0, counts.ctypes.data,
+                                  None, None) == 0
+    assert lib.ws_partition(0, 10, 1 << 18, 2, 2, C.byref(n), C.byref(n)) == 7
+    assert lib.ws_store_range(sieve._h, 0, 10, None, 0, 10, C.byref(n)) == 7
+    assert lib.ws_store_range(sieve._h, 0, 10, str(tmp_path).encode(), 2, 10, C.byref(n)) == 7
+    assert lib.ws_read_back(str(tmp_path / "nope").encode(), 0, 10, None, 0, C.byref(n)) == 11
+    assert lib.ws_verify_store(str(tmp_path / "nope").encode()) == 11
+    # the context stays usable after errors
+    assert sieve.count_range(0, 101).count == 25
+    t = sieve.timing()
+    assert t.total_ms >= 0
+    assert (lib.ws_last_error(sieve._h) or b"") == b""
