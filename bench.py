@@ -300,9 +300,21 @@ def run_ours(args, cfg, world, rank, local):
         if world > 1:
             e_ms = wsdist.max_over_ranks(e_ms)
         assert ce.count == c.count and ce.sum == c.sum and ce.xor == c.xor
+        tm = sv.timing()
+        # the values that landed in host memory, not just the device checksums
+        hv = host[:n]
+        host_ok = (int(hv.sum(dtype=np.uint64)) == ce.sum and
+                   int(np.bitwise_xor.reduce(hv)) == ce.xor and int(hv[-1]) == ce.largest)
+        if not host_ok:
+            raise SystemExit("e2e: host output disagrees with the device checksums")
+        wire = os.environ.get("WHEELSIEVE_HOST_WIRE", "1") != "0" and tm.d2h_bytes < 4 * n
         e2e = {"value": total_units / (e_ms / 1e3), "unit": cfg["unit"],
-               "h2d_bytes_per_step": 16 * world, "d2h_bytes_per_step": int(8 * total_units + 32),
-               "ms_per_step": e_ms, "steps": k_e2e, "timer": "host wall clock per call"}
+               "h2d_bytes_per_step": int(tm.h2d_bytes) * world,
+               "d2h_bytes_per_step": int(tm.d2h_bytes) * world,
+               "ms_per_step": e_ms, "steps": k_e2e, "timer": "host wall clock per call",
+               "transfer": ("16-bit wire entries + per-block counts, widened on the host "
+                            "(ws_wire.cpp)") if wire else "uint64 values",
+               "host_values_verified": True}
     elif kind in ("count", "checks"):
         k_e2e = max(2, min(args.steps, 10))
         per = np.zeros(max(1, sv.num_segments(lo, hi)), np.uint32)
@@ -312,8 +324,10 @@ def run_ours(args, cfg, world, rank, local):
         e_ms = (time.perf_counter() - t0) * 1e3 / k_e2e
         if world > 1:
             e_ms = wsdist.max_over_ranks(e_ms)
+        tm = sv.timing()
         e2e = {"value": total_units / (e_ms / 1e3), "unit": cfg["unit"],
-               "h2d_bytes_per_step": 16 * world, "d2h_bytes_per_step": int(4 * per.size + 32),
+               "h2d_bytes_per_step": int(tm.h2d_bytes) * world,
+               "d2h_bytes_per_step": int(tm.d2h_bytes) * world,
                "ms_per_step": e_ms, "steps": k_e2e, "timer": "host wall clock per call"}
     else:
         k_e2e = max(2, min(args.steps, 10))
@@ -323,8 +337,10 @@ def run_ours(args, cfg, world, rank, local):
         e_ms = (time.perf_counter() - t0) * 1e3 / k_e2e
         if world > 1:
             e_ms = wsdist.max_over_ranks(e_ms)
+        tm = sv.timing()
         e2e = {"value": total_units / (e_ms / 1e3), "unit": cfg["unit"],
-               "h2d_bytes_per_step": 8 * 4096, "d2h_bytes_per_step": 20 * 4096,
+               "h2d_bytes_per_step": int(tm.h2d_bytes) * world,
+               "d2h_bytes_per_step": int(tm.d2h_bytes) * world,
                "ms_per_step": e_ms, "steps": k_e2e, "timer": "host wall clock per call"}
 
     if rank != 0:

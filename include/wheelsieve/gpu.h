@@ -94,6 +94,9 @@ typedef struct ws_timing {
   uint64_t launches; /* kernels launched by the last call */
   uint64_t segments; /* segments sieved by the main kernel in the last call */
   uint64_t base_primes; /* sieving primes (>= 5) used by the last call */
+  uint64_t h2d_bytes;   /* bytes copied host->device by the last call */
+  uint64_t d2h_bytes;   /* bytes copied device->host by the last call (host-bound
+                           enumeration ships 2 bytes per prime, see ws_enumerate_range) */
 } ws_timing;
 
 void ws_opts_default(ws_opts* opts);
@@ -117,7 +120,12 @@ ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws
 /* Enumerate the primes of [L, R) in ascending order into out[0 .. *n_out).
  * Replaces run() with a value sink (MemorySink, sink.hpp:55-66).  Σ and ⊕
  * are always computed.  If the primes do not fit in cap, nothing is written
- * past cap, *n_out is the full count and WS_CAPACITY is returned. */
+ * past cap, *n_out is the full count and WS_CAPACITY is returned.
+ * Host output of more than one pipeline chunk (>= 128 segments) crosses PCIe
+ * in a 16-bit wire format -- each prime as its bit position in its 2^15-slot
+ * block plus one count per block -- and is widened on the host by a pool of
+ * threads (WHEELSIEVE_HOST_THREADS, default all; WHEELSIEVE_HOST_WIRE=0 ships
+ * uint64 values instead); order, count and checksums come from the device. */
 ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, uint64_t* out,
                              uint64_t cap, uint64_t* n_out, ws_checks* checks);
 

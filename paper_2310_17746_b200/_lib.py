@@ -44,7 +44,8 @@ class WsChecks(C.Structure):
 
 class WsTiming(C.Structure):
     _fields_ = [("base_ms", C.c_double), ("sieve_ms", C.c_double), ("total_ms", C.c_double),
-                ("launches", u64), ("segments", u64), ("base_primes", u64)]
+                ("launches", u64), ("segments", u64), ("base_primes", u64),
+                ("h2d_bytes", u64), ("d2h_bytes", u64)]
 
 
 def _load(path: str = LIB_PATH) -> C.CDLL:

@@ -26,6 +26,7 @@
 
 #include "wheelsieve/gpu.h"
 #include "ws_internal.h"
+#include "ws_wire.h"
 
 namespace {
 
@@ -133,7 +134,7 @@ struct ws_ctx {
   cudaStream_t stream = nullptr;
   uint32_t S = 1u << 18;
   int sms = 148;
-  int bps[3] = {2, 2, 2};  // resident blocks per SM per mode
+  int bps[wsk::kNumModes] = {2, 2, 2, 2};  // resident blocks per SM per mode
   std::string err;
   ws_timing timing{};
   cudaEvent_t ev[4] = {};
@@ -172,6 +173,17 @@ struct ws_ctx {
   cudaEvent_t ev_order = nullptr;
   static constexpr int kMaxChunks = 16;
   cudaEvent_t chunk_done[kMaxChunks] = {};
+  cudaEvent_t wire_done[kMaxChunks] = {};
+  // host-bound enumeration through the 16-bit wire format (ws_wire.cpp);
+  // WHEELSIEVE_HOST_WIRE=0 ships uint64 values instead
+  bool host_wire = true;
+  wswire::Pool* pool = nullptr;  // host expansion threads (created on first use)
+  DevBuf<uint16_t> wire;         // wire entries of every chunk
+  DevBuf<uint32_t> wblk;         // survivors per wire block
+  PinnedBuf pin_wire, pin_wblk;
+  uint64_t wire_piece = 1u << 22;  // entries per ring slot (WHEELSIEVE_WIRE_PIECE)
+  uint64_t wire_ring = 8;          // ring slots (WHEELSIEVE_WIRE_RING)
+  std::vector<cudaEvent_t> ring_ev;
   cudaEvent_t fill_done[2] = {}, sieve_done[2] = {};
   DevBuf<wsk::Run> runs;
   DevBuf<wsk::Job> jobs;
@@ -188,6 +200,14 @@ struct ws_ctx {
 
   ~ws_ctx() {
     cudaSetDevice(device);
+    if (pool) wswire::pool_destroy(pool);
+    wire.release();
+    wblk.release();
+    pin_wire.release();
+    pin_wblk.release();
+    for (cudaEvent_t e : wire_done)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ring_ev) cudaEventDestroy(e);
     for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n, &bucket[0], &bucket[1], &bcount[0], &bcount[1]})
       b->release();
     runs.release();
@@ -216,6 +236,20 @@ struct ws_ctx {
 };
 
 namespace {
+
+// Every host<->device copy goes through these, so ws_timing reports the
+// bytes that crossed PCIe in the last call.
+cudaError_t copy_async(ws_ctx* c, void* dst, const void* src, size_t n, cudaMemcpyKind k,
+                       cudaStream_t st) {
+  if (k == cudaMemcpyHostToDevice) c->timing.h2d_bytes += n;
+  if (k == cudaMemcpyDeviceToHost) c->timing.d2h_bytes += n;
+  return cudaMemcpyAsync(dst, src, n, k, st);
+}
+cudaError_t copy_sync(ws_ctx* c, void* dst, const void* src, size_t n, cudaMemcpyKind k) {
+  if (k == cudaMemcpyHostToDevice) c->timing.h2d_bytes += n;
+  if (k == cudaMemcpyDeviceToHost) c->timing.d2h_bytes += n;
+  return cudaMemcpy(dst, src, n, k);
+}
 
 uint64_t prime_count_bound(uint64_t L, uint64_t R) {
   if (R <= L) return 0;
@@ -269,9 +303,15 @@ double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
 // The segment kernel over every segment of ctx->h_jobs.  Without large
 // primes this is one launch; otherwise the segments are processed in windows
 // of W segments: bucket_fill (large-prime hit lists) then the sieve kernel.
+struct WireArgs {  // kEnumWire outputs
+  uint16_t* entries;
+  uint32_t* blk;
+  uint32_t log2w;
+};
+
 void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* out,
                unsigned long long out_cap, bool timed, uint32_t acc_base = 0,
-               bool record_start = true) {
+               bool record_start = true, const WireArgs* wire = nullptr) {
   uint64_t nseg = 0;
   for (const auto& j : c->h_jobs) nseg += j.nseg;
   const size_t nj = c->h_jobs.size();
@@ -288,10 +328,10 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   }
   void* hj = c->pin_up.alloc(nj * sizeof(wsk::Job), "pinned jobs");
   std::memcpy(hj, c->h_jobs.data(), nj * sizeof(wsk::Job));
-  ck(cudaMemcpyAsync(c->jobs.ptr, hj, nj * sizeof(wsk::Job), cudaMemcpyHostToDevice, c->stream),
+  ck(copy_async(c, c->jobs.ptr, hj, nj * sizeof(wsk::Job), cudaMemcpyHostToDevice, c->stream),
      "upload jobs");
   ck(cudaMemsetAsync(c->acc.ptr + acc_base, 0, nj * sizeof(wsk::JobAcc), c->stream), "zero acc");
-  if (mode == wsk::kEnumerate) {
+  if (mode >= wsk::kEnumerate) {
     c->status.reserve(nseg, "status");
     ck(cudaMemsetAsync(c->status.ptr, 0, nseg * sizeof(unsigned long long), c->stream),
        "zero status");
@@ -320,6 +360,11 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.out_cap = out_cap;
   p.words1 = c->words_out[0];
   p.words5 = c->words_out[1];
+  if (wire) {
+    p.out16 = wire->entries;
+    p.blk = wire->blk;
+    p.blk_log2w = wire->log2w;
+  }
   uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps[mode];
   // Buckets pay off only when most large primes are far above S (c4: up to
   // 120 S, c5: 16 S); up to a few S (c3: 3.8 S) the per-(prime, segment)
@@ -381,8 +426,8 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     c->runs.reserve(runs.size(), "runs");
     void* hr = c->pin_up.alloc(runs.size() * sizeof(wsk::Run), "pinned runs");
     std::memcpy(hr, runs.data(), runs.size() * sizeof(wsk::Run));
-    ck(cudaMemcpyAsync(c->runs.ptr, hr, runs.size() * sizeof(wsk::Run), cudaMemcpyHostToDevice,
-                       c->stream), "upload runs");
+    ck(copy_async(c, c->runs.ptr, hr, runs.size() * sizeof(wsk::Run), cudaMemcpyHostToDevice,
+                  c->stream), "upload runs");
   }
   // ev[2] (call start) / ev[4] order the fill stream after everything queued so far
   if (record_start) ck(cudaEventRecord(c->ev[2], c->stream), "event");
@@ -501,12 +546,12 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
 // memory and wait: the one synchronisation of a call.
 const wsk::JobAcc* fetch_results(ws_ctx* c, size_t n) {
   char* h = static_cast<char*>(c->pin_out.reserve(n * sizeof(wsk::JobAcc) + 16, "pinned out"));
-  ck(cudaMemcpyAsync(h, c->acc.ptr, n * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost, c->stream),
+  ck(copy_async(c, h, c->acc.ptr, n * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost, c->stream),
      "results");
   uint32_t* tabn = reinterpret_cast<uint32_t*>(h + n * sizeof(wsk::JobAcc));
   *tabn = c->nprimes;
   if (c->nprimes_dev)
-    ck(cudaMemcpyAsync(tabn, c->nprimes_dev, 4, cudaMemcpyDeviceToHost, c->stream), "table size");
+    ck(copy_async(c, tabn, c->nprimes_dev, 4, cudaMemcpyDeviceToHost, c->stream), "table size");
   ck(cudaStreamSynchronize(c->stream), "sync");
   ck(cudaGetLastError(), "kernel");
   c->timing.base_primes = *tabn + small_primes_upto(c->base_B);
@@ -568,6 +613,121 @@ bool is_device_ptr(const void* p) {
 // at once on the compute stream, and as each chunk finishes its values are
 // copied device->host on the copy stream while later chunks still sieve, so
 // the PCIe transfer (the bound for large outputs) hides the kernels.
+// Wire variant of the pipeline (ws_wire.cpp): the chunks' kernels write
+// 16-bit entries + per-block counts, each chunk crosses PCIe at 2 bytes per
+// prime, and the host pool widens it into `out` while later chunks copy.
+void enumerate_wire(ws_ctx* c, uint64_t L, uint64_t R, uint64_t nseg, uint64_t nch,
+                    const std::vector<uint64_t>& lo, const std::vector<uint64_t>& hi,
+                    const std::vector<uint64_t>& boff, uint64_t* out, uint64_t cap,
+                    ws_checks* chk) {
+  const uint64_t bslots = std::min<uint64_t>(c->S, wsk::kWireBlockSlots);
+  const uint64_t bps = c->S / bslots;
+  WireArgs wa{};
+  wa.log2w = static_cast<uint32_t>(__builtin_ctzll(bslots / 32));
+  c->wire.reserve(boff[nch] + 32, "wire entries");
+  c->wblk.reserve(nseg * bps, "wire block counts");
+  uint32_t* pb = static_cast<uint32_t*>(c->pin_wblk.reserve(nseg * bps * 4 + 64, "pinned wire"));
+  wsk::JobAcc* hacc = static_cast<wsk::JobAcc*>(
+      c->pin_out.reserve(nch * sizeof(wsk::JobAcc) + 16, "pinned out"));
+  std::vector<uint64_t> seg0(nch + 1), k0(nch);
+  for (uint64_t k = 0; k <= nch; ++k) seg0[k] = k * nseg / nch;
+  for (uint64_t k = 0; k < nch; ++k) {
+    const wsk::Job J = make_job(lo[k], hi[k], c->S, 0);
+    k0[k] = J.K0;
+    c->h_jobs.assign(1, J);
+    wa.entries = c->wire.ptr + boff[k];
+    wa.blk = c->wblk.ptr + seg0[k] * bps;
+    run_sieve(c, wsk::kEnumWire, nullptr, nullptr, boff[k + 1] - boff[k], true,
+              static_cast<uint32_t>(k), k == 0, &wa);
+    // accumulators straight into mapped pinned memory: no copy-engine entry
+    // on the compute stream to queue behind earlier chunks' payload copies
+    ck(wsk::launch_acc_to_host(c->acc.ptr + k, hacc + k, 1, c->stream), "chunk acc");
+    c->timing.launches += 1;
+    c->timing.d2h_bytes += sizeof(wsk::JobAcc);
+    ck(cudaEventRecord(c->chunk_done[k], c->stream), "event");
+  }
+  if (!c->pool) c->pool = wswire::pool_create(0);
+  // Payload pieces of `piece` entries cross into a ring of `ring` pinned
+  // slots, each expanded as soon as it lands and reused once expanded: a
+  // small reused staging set (64 MB by default) instead of one 0.9 GB
+  // buffer leaves more of the host's memory bandwidth to the 8-byte output
+  // (measured c2: 33.3 ms vs 35.7 ms per call; 1M x 8: 35.3, 256K x 8: 44).
+  const uint64_t piece = c->wire_piece, ring = c->wire_ring;
+  uint16_t* slots = static_cast<uint16_t*>(
+      c->pin_wire.reserve(piece * ring * sizeof(uint16_t) + 64, "pinned wire ring"));
+  while (c->ring_ev.size() < ring) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    c->ring_ev.push_back(e);
+  }
+  std::vector<wswire::Ticket> tickets(ring);
+  std::vector<uint64_t> opos(nch, 0), take(nch, 0);
+  struct Piece {
+    uint64_t k, a, m, slot;
+  };
+  std::vector<Piece> issued;
+  uint64_t kc = 0, ac = 0, pos = 0;
+  bool started = false;
+  // issues the next piece's D2H into the next ring slot; false when done
+  auto issue_next = [&]() -> bool {
+    while (kc < nch) {
+      if (!started) {
+        ck(cudaEventSynchronize(c->chunk_done[kc]), "chunk");
+        const uint64_t n = hacc[kc].count;
+        if (n > boff[kc + 1] - boff[kc]) throw Fail{WS_CUDA, "wire chunk exceeds its bound"};
+        take[kc] = pos < cap ? std::min(n, cap - pos) : 0;
+        opos[kc] = pos;
+        pos += n;
+        chk->count += n;
+        chk->sum += hacc[kc].sum;
+        chk->xor_ ^= hacc[kc].xr;
+        chk->largest = std::max<uint64_t>(chk->largest, hacc[kc].largest);
+        if (take[kc])
+          ck(copy_async(c, pb + seg0[kc] * bps, c->wblk.ptr + seg0[kc] * bps,
+                        (seg0[kc + 1] - seg0[kc]) * bps * 4, cudaMemcpyDeviceToHost, c->cstream),
+             "wire d2h");
+        started = true;
+        ac = 0;
+      }
+      if (ac < take[kc]) {
+        const uint64_t slot = issued.size() % ring;
+        if (issued.size() >= ring) wswire::ticket_wait(c->pool, &tickets[slot]);  // slot free
+        const uint64_t m = std::min(piece, take[kc] - ac);
+        ck(copy_async(c, slots + slot * piece, c->wire.ptr + boff[kc] + ac, m * sizeof(uint16_t),
+                      cudaMemcpyDeviceToHost, c->cstream), "wire d2h");
+        ck(cudaEventRecord(c->ring_ev[slot], c->cstream), "event");
+        issued.push_back(Piece{kc, ac, m, slot});
+        ac += m;
+        return true;
+      }
+      ++kc;
+      started = false;
+    }
+    return false;
+  };
+  try {
+    for (uint64_t r = 0; r + 1 < ring && issue_next(); ++r) {
+    }
+    for (size_t j = 0; j < issued.size(); ++j) {
+      const Piece pc = issued[j];
+      ck(cudaEventSynchronize(c->ring_ev[pc.slot]), "wire d2h");
+      // the piece holds entries [a, a + m) of chunk k; the expander finds
+      // entry a's block through the chunk's block counts
+      wswire::submit_expand(c->pool, slots + pc.slot * piece, pb + seg0[pc.k] * bps,
+                            (seg0[pc.k + 1] - seg0[pc.k]) * bps, k0[pc.k], bslots, pc.a, pc.m,
+                            out + opos[pc.k] + pc.a, &tickets[pc.slot]);
+      issue_next();  // into the slot of piece j + 1 - ring (waits for its expansion)
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    ck(cudaGetLastError(), "kernel");
+  } catch (...) {
+    wswire::pool_wait(c->pool);  // no task may outlive the call
+    throw;
+  }
+  wswire::pool_wait(c->pool);
+  c->timing.base_primes = c->nprimes + small_primes_upto(c->base_B);
+}
+
 void enumerate_to_host(ws_ctx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_t cap,
                        ws_checks* chk) {
   const wsk::Job whole = make_job(L, R, c->S, 0);
@@ -581,6 +741,9 @@ void enumerate_to_host(ws_ctx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_
     hi[k] = k + 1 == nch ? R : std::min<uint64_t>(R, lo0 + 6ull * c->S * b);
     boff[k + 1] = boff[k] + prime_count_bound(lo[k], hi[k]);
   }
+  // large outputs (several chunks) cross PCIe in the wire format
+  if (c->host_wire && nch > 1)
+    return enumerate_wire(c, L, R, nseg, nch, lo, hi, boff, out, cap, chk);
   c->vals.reserve(std::max<uint64_t>(boff[nch], 1), "enumeration buffer");
   wsk::JobAcc* hacc = static_cast<wsk::JobAcc*>(
       c->pin_out.reserve(nch * sizeof(wsk::JobAcc) + 16, "pinned out"));
@@ -588,8 +751,11 @@ void enumerate_to_host(ws_ctx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_
     c->h_jobs.assign(1, make_job(lo[k], hi[k], c->S, 0));
     run_sieve(c, wsk::kEnumerate, nullptr, c->vals.ptr + boff[k], boff[k + 1] - boff[k], true,
               static_cast<uint32_t>(k), k == 0);
-    ck(cudaMemcpyAsync(hacc + k, c->acc.ptr + k, sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost,
-                       c->stream), "chunk acc");
+    // accumulators straight into mapped pinned memory: no copy-engine entry
+    // on the compute stream to queue behind earlier chunks' payload copies
+    ck(wsk::launch_acc_to_host(c->acc.ptr + k, hacc + k, 1, c->stream), "chunk acc");
+    c->timing.launches += 1;
+    c->timing.d2h_bytes += sizeof(wsk::JobAcc);
     ck(cudaEventRecord(c->chunk_done[k], c->stream), "event");
   }
   uint64_t pos = 0;
@@ -598,8 +764,8 @@ void enumerate_to_host(ws_ctx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_
     const uint64_t n = hacc[k].count;
     const uint64_t take = pos < cap ? std::min(n, cap - pos) : 0;
     if (take)
-      ck(cudaMemcpyAsync(out + pos, c->vals.ptr + boff[k], take * 8, cudaMemcpyDeviceToHost,
-                         c->cstream), "d2h");
+      ck(copy_async(c, out + pos, c->vals.ptr + boff[k], take * 8, cudaMemcpyDeviceToHost,
+                    c->cstream), "d2h");
     pos += n;
     chk->count += n;
     chk->sum += hacc[k].sum;
@@ -706,6 +872,11 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_FILL_PIECE")) c->piece_override = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_RATIO")) c->bucket_min_ratio = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CTAS")) c->bucket_ctas_per_sm = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_HOST_WIRE")) c->host_wire = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
+    c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));
+  if (const char* e = std::getenv("WHEELSIEVE_WIRE_RING"))
+    c->wire_ring = std::max<uint64_t>(2, std::strtoull(e, nullptr, 10));
   c->sms = prop.multiProcessorCount;
   if (cudaSetDevice(dev) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -723,7 +894,8 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
             cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) == cudaSuccess;
   for (int i = 0; i < ws_ctx::kMaxChunks && ok; ++i)
-    ok = cudaEventCreateWithFlags(&c->chunk_done[i], cudaEventDisableTiming) == cudaSuccess;
+    ok = cudaEventCreateWithFlags(&c->chunk_done[i], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->wire_done[i], cudaEventDisableTiming) == cudaSuccess;
   if (ok) {
     std::vector<uint32_t> tab(wsk::small_table_words());
     wsk::build_small_tables(tab.data());
@@ -827,7 +999,7 @@ ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws
     const int mode = (flags & WS_WANT_CHECKS) ? wsk::kCountChecks : wsk::kCount;
     run_sieve(ctx, mode, dps, nullptr, 0, true);
     if (per_seg && !dev_out)
-      ck(cudaMemcpyAsync(per_seg, dps, std::min(nseg, per_seg_cap) * sizeof(uint32_t),
+      ck(copy_async(ctx, per_seg, dps, std::min(nseg, per_seg_cap) * sizeof(uint32_t),
                          cudaMemcpyDeviceToHost, ctx->stream), "per_seg");
     const wsk::JobAcc a = *fetch_results(ctx, 1);
     out->count = a.count;
@@ -866,8 +1038,8 @@ ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags
       dst = reinterpret_cast<unsigned long long*>(out) + std::min(npre, cap);
       dcap = cap > npre ? cap - npre : 0;
       if (npre && cap)
-        ck(cudaMemcpyAsync(out, pre, std::min(npre, cap) * 8, cudaMemcpyHostToDevice,
-                           ctx->stream), "prelude");
+        ck(copy_async(ctx, out, pre, std::min(npre, cap) * 8, cudaMemcpyHostToDevice,
+                      ctx->stream), "prelude");
     } else {
       for (uint64_t i = 0; i < npre && i < cap; ++i) out[i] = pre[i];
       enumerate_to_host(ctx, L, R, out + std::min(npre, cap), cap > npre ? cap - npre : 0, &chk);
@@ -942,17 +1114,17 @@ ws_status ws_sieve_segment(ws_ctx* ctx, uint64_t start, uint64_t len, uint32_t f
     ctx->words_out[0] = ctx->words_out[1] = nullptr;
     // uint32 LSB-first words are byte-identical to FlagArray's uint64 words
     const cudaMemcpyKind k = dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    ck(cudaMemcpyAsync(r1_words, tmp.ptr, out64 * 8, k, ctx->stream), "r1 words");
-    ck(cudaMemcpyAsync(r5_words, tmp.ptr + words32, out64 * 8, k, ctx->stream), "r5 words");
+    ck(copy_async(ctx, r1_words, tmp.ptr, out64 * 8, k, ctx->stream), "r1 words");
+    ck(copy_async(ctx, r5_words, tmp.ptr + words32, out64 * 8, k, ctx->stream), "r5 words");
     fetch_results(ctx, 1);
     tmp.release();
     // sieve_segment leaves the value 1 set; callers clear it (engine.cpp:244)
     if (start == 0) {
       if (dev_out) {
         uint64_t w0 = 0;
-        ck(cudaMemcpy(&w0, r1_words, 8, cudaMemcpyDeviceToHost), "w0");
+        ck(copy_sync(ctx, &w0, r1_words, 8, cudaMemcpyDeviceToHost), "w0");
         w0 |= 1;
-        ck(cudaMemcpy(r1_words, &w0, 8, cudaMemcpyHostToDevice), "w0");
+        ck(copy_sync(ctx, r1_words, &w0, 8, cudaMemcpyHostToDevice), "w0");
       } else {
         r1_words[0] |= 1;
       }
@@ -972,7 +1144,7 @@ ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64
     const uint64_t* L = Ls;
     if (dev_out) {
       hL.resize(n);
-      ck(cudaMemcpy(hL.data(), Ls, n * 8, cudaMemcpyDeviceToHost), "intervals in");
+      ck(copy_sync(ctx, hL.data(), Ls, n * 8, cudaMemcpyDeviceToHost), "intervals in");
       L = hL.data();
     }
     uint64_t maxR = 0, seg = 0;
@@ -1006,9 +1178,9 @@ ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64
       hx[i] = o.xor_;
     }
     if (dev_out) {
-      ck(cudaMemcpy(counts, hc.data(), n * 4, cudaMemcpyHostToDevice), "counts");
-      if (sums) ck(cudaMemcpy(sums, hs.data(), n * 8, cudaMemcpyHostToDevice), "sums");
-      if (xors) ck(cudaMemcpy(xors, hx.data(), n * 8, cudaMemcpyHostToDevice), "xors");
+      ck(copy_sync(ctx, counts, hc.data(), n * 4, cudaMemcpyHostToDevice), "counts");
+      if (sums) ck(copy_sync(ctx, sums, hs.data(), n * 8, cudaMemcpyHostToDevice), "sums");
+      if (xors) ck(copy_sync(ctx, xors, hx.data(), n * 8, cudaMemcpyHostToDevice), "xors");
     } else {
       std::memcpy(counts, hc.data(), n * 4);
       if (sums) std::memcpy(sums, hs.data(), n * 8);

@@ -27,7 +27,13 @@ struct JobAcc {
   unsigned long long count, sum, xr, largest;
 };
 
-enum Mode : int { kCount = 0, kCountChecks = 1, kEnumerate = 2 };
+// kEnumWire: ordered enumeration into the 16-bit host wire format -- each
+// prime as its bit position e in the interleaved survivor masks of its
+// 2^15-slot block (value = 6 * block_first_slot + 3e + 1 + (e & 1)), plus a
+// survivor count per block; the host expands it (ws_wire.cpp).
+enum Mode : int { kCount = 0, kCountChecks = 1, kEnumerate = 2, kEnumWire = 3 };
+constexpr int kNumModes = 4;
+constexpr uint32_t kWireBlockSlots = 1u << 15;
 
 // Large-prime buckets: per window of segments, the hits of every prime
 // p >= S (at most one per class per segment) are scattered into per-segment
@@ -67,6 +73,9 @@ struct SieveParams {
   unsigned long long* status;        // enumeration look-back words (zeroed)
   unsigned long long* out;           // enumeration output (after 2 and 3)
   unsigned long long out_cap;
+  uint16_t* out16;                   // kEnumWire: entries (same positions as `out`)
+  uint32_t* blk;                     // kEnumWire: survivors per block, segment s at s * bps
+  uint32_t blk_log2w;                // kEnumWire: log2(32-slot words per block)
   uint32_t* words1;                  // nullable (count modes): survivor flag words of
   uint32_t* words5;                  // each class, segment s at word s * S / 32
 };
@@ -74,9 +83,11 @@ struct SieveParams {
 size_t sieve_smem_bytes(uint32_t S, int mode);
 uint32_t small_table_words();
 void build_small_tables(uint32_t* out);  // host
-// blocks_per_sm[mode] for the three modes
+// blocks_per_sm[mode] for the kNumModes modes
 cudaError_t sieve_configure(int* blocks_per_sm);
 cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st);
+cudaError_t launch_acc_to_host(const JobAcc* acc, JobAcc* host_mapped, uint32_t n,
+                               cudaStream_t st);
 
 struct FillParams {
   const Run* runs;

@@ -492,12 +492,12 @@ constexpr uint32_t kStage = 1024;
 
 template <int MODE>
 constexpr size_t mode_smem_extra() {
-  return MODE == kEnumerate ? kWarps * kStage * sizeof(uint16_t) : 0;
+  return MODE >= kEnumerate ? kWarps * kStage * sizeof(uint16_t) : 0;
 }
 
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_kernel(const SieveParams P) {
+__global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_kernel(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bm1 = smem;
   uint32_t* bm5 = smem + P.S / 32;
@@ -509,6 +509,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
   __shared__ uint32_t wc_ctr;
   __shared__ unsigned long long seg_base;
   __shared__ uint32_t seg_total;
+  __shared__ uint32_t blk_cnt[kWarps];  // kEnumWire: survivors per block (<= 8 blocks)
+  constexpr bool kWire = MODE == kEnumWire;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 
   for (uint32_t i = threadIdx.x; i < kTabWords; i += blockDim.x) tab[i] = __ldg(P.small_tab + i);
@@ -519,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
       fetch_segment(P, si);
       wc_ctr = 0;
     }
+    if (kWire && threadIdx.x < kWarps) blk_cnt[threadIdx.x] = 0;
     __syncthreads();
     if (si.s == ~0ull) break;
     init_words(si, tab, bm1, bm5);
@@ -528,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
     if (P.bucket != nullptr && threadIdx.x == 0) P.bcount[si.s - P.s_begin] = 0;
 
     const uint64_t vbase = 6 * si.ks;
-    if (MODE != kEnumerate && P.words1 != nullptr) {  // SegmentBitmap export
+    if (MODE < kEnumerate && P.words1 != nullptr) {  // SegmentBitmap export
       const uint64_t wb = si.s * (P.S / 32);  // single-job launches
       const uint32_t nw = (si.len + 63) / 64 * 2;  // whole uint64 FlagArray words
       for (uint32_t w = threadIdx.x; w < nw; w += kThreads) {
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
         P.words5[wb + w] = ~bm5[w];
       }
     }
-    if (MODE != kEnumerate) {
+    if (MODE < kEnumerate) {
       uint32_t cnt = 0;
       unsigned long long lg = 0, sum = 0, xr = 0;
       for (uint32_t wp = threadIdx.x; wp < si.nwords; wp += kThreads) {
@@ -601,11 +604,12 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
       }
     } else {
       // ---- ordered enumeration ----
-      // warp `warp` owns logical words [w_begin, w_end); the last warp also
-      // takes the remainder, so warp order is word order.
-      const uint32_t wpw = si.nwords / kWarps;
-      const uint32_t w_begin = warp * wpw;
-      const uint32_t w_end = warp == kWarps - 1 ? si.nwords : w_begin + wpw;
+      // warp `warp` owns logical words [w_begin, w_end), in word order; the
+      // shares are whole 32-word rounds so that no round straddles a wire
+      // block (1024 words) even in a clipped last segment
+      const uint32_t wpw = (si.nwords + 32 * kWarps - 1) / (32 * kWarps) * 32;
+      const uint32_t w_begin = min(warp * wpw, si.nwords);
+      const uint32_t w_end = min(w_begin + wpw, si.nwords);
       uint32_t cnt = 0;
       for (uint32_t w = w_begin + lane; w < w_end; w += 32)
         cnt += __popc(~bm1[w]) + __popc(~bm5[w]);
@@ -657,7 +661,24 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
           // 2) coalesced: lane i writes survivors i, i+32, ... of the round
           unsigned long long* dst = P.out + pos;
           uint32_t soff = 0, n = 0;
-          if (seg_fits) {
+          if (kWire) {
+            // entry = bit position in the block's interleaved masks; rounds
+            // never straddle a block (32-word aligned, blocks of 1024 words
+            // or one whole segment)
+            uint16_t* dst16 = P.out16 + pos;
+            const uint32_t eofs = (w0 & ((1u << P.blk_log2w) - 1u)) << 6;
+            if (lane == 0) atomicAdd(&blk_cnt[w0 >> P.blk_log2w], rtotal);
+#pragma unroll 4
+            for (uint32_t i = lane; i < rtotal; i += 32) {
+              const uint32_t e = stage[i];
+              const uint32_t bb = e & 63u;
+              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+              if (seg_fits || pos + i < P.out_cap) dst16[i] = static_cast<uint16_t>(eofs + e);
+              soff += off;
+              ++n;
+              xr ^= rbase + off;
+            }
+          } else if (seg_fits) {
 #pragma unroll 4
             for (uint32_t i = lane; i < rtotal; i += 32) {
               const uint32_t e = stage[i];
@@ -688,11 +709,18 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
           __syncwarp();
         } else {
           unsigned long long o = pos + (incl - c);
+          if (kWire && lane == 0) atomicAdd(&blk_cnt[w0 >> P.blk_log2w], rtotal);
           for (int half = 0; half < 2; ++half)
             for (uint32_t x = half ? hi : lo; x; x &= x - 1) {
               const uint32_t bb = (__ffs(x) - 1) + 32u * half;
               const unsigned long long v = rbase + (192u * lane + 3u * bb + 1u + (bb & 1u));
-              if (o < P.out_cap) P.out[o] = v;
+              if (o < P.out_cap) {
+                if (kWire)
+                  P.out16[o] = static_cast<uint16_t>(
+                      (((w0 & ((1u << P.blk_log2w) - 1u)) + lane) << 6) | bb);
+                else
+                  P.out[o] = v;
+              }
               ++o;
               sum += v;
               xr ^= v;
@@ -711,6 +739,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kEnumerate ? 2 : 3) sieve_ke
         red_c[warp] = lg;
       }
       __syncthreads();
+      if (kWire && warp == 1) {
+        const uint32_t bps = max(1u, (P.S / 32) >> P.blk_log2w);
+        if (lane < bps) P.blk[si.s * bps + lane] = blk_cnt[lane];
+      }
       if (warp == 0) {
         unsigned long long su = lane < kWarps ? red_a[lane] : 0ull;
         unsigned long long x = lane < kWarps ? red_b[lane] : 0ull;
@@ -869,15 +901,16 @@ void build_small_tables(uint32_t* out) {
 
 size_t sieve_smem_bytes(uint32_t S, int mode) {
   const size_t base = (2 * (S / 32) + kTabWords) * sizeof(uint32_t);
-  return base + (mode == kEnumerate ? mode_smem_extra<kEnumerate>() : 0);
+  return base + (mode >= kEnumerate ? mode_smem_extra<kEnumerate>() : 0);
 }
 
 cudaError_t sieve_configure(int* blocks_per_sm) {
   cudaError_t e;
-  const void* fns[3] = {reinterpret_cast<const void*>(sieve_kernel<kCount>),
-                        reinterpret_cast<const void*>(sieve_kernel<kCountChecks>),
-                        reinterpret_cast<const void*>(sieve_kernel<kEnumerate>)};
-  for (int m = 0; m < 3; ++m) {
+  const void* fns[kNumModes] = {reinterpret_cast<const void*>(sieve_kernel<kCount>),
+                                reinterpret_cast<const void*>(sieve_kernel<kCountChecks>),
+                                reinterpret_cast<const void*>(sieve_kernel<kEnumerate>),
+                                reinterpret_cast<const void*>(sieve_kernel<kEnumWire>)};
+  for (int m = 0; m < kNumModes; ++m) {
     const size_t smem = sieve_smem_bytes(1u << 18, m);
     e = cudaFuncSetAttribute(fns[m], cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
@@ -895,7 +928,8 @@ cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t 
   switch (mode) {
     case kCount: sieve_kernel<kCount><<<grid, kThreads, smem, st>>>(p); break;
     case kCountChecks: sieve_kernel<kCountChecks><<<grid, kThreads, smem, st>>>(p); break;
-    default: sieve_kernel<kEnumerate><<<grid, kThreads, smem, st>>>(p); break;
+    case kEnumerate: sieve_kernel<kEnumerate><<<grid, kThreads, smem, st>>>(p); break;
+    default: sieve_kernel<kEnumWire><<<grid, kThreads, smem, st>>>(p); break;
   }
   return cudaGetLastError();
 }
@@ -907,6 +941,19 @@ cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st) {
   dim3 grid(nb, f.nruns);
   const size_t smem = (f.max_run_segs + 2 * kFillPrimesPerBlock) * sizeof(uint32_t);
   bucket_fill_kernel<<<grid, kFillThreads, smem, st>>>(f);
+  return cudaGetLastError();
+}
+
+// Copies n job accumulators to mapped pinned host memory with plain stores
+// (no copy engine: the pipelined enumeration keeps the D2H engine busy with
+// chunk payloads, and a queued 32-byte copy would stall the compute stream).
+__global__ void acc_to_host_kernel(const JobAcc* a, JobAcc* host, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) host[i] = a[i];
+}
+
+cudaError_t launch_acc_to_host(const JobAcc* acc, JobAcc* host_mapped, uint32_t n,
+                               cudaStream_t st) {
+  acc_to_host_kernel<<<1, 32, 0, st>>>(acc, host_mapped, n);
   return cudaGetLastError();
 }
 
