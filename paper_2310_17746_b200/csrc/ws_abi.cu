@@ -164,6 +164,7 @@ struct ws_ctx {
   uint32_t piece_override = 0;         // tuning knob (WHEELSIEVE_FILL_PIECE)
   uint32_t bucket_min_ratio = 8;       // buckets iff largest base prime >= ratio * S
   uint32_t bucket_ctas_per_sm = 0;     // tuning knob (WHEELSIEVE_BUCKET_CTAS)
+  uint32_t ctas_per_sm = 0;            // tuning knob, all launches (WHEELSIEVE_CTAS_PER_SM)
 
   // scratch
   DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)
@@ -366,6 +367,8 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     p.blk_log2w = wire->log2w;
   }
   uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps[mode];
+  if (c->ctas_per_sm)
+    max_grid = std::min<uint64_t>(max_grid, static_cast<uint64_t>(c->sms) * c->ctas_per_sm);
   // Buckets pay off only when most large primes are far above S (c4: up to
   // 120 S, c5: 16 S); up to a few S (c3: 3.8 S) the per-(prime, segment)
   // offset check in the kernel is cheaper than fill + apply + windowing.
@@ -872,6 +875,7 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_FILL_PIECE")) c->piece_override = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_RATIO")) c->bucket_min_ratio = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CTAS")) c->bucket_ctas_per_sm = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_CTAS_PER_SM")) c->ctas_per_sm = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_HOST_WIRE")) c->host_wire = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
     c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));

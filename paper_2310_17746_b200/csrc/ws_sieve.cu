@@ -230,25 +230,37 @@ __device__ void fetch_segment(const SieveParams& P, SegInfo& si) {
 // bitmaps hold COMPOSITE flags (bit set = crossed off or outside [L, R)):
 // the complement of the reference's FlagArray, so crossing off is a single
 // ATOMS.OR and survivors are ~word.
+// Stamps the small-prime patterns into the segment: one 32-bit word per
+// thread and iteration (a warp writes 128 contiguous bytes = one shared
+// wavefront, and its table reads are conflict-free; 4-word-per-lane 128-bit
+// stores move the same bytes but make the lanes' table reads 4-way bank
+// conflicted).  Table phases are carried incrementally (+32 * kThreads mod Q
+// per iteration) instead of a modulo per word.
+__device__ __forceinline__ uint32_t phase_step(uint32_t a, uint32_t step, uint32_t Q) {
+  a += step;
+  return a >= Q ? a - Q : a;
+}
+
 __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* tab, uint32_t* bm1,
                                            uint32_t* bm5) {
-  const uint32_t o0 = static_cast<uint32_t>(si.ks % 5005u);
-  const uint32_t o1 = static_cast<uint32_t>(si.ks % 7429u);
-  const uint32_t o2 = static_cast<uint32_t>(si.ks % 899u);
-  const uint32_t o3 = static_cast<uint32_t>(si.ks % 1517u);
-  const uint32_t o4 = static_cast<uint32_t>(si.ks % 2021u);
+  constexpr uint32_t kStride = 32u * kThreads;
+  uint32_t a0 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 5005u);
+  uint32_t a1 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 7429u);
+  uint32_t a2 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 899u);
+  uint32_t a3 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 1517u);
+  uint32_t a4 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 2021u);
   const uint32_t* t1 = tab;
   const uint32_t* t5 = tab + kTabPerClass;
   for (uint32_t w = threadIdx.x; w < si.nwords; w += kThreads) {
-    const uint32_t a0 = (o0 + 32 * w) % 5005u;
-    const uint32_t a1 = (o1 + 32 * w) % 7429u;
-    const uint32_t a2 = (o2 + 32 * w) % 899u;
-    const uint32_t a3 = (o3 + 32 * w) % 1517u;
-    const uint32_t a4 = (o4 + 32 * w) % 2021u;
     uint32_t m1 = tab_read(t1, a0) & tab_read(t1 + tab_off(1), a1) & tab_read(t1 + tab_off(2), a2) &
                   tab_read(t1 + tab_off(3), a3) & tab_read(t1 + tab_off(4), a4);
     uint32_t m5 = tab_read(t5, a0) & tab_read(t5 + tab_off(1), a1) & tab_read(t5 + tab_off(2), a2) &
                   tab_read(t5 + tab_off(3), a3) & tab_read(t5 + tab_off(4), a4);
+    a0 = phase_step(a0, kStride % 5005u, 5005u);
+    a1 = phase_step(a1, kStride % 7429u, 7429u);
+    a2 = phase_step(a2, kStride % 899u, 899u);
+    a3 = phase_step(a3, kStride % 1517u, 1517u);
+    a4 = phase_step(a4, kStride % 2021u, 2021u);
     if (w == 0 && si.ks < 8) {
       // the stamped primes themselves survive: 7, 13, 19, 31, 37, 43 at
       // class-1 indices 1, 2, 3, 5, 6, 7 and 5, 11, 17, 23, 29, 41, 47 at
@@ -264,9 +276,6 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
   }
 }
 
-// First hits (segment-relative) of prime p in both classes, or false when
-// p is not yet active in this segment (p*p beyond its end; since primes
-// ascend, no later prime is active either).
 // First hits (segment-relative) of prime p in both classes, or false when
 // p is not yet active in this segment (p*p beyond its end; since primes
 // ascend, no later prime is active either).  The activation test is two
