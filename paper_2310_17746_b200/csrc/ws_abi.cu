@@ -383,6 +383,8 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     if (c->cap_override) cap = c->cap_override;
     W = std::max<uint64_t>(8, c->bucket_budget / (4ull * cap));
     W = std::min<uint64_t>({W, wsk::kMaxWindow, nseg});
+    // the fill kernel indexes a window's lists with 32-bit entry indices
+    W = std::min<uint64_t>(W, ((1ull << 32) - (1ull << 26)) / cap - 1);
     for (int b = 0; b < 2; ++b) {
       c->bucket[b].reserve(W * cap, "bucket lists");
       c->bcount[b].reserve(W, "bucket counts");

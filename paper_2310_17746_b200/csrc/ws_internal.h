@@ -37,7 +37,8 @@ constexpr uint32_t kWireBlockSlots = 1u << 15;
 
 // Large-prime buckets: per window of segments, the hits of every prime
 // p >= S (at most one per class per segment) are scattered into per-segment
-// lists of uint32 entries (slot | class << 18) by bucket_fill_kernel and
+// lists of uint32 entries (slot | class * S: the bit index into the CTA's
+// contiguous [6k+1 | 6k+5] bitmap) by bucket_fill_kernel and
 // applied by the sieve kernel.  A list that overflows its capacity is
 // detected by the sieve kernel, which then processes that segment's large
 // primes directly (correct, just slower).

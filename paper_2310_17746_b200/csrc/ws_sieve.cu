@@ -393,22 +393,34 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     mark_if(a5, rel5, len);
   }
   if (use_bucket) {
+    // an entry is the bit index into [bm1 | bm5] (class at bit log2 S), so a
+    // hit is shift + atomic; lists are read 4 entries per 128-bit streamed
+    // load, two loads in flight per thread
     const uint64_t ls = si.s - P.s_begin;
     const uint32_t n = P.bcount[ls];
-    const uint32_t* list = P.bucket + ls * P.bcap;
+    const uint32_t* list = P.bucket + ls * P.bcap;  // 128 B aligned (bcap % 32 == 0)
+    const uint4* list4 = reinterpret_cast<const uint4*>(list);
+    const uint32_t n4 = n >> 2;
     uint32_t i = threadIdx.x;
-    for (; i + 3 * kThreads < n; i += 4 * kThreads) {  // 4 streamed loads in flight
-      const uint32_t e0 = __ldcs(list + i), e1 = __ldcs(list + i + kThreads);
-      const uint32_t e2 = __ldcs(list + i + 2 * kThreads), e3 = __ldcs(list + i + 3 * kThreads);
-      mark((e0 >> 18) ? a5 : a1, e0 & 0x3FFFFu);
-      mark((e1 >> 18) ? a5 : a1, e1 & 0x3FFFFu);
-      mark((e2 >> 18) ? a5 : a1, e2 & 0x3FFFFu);
-      mark((e3 >> 18) ? a5 : a1, e3 & 0x3FFFFu);
+    for (; i + kThreads < n4; i += 2 * kThreads) {
+      const uint4 x = __ldcs(list4 + i), y = __ldcs(list4 + i + kThreads);
+      mark(a1, x.x);
+      mark(a1, x.y);
+      mark(a1, x.z);
+      mark(a1, x.w);
+      mark(a1, y.x);
+      mark(a1, y.y);
+      mark(a1, y.z);
+      mark(a1, y.w);
     }
-    for (; i < n; i += kThreads) {
-      const uint32_t e = __ldcs(list + i);
-      mark((e >> 18) ? a5 : a1, e & 0x3FFFFu);
+    if (i < n4) {
+      const uint4 x = __ldcs(list4 + i);
+      mark(a1, x.x);
+      mark(a1, x.y);
+      mark(a1, x.z);
+      mark(a1, x.w);
     }
+    for (uint32_t j = 4 * n4 + threadIdx.x; j < n; j += kThreads) mark(a1, __ldcs(list + j));
   }
 }
 
@@ -804,20 +816,24 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
       if (prime_offsets(p, i, F.prime_inv, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
         if (q1 < span) r1 = q1;
         if (q5 < span) r5 = q5;
-        // 64-bit stepping: p can be within `span` of 2^32 near the top of
-        // the 64-bit value range, where a 32-bit h + p would wrap
-        for (uint64_t h = r1; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
-        for (uint64_t h = r5; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+        if (p <= 0xFFFFFFFFu - span) {  // 32-bit stepping cannot wrap
+          for (uint32_t h = r1; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+          for (uint32_t h = r5; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+        } else {  // p within `span` of 2^32 (top of the 64-bit value range)
+          for (uint64_t h = r1; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+          for (uint64_t h = r5; h < span; h += p) atomicAdd(hist + (h >> F.log2S), 1u);
+        }
       }
     }
     first1[li] = r1;
     first5[li] = r5;
   }
   __syncthreads();
-  // reserve one contiguous slice per (block, segment)
+  // reserve one contiguous slice per (block, segment); the cursor becomes
+  // the slice's window-global entry index (the window holds < 2^32 entries)
   for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) {
     const uint32_t c = hist[i];
-    hist[i] = c ? atomicAdd(F.bcount + run.seg0 + i, c) : 0u;
+    hist[i] = (run.seg0 + i) * F.bcap + (c ? atomicAdd(F.bcount + run.seg0 + i, c) : 0u);
   }
   __syncthreads();
   // pass 2: write the entries
@@ -829,14 +845,20 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
     const uint32_t r1 = first1[li], r5 = first5[li];
     if (r1 == 0xFFFFFFFFu && r5 == 0xFFFFFFFFu) continue;
     const uint32_t p = F.prime_p[i];
-    for (int c = 0; c < 2; ++c) {
-      for (uint64_t h = c ? r5 : r1; h < span; h += p) {
-        const uint32_t seg = static_cast<uint32_t>(h >> F.log2S);
-        const uint32_t pos = atomicAdd(hist + seg, 1u);
-        if (pos < F.bcap)
-          F.bucket[static_cast<uint64_t>(run.seg0 + seg) * F.bcap + pos] =
-              (static_cast<uint32_t>(h) & (S - 1)) | (static_cast<uint32_t>(c) << 18);
-      }
+    // an entry is written while its segment's list has room: index below
+    // the end of the segment's list (overflow is detected by the sieve)
+    auto put = [&](uint32_t seg, uint32_t entry) {
+      const uint32_t idx = atomicAdd(hist + seg, 1u);
+      if (idx < (run.seg0 + seg + 1) * F.bcap) F.bucket[idx] = entry;
+    };
+    if (p <= 0xFFFFFFFFu - span) {
+      for (uint32_t h = r1; h < span; h += p) put(h >> F.log2S, h & (S - 1));
+      for (uint32_t h = r5; h < span; h += p) put(h >> F.log2S, (h & (S - 1)) | S);
+    } else {
+      for (uint64_t h = r1; h < span; h += p)
+        put(static_cast<uint32_t>(h >> F.log2S), static_cast<uint32_t>(h) & (S - 1));
+      for (uint64_t h = r5; h < span; h += p)
+        put(static_cast<uint32_t>(h >> F.log2S), (static_cast<uint32_t>(h) & (S - 1)) | S);
     }
   }
 }
