@@ -182,6 +182,10 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # the host-side wire expanders of co-located ranks share the host's cores
+    nloc = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    if nloc > 1 and "WHEELSIEVE_HOST_THREADS" not in os.environ:
+        os.environ["WHEELSIEVE_HOST_THREADS"] = str(max(1, len(os.sched_getaffinity(0)) // nloc))
     return ws, rank, local
 
 

@@ -17,6 +17,7 @@
 #include "ws_wire.h"
 
 #include <immintrin.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <condition_variable>
@@ -93,7 +94,11 @@ unsigned default_threads() {
     const long v = std::strtol(e, nullptr, 10);
     if (v > 0) return static_cast<unsigned>(std::min<long>(v, 256));
   }
-  const unsigned h = std::thread::hardware_concurrency();
+  // the CPUs this process may run on (affinity / cgroup), not the machine's
+  cpu_set_t set;
+  unsigned h = 0;
+  if (sched_getaffinity(0, sizeof set, &set) == 0) h = static_cast<unsigned>(CPU_COUNT(&set));
+  if (!h) h = std::thread::hardware_concurrency();
   return std::max(1u, std::min(h ? h : 4u, 64u));
 }
 
