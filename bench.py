@@ -316,7 +316,7 @@ def run_ours(args, cfg, world, rank, local):
                "h2d_bytes_per_step": int(tm.h2d_bytes) * world,
                "d2h_bytes_per_step": int(tm.d2h_bytes) * world,
                "ms_per_step": e_ms, "steps": k_e2e, "timer": "host wall clock per call",
-               "transfer": ("16-bit wire entries + per-block counts, widened on the host "
+               "transfer": ("8-bit wire entries + per-block counts, widened on the host "
                             "(ws_wire.cpp)") if wire else "uint64 values",
                "host_values_verified": True}
     elif kind in ("count", "checks"):

@@ -96,7 +96,7 @@ typedef struct ws_timing {
   uint64_t base_primes; /* sieving primes (>= 5) used by the last call */
   uint64_t h2d_bytes;   /* bytes copied host->device by the last call */
   uint64_t d2h_bytes;   /* bytes copied device->host by the last call (host-bound
-                           enumeration ships 2 bytes per prime, see ws_enumerate_range) */
+                           enumeration ships ~1 byte per prime, see ws_enumerate_range) */
 } ws_timing;
 
 void ws_opts_default(ws_opts* opts);
@@ -122,10 +122,11 @@ ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws
  * are always computed.  If the primes do not fit in cap, nothing is written
  * past cap, *n_out is the full count and WS_CAPACITY is returned.
  * Host output of more than one pipeline chunk (>= 128 segments) crosses PCIe
- * in a 16-bit wire format -- each prime as its bit position in its 2^15-slot
- * block plus one count per block -- and is widened on the host by a pool of
- * threads (WHEELSIEVE_HOST_THREADS, default all; WHEELSIEVE_HOST_WIRE=0 ships
- * uint64 values instead); order, count and checksums come from the device. */
+ * in an 8-bit wire format -- each prime as its bit position in its 128-slot
+ * block, one count byte per block and per-segment totals -- and is widened on
+ * the host by a pool of threads (WHEELSIEVE_HOST_THREADS, default the CPUs of
+ * the process's affinity mask; WHEELSIEVE_HOST_WIRE=0 ships uint64 values
+ * instead); order, count and checksums come from the device. */
 ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, uint64_t* out,
                              uint64_t cap, uint64_t* n_out, ws_checks* checks);
 

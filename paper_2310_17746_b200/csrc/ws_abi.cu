@@ -175,14 +175,14 @@ struct ws_ctx {
   static constexpr int kMaxChunks = 16;
   cudaEvent_t chunk_done[kMaxChunks] = {};
   cudaEvent_t wire_done[kMaxChunks] = {};
-  // host-bound enumeration through the 16-bit wire format (ws_wire.cpp);
+  // host-bound enumeration through the 8-bit wire format (ws_wire.cpp);
   // WHEELSIEVE_HOST_WIRE=0 ships uint64 values instead
   bool host_wire = true;
   wswire::Pool* pool = nullptr;  // host expansion threads (created on first use)
-  DevBuf<uint16_t> wire;         // wire entries of every chunk
-  DevBuf<uint32_t> wblk;         // survivors per wire block
+  DevBuf<uint8_t> wire;          // wire entries of every chunk
+  DevBuf<uint8_t> wblk;          // survivors per wire block
   PinnedBuf pin_wire, pin_wblk;
-  uint64_t wire_piece = 1u << 22;  // entries per ring slot (WHEELSIEVE_WIRE_PIECE)
+  uint64_t wire_piece = 1u << 23;  // entries (bytes) per ring slot (WHEELSIEVE_WIRE_PIECE)
   uint64_t wire_ring = 8;          // ring slots (WHEELSIEVE_WIRE_RING)
   std::vector<cudaEvent_t> ring_ev;
   cudaEvent_t fill_done[2] = {}, sieve_done[2] = {};
@@ -305,9 +305,8 @@ double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
 // primes this is one launch; otherwise the segments are processed in windows
 // of W segments: bucket_fill (large-prime hit lists) then the sieve kernel.
 struct WireArgs {  // kEnumWire outputs
-  uint16_t* entries;
-  uint32_t* blk;
-  uint32_t log2w;
+  uint8_t* entries;
+  uint8_t* blk8;
 };
 
 void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* out,
@@ -362,9 +361,8 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.words1 = c->words_out[0];
   p.words5 = c->words_out[1];
   if (wire) {
-    p.out16 = wire->entries;
-    p.blk = wire->blk;
-    p.blk_log2w = wire->log2w;
+    p.out8 = wire->entries;
+    p.blk8 = wire->blk8;
   }
   uint64_t max_grid = static_cast<uint64_t>(c->sms) * c->bps[mode];
   if (c->ctas_per_sm)
@@ -618,48 +616,51 @@ bool is_device_ptr(const void* p) {
 // at once on the compute stream, and as each chunk finishes its values are
 // copied device->host on the copy stream while later chunks still sieve, so
 // the PCIe transfer (the bound for large outputs) hides the kernels.
-// Wire variant of the pipeline (ws_wire.cpp): the chunks' kernels write
-// 16-bit entries + per-block counts, each chunk crosses PCIe at 2 bytes per
-// prime, and the host pool widens it into `out` while later chunks copy.
-void enumerate_wire(ws_ctx* c, uint64_t L, uint64_t R, uint64_t nseg, uint64_t nch,
-                    const std::vector<uint64_t>& lo, const std::vector<uint64_t>& hi,
-                    const std::vector<uint64_t>& boff, uint64_t* out, uint64_t cap,
-                    ws_checks* chk) {
-  const uint64_t bslots = std::min<uint64_t>(c->S, wsk::kWireBlockSlots);
-  const uint64_t bps = c->S / bslots;
-  WireArgs wa{};
-  wa.log2w = static_cast<uint32_t>(__builtin_ctzll(bslots / 32));
-  c->wire.reserve(boff[nch] + 32, "wire entries");
+// Wire variant of the pipeline (ws_wire.cpp): the chunks' kernels write one
+// byte per prime + one count byte per 128-slot block + per-segment totals;
+// each chunk crosses PCIe at ~1 byte per prime and the host pool widens it
+// into `out` while later pieces copy.
+void enumerate_wire(ws_ctx* c, uint64_t nseg, uint64_t nch, const std::vector<uint64_t>& lo,
+                    const std::vector<uint64_t>& hi, const std::vector<uint64_t>& boff,
+                    uint64_t* out, uint64_t cap, ws_checks* chk) {
+  const uint64_t bps = c->S / wsk::kWireBlockSlots;
+  c->wire.reserve(boff[nch] + 64, "wire entries");
   c->wblk.reserve(nseg * bps, "wire block counts");
-  uint32_t* pb = static_cast<uint32_t*>(c->pin_wblk.reserve(nseg * bps * 4 + 64, "pinned wire"));
-  wsk::JobAcc* hacc = static_cast<wsk::JobAcc*>(
-      c->pin_out.reserve(nch * sizeof(wsk::JobAcc) + 16, "pinned out"));
+  c->per_seg.reserve(nseg, "per-segment counts");
+  uint8_t* pb = static_cast<uint8_t*>(c->pin_wblk.reserve(nseg * bps + 64, "pinned wire"));
+  const size_t acc_bytes = (nch * sizeof(wsk::JobAcc) + 63) / 64 * 64;
+  char* hout = static_cast<char*>(c->pin_out.reserve(acc_bytes + nseg * 4 + 64, "pinned out"));
+  wsk::JobAcc* hacc = reinterpret_cast<wsk::JobAcc*>(hout);
+  uint32_t* hseg = reinterpret_cast<uint32_t*>(hout + acc_bytes);  // per-segment totals
   std::vector<uint64_t> seg0(nch + 1), k0(nch);
   for (uint64_t k = 0; k <= nch; ++k) seg0[k] = k * nseg / nch;
+  // blocks past a clipped last segment are never written
+  ck(cudaMemsetAsync(c->wblk.ptr, 0, nseg * bps, c->stream), "zero wire counts");
   for (uint64_t k = 0; k < nch; ++k) {
     const wsk::Job J = make_job(lo[k], hi[k], c->S, 0);
     k0[k] = J.K0;
     c->h_jobs.assign(1, J);
-    wa.entries = c->wire.ptr + boff[k];
-    wa.blk = c->wblk.ptr + seg0[k] * bps;
-    run_sieve(c, wsk::kEnumWire, nullptr, nullptr, boff[k + 1] - boff[k], true,
+    WireArgs wa{c->wire.ptr + boff[k], c->wblk.ptr + seg0[k] * bps};
+    run_sieve(c, wsk::kEnumWire, c->per_seg.ptr + seg0[k], nullptr, boff[k + 1] - boff[k], true,
               static_cast<uint32_t>(k), k == 0, &wa);
-    // accumulators straight into mapped pinned memory: no copy-engine entry
-    // on the compute stream to queue behind earlier chunks' payload copies
+    // accumulators and segment totals straight into mapped pinned memory: no
+    // copy-engine entry on the compute stream to queue behind earlier
+    // chunks' payload copies
+    const uint32_t ns = static_cast<uint32_t>(seg0[k + 1] - seg0[k]);
     ck(wsk::launch_acc_to_host(c->acc.ptr + k, hacc + k, 1, c->stream), "chunk acc");
-    c->timing.launches += 1;
-    c->timing.d2h_bytes += sizeof(wsk::JobAcc);
+    ck(wsk::launch_u32_to_host(c->per_seg.ptr + seg0[k], hseg + seg0[k], ns, c->stream),
+       "chunk totals");
+    c->timing.launches += 2;
+    c->timing.d2h_bytes += sizeof(wsk::JobAcc) + 4ull * ns;
     ck(cudaEventRecord(c->chunk_done[k], c->stream), "event");
   }
   if (!c->pool) c->pool = wswire::pool_create(0);
   // Payload pieces of `piece` entries cross into a ring of `ring` pinned
   // slots, each expanded as soon as it lands and reused once expanded: a
-  // small reused staging set (64 MB by default) instead of one 0.9 GB
-  // buffer leaves more of the host's memory bandwidth to the 8-byte output
-  // (measured c2: 33.3 ms vs 35.7 ms per call; 1M x 8: 35.3, 256K x 8: 44).
+  // small reused staging set instead of one buffer of the whole payload
+  // leaves more of the host's memory bandwidth to the 8-byte output.
   const uint64_t piece = c->wire_piece, ring = c->wire_ring;
-  uint16_t* slots = static_cast<uint16_t*>(
-      c->pin_wire.reserve(piece * ring * sizeof(uint16_t) + 64, "pinned wire ring"));
+  uint8_t* slots = static_cast<uint8_t*>(c->pin_wire.reserve(piece * ring + 64, "pinned wire ring"));
   while (c->ring_ev.size() < ring) {
     cudaEvent_t e;
     ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -667,6 +668,8 @@ void enumerate_wire(ws_ctx* c, uint64_t L, uint64_t R, uint64_t nseg, uint64_t n
   }
   std::vector<wswire::Ticket> tickets(ring);
   std::vector<uint64_t> opos(nch, 0), take(nch, 0);
+  std::vector<std::vector<uint64_t>> seg_off(nch);
+  std::vector<wswire::WireChunk> chunks(nch);
   struct Piece {
     uint64_t k, a, m, slot;
   };
@@ -680,6 +683,11 @@ void enumerate_wire(ws_ctx* c, uint64_t L, uint64_t R, uint64_t nseg, uint64_t n
         ck(cudaEventSynchronize(c->chunk_done[kc]), "chunk");
         const uint64_t n = hacc[kc].count;
         if (n > boff[kc + 1] - boff[kc]) throw Fail{WS_CUDA, "wire chunk exceeds its bound"};
+        const uint64_t ns = seg0[kc + 1] - seg0[kc];
+        seg_off[kc].assign(ns + 1, 0);
+        for (uint64_t s = 0; s < ns; ++s) seg_off[kc][s + 1] = seg_off[kc][s] + hseg[seg0[kc] + s];
+        if (seg_off[kc][ns] != n) throw Fail{WS_CUDA, "wire segment totals disagree"};
+        chunks[kc] = wswire::WireChunk{pb + seg0[kc] * bps, seg_off[kc].data(), ns, bps, k0[kc]};
         take[kc] = pos < cap ? std::min(n, cap - pos) : 0;
         opos[kc] = pos;
         pos += n;
@@ -688,9 +696,8 @@ void enumerate_wire(ws_ctx* c, uint64_t L, uint64_t R, uint64_t nseg, uint64_t n
         chk->xor_ ^= hacc[kc].xr;
         chk->largest = std::max<uint64_t>(chk->largest, hacc[kc].largest);
         if (take[kc])
-          ck(copy_async(c, pb + seg0[kc] * bps, c->wblk.ptr + seg0[kc] * bps,
-                        (seg0[kc + 1] - seg0[kc]) * bps * 4, cudaMemcpyDeviceToHost, c->cstream),
-             "wire d2h");
+          ck(copy_async(c, pb + seg0[kc] * bps, c->wblk.ptr + seg0[kc] * bps, ns * bps,
+                        cudaMemcpyDeviceToHost, c->cstream), "wire d2h");
         started = true;
         ac = 0;
       }
@@ -698,7 +705,7 @@ void enumerate_wire(ws_ctx* c, uint64_t L, uint64_t R, uint64_t nseg, uint64_t n
         const uint64_t slot = issued.size() % ring;
         if (issued.size() >= ring) wswire::ticket_wait(c->pool, &tickets[slot]);  // slot free
         const uint64_t m = std::min(piece, take[kc] - ac);
-        ck(copy_async(c, slots + slot * piece, c->wire.ptr + boff[kc] + ac, m * sizeof(uint16_t),
+        ck(copy_async(c, slots + slot * piece, c->wire.ptr + boff[kc] + ac, m,
                       cudaMemcpyDeviceToHost, c->cstream), "wire d2h");
         ck(cudaEventRecord(c->ring_ev[slot], c->cstream), "event");
         issued.push_back(Piece{kc, ac, m, slot});
@@ -716,10 +723,8 @@ void enumerate_wire(ws_ctx* c, uint64_t L, uint64_t R, uint64_t nseg, uint64_t n
     for (size_t j = 0; j < issued.size(); ++j) {
       const Piece pc = issued[j];
       ck(cudaEventSynchronize(c->ring_ev[pc.slot]), "wire d2h");
-      // the piece holds entries [a, a + m) of chunk k; the expander finds
-      // entry a's block through the chunk's block counts
-      wswire::submit_expand(c->pool, slots + pc.slot * piece, pb + seg0[pc.k] * bps,
-                            (seg0[pc.k + 1] - seg0[pc.k]) * bps, k0[pc.k], bslots, pc.a, pc.m,
+      // the piece holds entries [a, a + m) of chunk k
+      wswire::submit_expand(c->pool, chunks[pc.k], slots + pc.slot * piece, pc.a, pc.m,
                             out + opos[pc.k] + pc.a, &tickets[pc.slot]);
       issue_next();  // into the slot of piece j + 1 - ring (waits for its expansion)
     }
@@ -748,7 +753,7 @@ void enumerate_to_host(ws_ctx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_
   }
   // large outputs (several chunks) cross PCIe in the wire format
   if (c->host_wire && nch > 1)
-    return enumerate_wire(c, L, R, nseg, nch, lo, hi, boff, out, cap, chk);
+    return enumerate_wire(c, nseg, nch, lo, hi, boff, out, cap, chk);
   c->vals.reserve(std::max<uint64_t>(boff[nch], 1), "enumeration buffer");
   wsk::JobAcc* hacc = static_cast<wsk::JobAcc*>(
       c->pin_out.reserve(nch * sizeof(wsk::JobAcc) + 16, "pinned out"));

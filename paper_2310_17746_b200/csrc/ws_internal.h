@@ -27,13 +27,15 @@ struct JobAcc {
   unsigned long long count, sum, xr, largest;
 };
 
-// kEnumWire: ordered enumeration into the 16-bit host wire format -- each
+// kEnumWire: ordered enumeration into the 8-bit host wire format -- each
 // prime as its bit position e in the interleaved survivor masks of its
-// 2^15-slot block (value = 6 * block_first_slot + 3e + 1 + (e & 1)), plus a
-// survivor count per block; the host expands it (ws_wire.cpp).
+// 128-slot (4-word) block (value = 6 * block_first_slot + 3e + 1 + (e & 1)),
+// one survivor-count byte per block (a block spans 768 integers, far fewer
+// than 255 primes) and the per-segment totals; the host widens it
+// (ws_wire.cpp).
 enum Mode : int { kCount = 0, kCountChecks = 1, kEnumerate = 2, kEnumWire = 3 };
 constexpr int kNumModes = 4;
-constexpr uint32_t kWireBlockSlots = 1u << 15;
+constexpr uint32_t kWireBlockSlots = 128;
 
 // Large-prime buckets: per window of segments, the hits of every prime
 // p >= S (at most one per class per segment) are scattered into per-segment
@@ -74,9 +76,8 @@ struct SieveParams {
   unsigned long long* status;        // enumeration look-back words (zeroed)
   unsigned long long* out;           // enumeration output (after 2 and 3)
   unsigned long long out_cap;
-  uint16_t* out16;                   // kEnumWire: entries (same positions as `out`)
-  uint32_t* blk;                     // kEnumWire: survivors per block, segment s at s * bps
-  uint32_t blk_log2w;                // kEnumWire: log2(32-slot words per block)
+  uint8_t* out8;                     // kEnumWire: entries (same positions as `out`)
+  uint8_t* blk8;                     // kEnumWire: survivors per block, segment s at s * S / 128
   uint32_t* words1;                  // nullable (count modes): survivor flag words of
   uint32_t* words5;                  // each class, segment s at word s * S / 32
 };
@@ -88,6 +89,9 @@ void build_small_tables(uint32_t* out);  // host
 cudaError_t sieve_configure(int* blocks_per_sm);
 cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st);
 cudaError_t launch_acc_to_host(const JobAcc* acc, JobAcc* host_mapped, uint32_t n,
+                               cudaStream_t st);
+// n words to mapped pinned host memory with plain stores (see acc_to_host_kernel)
+cudaError_t launch_u32_to_host(const uint32_t* src, uint32_t* host_mapped, uint32_t n,
                                cudaStream_t st);
 
 struct FillParams {

@@ -530,7 +530,6 @@ __global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_ke
   __shared__ uint32_t wc_ctr;
   __shared__ unsigned long long seg_base;
   __shared__ uint32_t seg_total;
-  __shared__ uint32_t blk_cnt[kWarps];  // kEnumWire: survivors per block (<= 8 blocks)
   constexpr bool kWire = MODE == kEnumWire;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 
@@ -542,7 +541,6 @@ __global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_ke
       fetch_segment(P, si);
       wc_ctr = 0;
     }
-    if (kWire && threadIdx.x < kWarps) blk_cnt[threadIdx.x] = 0;
     __syncthreads();
     if (si.s == ~0ull) break;
     init_words(si, tab, bm1, bm5);
@@ -669,6 +667,12 @@ __global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_ke
         const uint32_t incl = warp_incl_scan(c, lane);
         const uint32_t rtotal = __shfl_sync(kFull, incl, 31);
         const unsigned long long rbase = vbase + 192ull * w0;  // value base of the round
+        if (kWire) {  // survivors per 4-word wire block (lanes 4k .. 4k+3), one byte each
+          uint32_t bc = c + __shfl_down_sync(kFull, c, 1, 4);
+          bc += __shfl_down_sync(kFull, bc, 2, 4);
+          if ((lane & 3u) == 0 && w < w_end)
+            P.blk8[si.s * (P.S / 128) + (w >> 2)] = static_cast<uint8_t>(bc);
+        }
         if (rtotal == 0) continue;
         if (rtotal <= kStage) {
           // 1) each lane drops its survivor positions (64*lane + bit) into the stage
@@ -683,18 +687,15 @@ __global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_ke
           unsigned long long* dst = P.out + pos;
           uint32_t soff = 0, n = 0;
           if (kWire) {
-            // entry = bit position in the block's interleaved masks; rounds
-            // never straddle a block (32-word aligned, blocks of 1024 words
-            // or one whole segment)
-            uint16_t* dst16 = P.out16 + pos;
-            const uint32_t eofs = (w0 & ((1u << P.blk_log2w) - 1u)) << 6;
-            if (lane == 0) atomicAdd(&blk_cnt[w0 >> P.blk_log2w], rtotal);
+            // entry = the survivor's bit position in its 4-word block's
+            // interleaved masks: the low byte of 64 * lane + bit
+            uint8_t* dst8 = P.out8 + pos;
 #pragma unroll 4
             for (uint32_t i = lane; i < rtotal; i += 32) {
               const uint32_t e = stage[i];
               const uint32_t bb = e & 63u;
               const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
-              if (seg_fits || pos + i < P.out_cap) dst16[i] = static_cast<uint16_t>(eofs + e);
+              if (seg_fits || pos + i < P.out_cap) dst8[i] = static_cast<uint8_t>(e);
               soff += off;
               ++n;
               xr ^= rbase + off;
@@ -730,15 +731,13 @@ __global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_ke
           __syncwarp();
         } else {
           unsigned long long o = pos + (incl - c);
-          if (kWire && lane == 0) atomicAdd(&blk_cnt[w0 >> P.blk_log2w], rtotal);
           for (int half = 0; half < 2; ++half)
             for (uint32_t x = half ? hi : lo; x; x &= x - 1) {
               const uint32_t bb = (__ffs(x) - 1) + 32u * half;
               const unsigned long long v = rbase + (192u * lane + 3u * bb + 1u + (bb & 1u));
               if (o < P.out_cap) {
                 if (kWire)
-                  P.out16[o] = static_cast<uint16_t>(
-                      (((w0 & ((1u << P.blk_log2w) - 1u)) + lane) << 6) | bb);
+                  P.out8[o] = static_cast<uint8_t>(((lane & 3u) << 6) | bb);
                 else
                   P.out[o] = v;
               }
@@ -760,10 +759,6 @@ __global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_ke
         red_c[warp] = lg;
       }
       __syncthreads();
-      if (kWire && warp == 1) {
-        const uint32_t bps = max(1u, (P.S / 32) >> P.blk_log2w);
-        if (lane < bps) P.blk[si.s * bps + lane] = blk_cnt[lane];
-      }
       if (warp == 0) {
         unsigned long long su = lane < kWarps ? red_a[lane] : 0ull;
         unsigned long long x = lane < kWarps ? red_b[lane] : 0ull;
@@ -985,6 +980,18 @@ __global__ void acc_to_host_kernel(const JobAcc* a, JobAcc* host, uint32_t n) {
 cudaError_t launch_acc_to_host(const JobAcc* acc, JobAcc* host_mapped, uint32_t n,
                                cudaStream_t st) {
   acc_to_host_kernel<<<1, 32, 0, st>>>(acc, host_mapped, n);
+  return cudaGetLastError();
+}
+
+__global__ void u32_to_host_kernel(const uint32_t* src, uint32_t* host, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    host[i] = src[i];
+}
+
+cudaError_t launch_u32_to_host(const uint32_t* src, uint32_t* host_mapped, uint32_t n,
+                               cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  u32_to_host_kernel<<<(n + 255) / 256 < 64 ? (n + 255) / 256 : 64, 256, 0, st>>>(src, host_mapped, n);
   return cudaGetLastError();
 }
 

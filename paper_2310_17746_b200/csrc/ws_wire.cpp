@@ -1,19 +1,19 @@
-// Host side of the 16-bit wire format (kEnumWire, ws_internal.h).
+// Host side of the 8-bit wire format (kEnumWire, ws_internal.h).
 //
-// For host-bound enumeration the PCIe link, not the sieve, is the bound: the
-// primes below 1e10 are 3.64 GB as uint64 (65 ms at the measured 56 GB/s
-// D2H) against 2.5 ms of sieving.  The kernel therefore ships every prime
-// as the 16-bit bit position e of its 2^15-slot block plus one survivor
-// count per block (4x fewer bytes), and the host expands
+// For host-bound enumeration the PCIe link and the host's memory, not the
+// sieve, are the bound: the primes below 1e10 are 3.64 GB as uint64 (65 ms at
+// the measured 56 GB/s D2H) against 2.5 ms of sieving.  The kernel therefore
+// ships every prime as one byte -- its bit position e in the interleaved
+// survivor masks of its 128-slot block -- plus one count byte per block and
+// the per-segment totals (0.47 GB at c2), and the host widens
 //     value = 6 * block_first_slot + 3e + 1 + (e & 1)
-// straight into the caller's buffer.  The expansion is a streaming write
-// (3.64 GB at ~190 GB/s with non-temporal AVX-512 stores on the GPU box's
-// host, vs ~80 GB/s for ordinary stores), split over a small persistent
-// thread pool and overlapped chunk by chunk with the D2H of later chunks.
+// straight into the caller's buffer with non-temporal AVX-512 stores (IFMA
+// where present), split over a small persistent thread pool and overlapped
+// piece by piece with the D2H of later pieces.
 //
-// The order, count and checksums are fixed on the device; the host only
-// widens each entry.  Built with g++ (AVX-512 through target attributes and
-// a runtime CPU check; a scalar path otherwise).
+// Order, count and checksums are fixed on the device; the host only widens
+// entries.  Built with g++ (AVX-512 through target attributes and a runtime
+// CPU check; a scalar path otherwise).
 #include "ws_wire.h"
 
 #include <immintrin.h>
@@ -102,14 +102,23 @@ unsigned default_threads() {
   return std::max(1u, std::min(h ? h : 4u, 64u));
 }
 
+// Locates entry `skip`: its block b and its offset inside that block.
+void locate(const WireChunk& ch, uint64_t skip, uint64_t& b, uint64_t& off) {
+  const uint64_t s = static_cast<uint64_t>(
+      std::upper_bound(ch.seg_off, ch.seg_off + ch.nseg + 1, skip) - ch.seg_off - 1);
+  off = skip - ch.seg_off[s];
+  b = s * ch.bps;
+  while (off >= ch.cnt[b]) off -= ch.cnt[b++];
+}
+
 // ---- scalar expansion ------------------------------------------------------
-void expand_scalar(const uint16_t* e, const uint32_t* cnt, uint64_t nblk, uint64_t slot0,
-                   uint64_t bslots, uint64_t skip, uint64_t n, uint64_t* out) {
-  uint64_t b = 0, off = skip, done = 0;  // entry `skip` is entry `off` of block b
-  while (b < nblk && off >= cnt[b]) off -= cnt[b], ++b;
-  for (; b < nblk && done < n; ++b) {
-    const uint64_t base1 = 6 * (slot0 + b * bslots) + 1;
-    const uint64_t m = std::min<uint64_t>(cnt[b] - off, n - done);
+void expand_scalar(const WireChunk& ch, const uint8_t* e, uint64_t skip, uint64_t n,
+                   uint64_t* out) {
+  uint64_t b, off, done = 0;
+  locate(ch, skip, b, off);
+  for (; done < n; ++b) {
+    const uint64_t base1 = 6 * (ch.slot0 + b * kBlockSlots) + 1;
+    const uint64_t m = std::min<uint64_t>(ch.cnt[b] - off, n - done);
     for (uint64_t i = 0; i < m; ++i) {
       const uint64_t x = e[done + i];
       out[done + i] = base1 + 3 * x + (x & 1);
@@ -140,11 +149,10 @@ const LaneTables kLanes;
 
 template <bool IFMA>
 __attribute__((target("avx512f,avx512bw,avx512vl,avx512ifma"))) void expand_avx512(
-    const uint16_t* e, const uint32_t* cnt, uint64_t nblk, uint64_t slot0, uint64_t bslots,
-    uint64_t skip, uint64_t n, uint64_t* out) {
+    const WireChunk& ch, const uint8_t* e, uint64_t skip, uint64_t n, uint64_t* out) {
   if (n == 0) return;
-  uint64_t b = 0, off = skip;  // entry `skip` is entry `off` of block b
-  while (b < nblk && off >= cnt[b]) off -= cnt[b], ++b;
+  uint64_t b, off;
+  locate(ch, skip, b, off);
   uint64_t* line = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(out) & ~uintptr_t{63});
   const uint32_t head = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(out) >> 3) & 7u);
   uint32_t na = head;  // carry lanes in use (the head lanes are not ours)
@@ -152,15 +160,16 @@ __attribute__((target("avx512f,avx512bw,avx512vl,avx512ifma"))) void expand_avx5
   __m512i carry = _mm512_setzero_si512();
   const __m512i one = _mm512_set1_epi64(1), three = _mm512_set1_epi64(3);
   uint64_t left = n;
-  for (; b < nblk && left; ++b) {
-    const uint64_t m = std::min<uint64_t>(cnt[b] - off, left);
-    const uint16_t* p = e;
-    const __m512i base1 = _mm512_set1_epi64(static_cast<long long>(6 * (slot0 + b * bslots) + 1));
+  for (; left; ++b) {
+    const uint64_t m = std::min<uint64_t>(ch.cnt[b] - off, left);
+    const uint8_t* p = e;
+    const __m512i base1 =
+        _mm512_set1_epi64(static_cast<long long>(6 * (ch.slot0 + b * kBlockSlots) + 1));
     for (uint64_t i = 0; i < m; i += 8) {
       const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(8, m - i));
-      const __m128i raw = k == 8 ? _mm_loadu_si128(reinterpret_cast<const __m128i*>(p + i))
-                                 : _mm_maskz_loadu_epi16(static_cast<__mmask8>((1u << k) - 1), p + i);
-      const __m512i x = _mm512_cvtepu16_epi64(raw);
+      const __m128i raw = k == 8 ? _mm_loadl_epi64(reinterpret_cast<const __m128i*>(p + i))
+                                 : _mm_maskz_loadu_epi8(static_cast<__mmask16>((1u << k) - 1), p + i);
+      const __m512i x = _mm512_cvtepu8_epi64(raw);
       __m512i v;
       if constexpr (IFMA)
         v = _mm512_madd52lo_epu64(_mm512_add_epi64(_mm512_and_si512(x, one), base1), x, three);
@@ -217,27 +226,27 @@ unsigned pool_size(const Pool* p) { return static_cast<unsigned>(p->threads.size
 void pool_wait(Pool* p) { p->wait(); }
 void ticket_wait(Pool* p, Ticket* t) { p->wait(t); }
 
-void expand_range(const uint16_t* e, const uint32_t* cnt, uint64_t nblk, uint64_t slot0,
-                  uint64_t bslots, uint64_t skip, uint64_t n, uint64_t* out) {
+void expand_range(const WireChunk& ch, const uint8_t* e, uint64_t skip, uint64_t n,
+                  uint64_t* out) {
+  if (n == 0) return;
   switch (isa_level()) {
-    case 2: expand_avx512<true>(e, cnt, nblk, slot0, bslots, skip, n, out); break;
-    case 1: expand_avx512<false>(e, cnt, nblk, slot0, bslots, skip, n, out); break;
-    default: expand_scalar(e, cnt, nblk, slot0, bslots, skip, n, out); break;
+    case 2: expand_avx512<true>(ch, e, skip, n, out); break;
+    case 1: expand_avx512<false>(ch, e, skip, n, out); break;
+    default: expand_scalar(ch, e, skip, n, out); break;
   }
 }
 
-void submit_expand(Pool* pool, const uint16_t* e, const uint32_t* cnt, uint64_t nblk,
-                   uint64_t slot0, uint64_t bslots, uint64_t skip, uint64_t n, uint64_t* out,
-                   Ticket* t) {
+void submit_expand(Pool* pool, const WireChunk& ch, const uint8_t* e, uint64_t skip, uint64_t n,
+                   uint64_t* out, Ticket* t) {
   if (n == 0) return;
-  // equal shares of the values; each task skips to its first entry through
-  // the block counts (a prefix walk over <= a few thousand counts)
+  // equal shares of the values; each task finds its first entry through the
+  // segment offsets and at most one segment's block counts
   const uint64_t per = std::max<uint64_t>(uint64_t{1} << 16, n / (2 * pool_size(pool)) + 1);
   std::vector<std::function<void()>> fs;
   for (uint64_t a = 0; a < n; a += per) {
     const uint64_t m = std::min(per, n - a);
     fs.emplace_back([=] {
-      expand_range(e + a, cnt, nblk, slot0, bslots, skip + a, m, out + a);
+      expand_range(ch, e + a, skip + a, m, out + a);
       if (t) t->left.fetch_sub(1, std::memory_order_release);
     });
   }

@@ -1,9 +1,10 @@
-"""Host-bound enumeration through the 16-bit wire format (kEnumWire +
+"""Host-bound enumeration through the 8-bit wire format (kEnumWire +
 csrc/ws_wire.cpp): every multi-chunk host enumeration takes this path, so its
 VALUES (not only the device-side checksums) are checked here -- against the
-oracle on multi-chunk windows for wire blocks of one segment (S = 2^12),
-two per segment (2^16) and eight (2^18), against the reference goldens on
-[0, 1e10), under a truncating capacity, and against the uint64 D2H path."""
+oracle on multi-chunk windows at segment sizes 2^12, 2^16 and 2^18 (32, 512
+and 2048 128-slot wire blocks per segment; clipped last segments), against
+the reference goldens on [0, 1e10), under a truncating capacity, and against
+the uint64 D2H path."""
 import os
 
 import numpy as np
@@ -21,9 +22,9 @@ def _host_checks(v):
 
 
 @pytest.mark.parametrize("slots,L,W", [
-    (1 << 12, 10**12 - 7, 3 * 10**7),        # 1221 segments, one block each
-    (1 << 16, 2**40 + 1, 2 * 10**8),         # two blocks per segment
-    (1 << 18, 10**15, 4 * 10**8),            # 255 segments, eight blocks each
+    (1 << 12, 10**12 - 7, 3 * 10**7),        # 1221 segments
+    (1 << 16, 2**40 + 1, 2 * 10**8),
+    (1 << 18, 10**15, 4 * 10**8),            # 255 segments
     (1 << 18, 0, 3 * 10**8 + 1),             # dense start (2, 3 prelude + wire)
 ])
 def test_multichunk_windows_vs_oracle(port, slots, L, W):

@@ -1,6 +1,6 @@
-"""Host expander of the 16-bit enumeration wire format (csrc/ws_wire.cpp) on
+"""Host expander of the 8-bit enumeration wire format (csrc/ws_wire.cpp) on
 CPU: random block layouts, output alignments and partial ranges, AVX-512 and
-scalar paths (the GPU side is covered by the enumeration parity tests, which
+AVX-512 without IFMA and scalar paths (the GPU side is covered by the enumeration parity tests, which
 take the wire path for every multi-chunk host enumeration)."""
 import os
 import subprocess
@@ -20,8 +20,9 @@ def exe(tmp_path_factory):
     return out
 
 
-@pytest.mark.parametrize("scalar", ["0", "1"])
-def test_wire_expand(exe, scalar):
-    env = dict(os.environ, WHEELSIEVE_HOST_SCALAR=scalar)
+@pytest.mark.parametrize("isa", ["ifma", "avx512", "scalar"])
+def test_wire_expand(exe, isa):
+    env = dict(os.environ, WHEELSIEVE_HOST_SCALAR=str(int(isa == "scalar")),
+               WHEELSIEVE_HOST_NO_IFMA=str(int(isa == "avx512")))
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr
