@@ -111,3 +111,26 @@ def test_abi_error_paths(sieve, tmp_path):
     t = sieve.timing()
     assert t.total_ms >= 0
     assert (lib.ws_last_error(sieve._h) or b"") == b""
+
+
+def test_context_lifecycle_releases_device_memory():
+    """Every path's scratch (wire ring, bucket windows, interval jobs, segment
+    export) is released by ws_ctx_destroy: device memory returns to baseline
+    over repeated create / use / destroy cycles."""
+    import torch
+
+    def cycle():
+        with ws.Sieve() as s:
+            v, n, _ = s.enumerate_range(10**12, 10**12 + 3 * 10**8)  # wire path
+            assert n == v.size > 0
+            s.count_range(10**15, 10**15 + 2 * 10**9, checks=True)  # bucket windows
+            s.count_intervals(np.arange(5, dtype=np.uint64) * 2**30 + 2**40, 2**20)
+            s.sieve_segment(6 * 10**9, 4096)
+        torch.cuda.synchronize()
+
+    cycle()  # first use: CUDA context, module load
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(4):
+        cycle()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20, (free0, free1)
