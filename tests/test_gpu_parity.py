@@ -305,3 +305,25 @@ def test_config4_full_window_reference_golden(sieve):
         c = sieve.count_range(big["L"], big["R"], checks=True, fresh_base=fresh)
         assert (c.count, c.sum, c.xor, c.largest) == (big["count"], big["sum"], big["xor"],
                                                       big["largest"])
+
+
+def test_config4_full_window_enumeration():
+    """Config 4 "count and enumerate": all 2,895,317,534 primes of
+    [1e15, 1e15 + 1e11) enumerated into HBM (23.2 GB), ascending, with the
+    reference's count / sum / xor / largest."""
+    import torch
+
+    import paper_2310_17746_b200 as ws
+    r = load_golden("reference_big.json")["c4"]
+    L, R = 10**15, 10**15 + 10**11
+    s = ws.Sieve()
+    out = torch.empty(r["count"] + 64, dtype=torch.int64, device="cuda")
+    _, n, c = s.enumerate_range(L, R, out=out)
+    assert (n, c.sum, c.xor, c.largest) == (r["count"], r["sum"], r["xor"], r["largest"])
+    v = out[:n]
+    assert bool((v[1:] > v[:-1]).all())
+    assert int(v[0]) > L and int(v[-1]) == r["largest"]
+    # the array itself carries the checksums (int64 wrap = mod 2^64)
+    assert int(v.sum()) % 2**64 == r["sum"]
+    s.close()
+    del out
