@@ -327,3 +327,11 @@ def test_config4_full_window_enumeration():
     assert int(v.sum()) % 2**64 == r["sum"]
     s.close()
     del out
+
+
+@pytest.mark.parametrize("N,pi", [(2**32, 203_280_221), (2**40, 41_203_088_796),
+                                  (10**13, 346_065_536_839), (10**14, 3_204_941_750_802)])
+def test_published_prime_counts(sieve, N, pi):
+    """Beyond the reference goldens (which stop at 1e12): standard published
+    values of pi(x) (e.g. OEIS A006880 / A007053), up to 1e14."""
+    assert sieve.count_range(0, N + 1).count == pi
