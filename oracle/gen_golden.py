@@ -4,6 +4,7 @@ UNMODIFIED reference library (oracle/_ref/libwsref.so, built from
 
     python oracle/gen_golden.py            # quick goldens (~1-2 min on 8 cores)
     python oracle/gen_golden.py --big      # + pi(1e11), pi(1e12), full C4 window (~15 min)
+    python oracle/gen_golden.py --scale    # only: c2 weak-scaling prefixes [0, N*1e10), N=2,4,8
 
 Every record carries `source: "reference"` and the reference entry point used
 (`run` = engine.cpp:344, `range` = the SURVEY §3.3 composition of
@@ -54,12 +55,26 @@ PREFIXES = [2, 3, 4, 5, 29, 30, 96, 100, 1000, 5999, 10_000, 99_991, 100_000, 12
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--scale", action="store_true")
     ap.add_argument("--threads", type=int, default=0)
     a = ap.parse_args()
     ref = Reference()
     T = a.threads or ref.hw_threads()
     os.makedirs(GOLDEN, exist_ok=True)
     t0 = time.time()
+    if a.scale:  # bench.py --gpus N on c2 (weak): rank r enumerates [r*1e10, (r+1)*1e10)
+        recs = []
+        for n in (2, 4, 8):
+            t = time.time()
+            r = ref.run_checks(n * 10**10 - 1, T)
+            recs.append(dict(gpus=n, limit=n * 10**10 - 1, count=r["count"], sum=r["sum"],
+                             xor=r["xor"], largest=r["largest"], wall_s=time.time() - t))
+            print("scale", n, time.time() - t, flush=True)
+        meta = dict(source="reference", entry="run() with a sum/xor PrimeSink", threads=T,
+                    generator="oracle/gen_golden.py --scale")
+        with open(os.path.join(GOLDEN, "reference_scale.json"), "w") as f:
+            json.dump(dict(meta=meta, c2_weak=recs), f, indent=1)
+        return
 
     # 1. prefixes through run() (count + sum + xor + largest)
     prefixes = []

@@ -139,3 +139,14 @@ def test_port_matches_reference_random_windows(port):
         assert (a["count"], a["sum"], a["xor"], a["largest"]) == (
             b["count"], b["sum"], b["xor"], b["largest"])
         assert list(a["per_seg"]) == list(b["per_seg"])
+
+
+def test_scale_goldens_consistent(golden):
+    """The weak-scaling c2 goldens (reference run() over [0, N*1e10)) extend
+    the config-2 golden: counts grow, and pi(2e10) is the published value."""
+    from conftest import load_golden
+    g = load_golden("reference_scale.json")["c2_weak"]
+    c2 = [p for p in golden["prefixes"] if p["limit"] == 10**10 - 1][0]
+    counts = [c2["count"]] + [r["count"] for r in sorted(g, key=lambda r: r["gpus"])]
+    assert counts == sorted(counts) and len(set(counts)) == 4
+    assert g[0]["gpus"] == 2 and g[0]["count"] == 882_206_716
