@@ -163,7 +163,7 @@ __host__ __device__ uint32_t table_word(uint32_t idx) {
 
 __device__ __forceinline__ uint32_t tab_read(const uint32_t* t, uint32_t off) {
   const uint32_t i = off >> 5;
-  return __funnelshift_r(t[i], t[i + 1], off & 31u);
+  return __funnelshift_r(__ldg(t + i), __ldg(t + i + 1), off & 31u);
 }
 
 // ---------------------------------------------------------------------------
@@ -507,9 +507,11 @@ __device__ unsigned long long lookback(unsigned long long* status, uint64_t s,
   return prefix;
 }
 
-// Emission staging: per warp, up to kStage 16-bit survivor positions of one
-// 32-word round (bit 64*lane + b of the interleaved masks).
-constexpr uint32_t kStage = 1024;
+// Emission staging: per warp, a window of up to kStage 16-bit survivor
+// positions of one 32-word round (bit 64*lane + b of the interleaved masks).
+// 320 is the largest window that keeps 3 CTAs per SM (3 x (64 KiB bitmap +
+// 10 KiB stage + static + reserved) <= 228 KiB); a C2 round averages ~280.
+constexpr uint32_t kStage = 320;
 
 template <int MODE>
 constexpr size_t mode_smem_extra() {
@@ -518,12 +520,12 @@ constexpr size_t mode_smem_extra() {
 
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_kernel(const SieveParams P) {
+__global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bm1 = smem;
   uint32_t* bm5 = smem + P.S / 32;
-  uint32_t* tab = smem + 2 * (P.S / 32);
-  uint16_t* stage_all = reinterpret_cast<uint16_t*>(tab + kTabWords);
+  const uint32_t* tab = P.small_tab;  // 4.4 KB, L1-resident
+  uint16_t* stage_all = reinterpret_cast<uint16_t*>(smem + 2 * (P.S / 32));
   __shared__ SegInfo si;
   __shared__ unsigned long long red_a[kWarps], red_b[kWarps], red_c[kWarps];
   __shared__ uint32_t red_n[kWarps];
@@ -533,7 +535,6 @@ __global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_ke
   constexpr bool kWire = MODE == kEnumWire;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 
-  for (uint32_t i = threadIdx.x; i < kTabWords; i += blockDim.x) tab[i] = __ldg(P.small_tab + i);
   const uint32_t nprimes = P.nprimes_dev ? min(P.nprimes, *P.nprimes_dev) : P.nprimes;
   for (;;) {
     __syncthreads();  // bitmap / si reuse guard
@@ -674,79 +675,81 @@ __global__ void __launch_bounds__(kThreads, MODE >= kEnumerate ? 2 : 3) sieve_ke
             P.blk8[si.s * (P.S / 128) + (w >> 2)] = static_cast<uint8_t>(bc);
         }
         if (rtotal == 0) continue;
-        if (rtotal <= kStage) {
-          // 1) each lane drops its survivor positions (64*lane + bit) into the stage
-          uint16_t* sp = stage + (incl - c);
-          const uint32_t eb = lane << 6;
+        // The round's survivors go out in windows of kStage positions: each
+        // pass, lanes drop the positions (64*lane + bit) that fall in the
+        // window into the stage, then lane i writes window entries i, i+32, ...
+        // coalesced.  Almost every round is one window; dense ones (small
+        // values) take a few.
+        const uint32_t eb = lane << 6;
 #pragma unroll 1
-          for (uint32_t x = lo; x; x &= x - 1) *sp++ = static_cast<uint16_t>(eb | (__ffs(x) - 1));
+        for (uint32_t wlo = 0; wlo < rtotal; wlo += kStage) {
+          const uint32_t wn = min(kStage, rtotal - wlo);
+          if (rtotal <= kStage) {  // one window (warp-uniform): no position test
+            uint16_t* sp = stage + (incl - c);
 #pragma unroll 1
-          for (uint32_t x = hi; x; x &= x - 1) *sp++ = static_cast<uint16_t>(eb | 31u + __ffs(x));
+            for (uint32_t x = lo; x; x &= x - 1) *sp++ = static_cast<uint16_t>(eb | (__ffs(x) - 1));
+#pragma unroll 1
+            for (uint32_t x = hi; x; x &= x - 1) *sp++ = static_cast<uint16_t>(eb | 31u + __ffs(x));
+          } else if (incl > wlo && incl - c < wlo + wn) {  // lane has entries in the window
+            uint32_t q = incl - c - wlo;  // window-relative position (wraps below 0)
+#pragma unroll 1
+            for (uint32_t x = lo; x; x &= x - 1, ++q)
+              if (q < wn) stage[q] = static_cast<uint16_t>(eb | (__ffs(x) - 1));
+#pragma unroll 1
+            for (uint32_t x = hi; x; x &= x - 1, ++q)
+              if (q < wn) stage[q] = static_cast<uint16_t>(eb | 31u + __ffs(x));
+          }
           __syncwarp();
-          // 2) coalesced: lane i writes survivors i, i+32, ... of the round
-          unsigned long long* dst = P.out + pos;
+          const unsigned long long wpos = pos + wlo;
           uint32_t soff = 0, n = 0;
           if (kWire) {
             // entry = the survivor's bit position in its 4-word block's
             // interleaved masks: the low byte of 64 * lane + bit
-            uint8_t* dst8 = P.out8 + pos;
+            uint8_t* dst8 = P.out8 + wpos;
 #pragma unroll 4
-            for (uint32_t i = lane; i < rtotal; i += 32) {
+            for (uint32_t i = lane; i < wn; i += 32) {
               const uint32_t e = stage[i];
               const uint32_t bb = e & 63u;
               const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
-              if (seg_fits || pos + i < P.out_cap) dst8[i] = static_cast<uint8_t>(e);
+              if (seg_fits || wpos + i < P.out_cap) dst8[i] = static_cast<uint8_t>(e);
               soff += off;
               ++n;
               xr ^= rbase + off;
             }
-          } else if (seg_fits) {
-#pragma unroll 4
-            for (uint32_t i = lane; i < rtotal; i += 32) {
-              const uint32_t e = stage[i];
-              const uint32_t bb = e & 63u;
-              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
-              const unsigned long long v = rbase + off;
-              dst[i] = v;
-              soff += off;
-              ++n;
-              xr ^= v;
-            }
           } else {
-            for (uint32_t i = lane; i < rtotal; i += 32) {
-              const uint32_t e = stage[i];
-              const uint32_t bb = e & 63u;
-              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
-              const unsigned long long v = rbase + off;
-              if (pos + i < P.out_cap) dst[i] = v;
-              soff += off;
-              ++n;
-              xr ^= v;
+            unsigned long long* dst = P.out + wpos;
+            if (seg_fits) {
+#pragma unroll 4
+              for (uint32_t i = lane; i < wn; i += 32) {
+                const uint32_t e = stage[i];
+                const uint32_t bb = e & 63u;
+                const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+                const unsigned long long v = rbase + off;
+                dst[i] = v;
+                soff += off;
+                ++n;
+                xr ^= v;
+              }
+            } else {
+              for (uint32_t i = lane; i < wn; i += 32) {
+                const uint32_t e = stage[i];
+                const uint32_t bb = e & 63u;
+                const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+                const unsigned long long v = rbase + off;
+                if (wpos + i < P.out_cap) dst[i] = v;
+                soff += off;
+                ++n;
+                xr ^= v;
+              }
             }
           }
           sum += rbase * n + soff;
-          const uint32_t e = stage[rtotal - 1];
-          const uint32_t bb = e & 63u;
-          lg = rbase + (192u * (e >> 6) + 3u * bb + 1u + (bb & 1u));
+          if (wlo + wn == rtotal) {  // the round's largest survivor
+            const uint32_t e = stage[wn - 1];
+            const uint32_t bb = e & 63u;
+            lg = rbase + (192u * (e >> 6) + 3u * bb + 1u + (bb & 1u));
+          }
           __syncwarp();
-        } else {
-          unsigned long long o = pos + (incl - c);
-          for (int half = 0; half < 2; ++half)
-            for (uint32_t x = half ? hi : lo; x; x &= x - 1) {
-              const uint32_t bb = (__ffs(x) - 1) + 32u * half;
-              const unsigned long long v = rbase + (192u * lane + 3u * bb + 1u + (bb & 1u));
-              if (o < P.out_cap) {
-                if (kWire)
-                  P.out8[o] = static_cast<uint8_t>(((lane & 3u) << 6) | bb);
-                else
-                  P.out[o] = v;
-              }
-              ++o;
-              sum += v;
-              xr ^= v;
-              lg = max(lg, v);
-            }
-          lg = warp_max64(lg);
         }
         pos += rtotal;
       }
@@ -926,7 +929,7 @@ void build_small_tables(uint32_t* out) {
 }
 
 size_t sieve_smem_bytes(uint32_t S, int mode) {
-  const size_t base = (2 * (S / 32) + kTabWords) * sizeof(uint32_t);
+  const size_t base = 2 * (S / 32) * sizeof(uint32_t);
   return base + (mode >= kEnumerate ? mode_smem_extra<kEnumerate>() : 0);
 }
 
