@@ -33,6 +33,10 @@ elif cfg == "c4":
 elif cfg == "c4s":  # 1/8 share of c4
     lo, hi = ws.partition(10**15, 10**15 + 10**11, 7, 8)
     f = lambda: sv.count_range(lo, hi, checks=True)
+elif cfg == "c4e":
+    out = torch.empty(ws.prime_count_bound(10**15, 10**15 + 10**11), dtype=torch.int64,
+                      device="cuda")
+    f = lambda: sv.enumerate_range(10**15, 10**15 + 10**11, out=out)[2]
 elif cfg == "c5":
     Ls = splitmix_starts(42, 4096, 2**32, 2**44)
     f = lambda: sv.count_intervals(Ls, 2**24)
