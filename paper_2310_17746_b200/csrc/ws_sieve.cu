@@ -280,6 +280,38 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
 // p is not yet active in this segment (p*p beyond its end; since primes
 // ascend, no later prime is active either).  The activation test is two
 // 32-bit compares against the segment's thresholds.
+// ks mod p with 1/p already in a register (the per-thread prime loops load
+// it together with p, one iteration ahead)
+__device__ __forceinline__ uint32_t mod_p_inv(const ModCtx& c, uint32_t p, double inv_p,
+                                              const unsigned long long* m, uint32_t i) {
+  if (c.fast) {
+    const double t = __fma_rn(c.ksd, inv_p, 6755399441055744.0);
+    const uint32_t q = static_cast<uint32_t>(__double2loint(t));
+    uint32_t r = c.kslo - q * p;
+    if (static_cast<int32_t>(r) < 0) r += p;
+    return r;
+  }
+  return mod_barrett(c.ks, p, __ldg(m + i));
+}
+
+__device__ __forceinline__ bool prime_offsets_inv(uint32_t p, double inv_p, uint32_t i,
+                                                  const unsigned long long* m, const ModCtx& mc,
+                                                  uint32_t t_lo, uint32_t t_hi, uint32_t& rel1,
+                                                  uint32_t& rel5) {
+  if (p > t_hi) return false;
+  const uint32_t t1 = target1(p), t5 = target5(p);
+  if (p > t_lo) {  // activation segment (see prime_offsets)
+    const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;
+    rel1 = static_cast<uint32_t>(ksq - mc.ks);
+    rel5 = rel1 + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
+  } else {
+    const uint32_t r = mod_p_inv(mc, p, inv_p, m, i);
+    rel1 = t1 >= r ? t1 - r : t1 + p - r;
+    rel5 = t5 >= r ? t5 - r : t5 + p - r;
+  }
+  return true;
+}
+
 __device__ __forceinline__ bool prime_offsets(uint32_t p, uint32_t i, const double* inv,
                                               const unsigned long long* m, const ModCtx& mc,
                                               uint32_t t_lo, uint32_t t_hi, uint32_t& rel1,
@@ -365,32 +397,61 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   // p < S: one thread per prime, static warp-sized chunks; both classes
   // advance together (their hits are the same stride p apart)
   const uint32_t mid_end = n_S < lp_end ? n_S : lp_end;
-  for (uint32_t base = n_wc + 32 * warp; base < mid_end; base += 32 * kWarps) {
-    if (P.prime_p[base] > t_hi) break;  // primes ascend: the rest is inactive
-    const uint32_t i = base + lane;
-    if (i >= mid_end) continue;
-    const uint32_t p = P.prime_p[i];
-    uint32_t rel1, rel5;
-    if (!prime_offsets(p, i, P.prime_inv, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) continue;
-    const int32_t d = static_cast<int32_t>(rel5 - rel1);
-    const uint32_t dpos = d > 0 ? static_cast<uint32_t>(d) : 0u;
-    uint32_t h = rel1;
-    for (; h + dpos < len; h += p) {
-      mark(a1, h);
-      mark(a5, h + d);
+  // The per-thread prime loops below load p and 1/p one iteration ahead: the
+  // loads are independent of the segment, and issuing them together and early
+  // turns two dependent global round trips per (prime, segment) into none on
+  // the critical path.
+  constexpr uint32_t kStride = 32 * kWarps;
+  auto load = [&](uint32_t idx, uint32_t end, uint32_t& p, double& ip) {
+    if (idx < end) {
+      p = __ldg(P.prime_p + idx);
+      ip = __ldg(P.prime_inv + idx);
+    } else {
+      p = 0xFFFFFFFFu;
+      ip = 0.0;
     }
-    mark_if(a1, h, len);
-    mark_if(a5, h + d, d < 0 ? len : 0u);
+  };
+  // p < S: one thread per prime, static warp-sized chunks; both classes
+  // advance together (their hits are the same stride p apart)
+  {
+    uint32_t base = n_wc + 32 * warp;
+    uint32_t pn;
+    double ipn;
+    load(base + lane, mid_end, pn, ipn);
+    for (; base < mid_end; base += kStride) {
+      const uint32_t p = pn, i = base + lane;
+      const double ip = ipn;
+      load(base + kStride + lane, mid_end, pn, ipn);
+      if (__shfl_sync(kFull, p, 0) > t_hi) break;  // primes ascend: the rest is inactive
+      uint32_t rel1, rel5;
+      if (!prime_offsets_inv(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) continue;
+      const int32_t d = static_cast<int32_t>(rel5 - rel1);
+      const uint32_t dpos = d > 0 ? static_cast<uint32_t>(d) : 0u;
+      uint32_t h = rel1;
+      for (; h + dpos < len; h += p) {
+        mark(a1, h);
+        mark(a5, h + d);
+      }
+      mark_if(a1, h, len);
+      mark_if(a5, h + d, d < 0 ? len : 0u);
+    }
   }
   // p >= S (no bucket list): at most one hit per class -- no loop, no branch
-  for (uint32_t base = mid_end + 32 * warp; base < lp_end; base += 32 * kWarps) {
-    if (__ldg(P.prime_p + base) > t_hi) break;
-    const uint32_t i = base + lane;
-    const uint32_t p = i < lp_end ? __ldg(P.prime_p + i) : 0xFFFFFFFFu;
-    uint32_t rel1 = len, rel5 = len;
-    prime_offsets(p, i, P.prime_inv, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
-    mark_if(a1, rel1, len);
-    mark_if(a5, rel5, len);
+  {
+    uint32_t base = mid_end + 32 * warp;
+    uint32_t pn;
+    double ipn;
+    load(base + lane, lp_end, pn, ipn);
+    for (; base < lp_end; base += kStride) {
+      const uint32_t p = pn, i = base + lane;
+      const double ip = ipn;
+      load(base + kStride + lane, lp_end, pn, ipn);
+      if (__shfl_sync(kFull, p, 0) > t_hi) break;
+      uint32_t rel1 = len, rel5 = len;
+      prime_offsets_inv(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
+      mark_if(a1, rel1, len);
+      mark_if(a5, rel5, len);
+    }
   }
   if (use_bucket) {
     // an entry is the bit index into [bm1 | bm5] (class at bit log2 S), so a
