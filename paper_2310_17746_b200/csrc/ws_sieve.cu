@@ -863,16 +863,28 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
   __syncthreads();
   const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
   const uint32_t p_end = F.nprimes_dev ? min(F.p_end, *F.nprimes_dev) : F.p_end;
-  // pass 1: first hits (Barrett, p*p activation) + per-segment histogram
+  // pass 1: first hits (Barrett, p*p activation) + per-segment histogram;
+  // p and 1/p are loaded one prime ahead (independent of the run)
+  uint32_t pn = 0;
+  double ipn = 0.0;
+  if (first + threadIdx.x < p_end) {
+    pn = __ldg(F.prime_p + first + threadIdx.x);
+    ipn = __ldg(F.prime_inv + first + threadIdx.x);
+  }
 #pragma unroll 1
   for (int j = 0; j < kFillPrimesPerThread; ++j) {
     const uint32_t li = j * kFillThreads + threadIdx.x;
     const uint32_t i = first + li;
     uint32_t r1 = 0xFFFFFFFFu, r5 = 0xFFFFFFFFu;
+    const uint32_t p = pn;
+    const double ip = ipn;
+    if (i + kFillThreads < p_end && j + 1 < kFillPrimesPerThread) {
+      pn = __ldg(F.prime_p + i + kFillThreads);
+      ipn = __ldg(F.prime_inv + i + kFillThreads);
+    }
     if (i < p_end) {
-      const uint32_t p = F.prime_p[i];
       uint32_t q1, q5;
-      if (prime_offsets(p, i, F.prime_inv, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
+      if (prime_offsets_inv(p, ip, i, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
         if (q1 < span) r1 = q1;
         if (q5 < span) r5 = q5;
         if (p <= 0xFFFFFFFFu - span) {  // 32-bit stepping cannot wrap
