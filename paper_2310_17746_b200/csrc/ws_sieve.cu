@@ -378,15 +378,27 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   const ModCtx mc = mod_ctx(ks);
   const uint32_t n_wc = min(P.n_wc, nprimes), n_mid = min(P.n_mid, nprimes);
   const uint32_t n_S = min(P.n_S, n_mid);
-  // warp-cooperative primes, handed out dynamically (largest work first)
-  for (;;) {
-    uint32_t i = 0;
-    if (lane == 0) i = atomicAdd(wc_ctr, 1u);
-    i = __shfl_sync(kFull, i, 0);
-    if (i >= n_wc) break;
-    const uint32_t p = P.prime_p[i];
+  // warp-cooperative primes, handed out dynamically (largest work first); the
+  // next prime is claimed and its p and 1/p loaded while the current one is
+  // marked
+  auto claim = [&](uint32_t& i, uint32_t& p, double& ip) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(wc_ctr, 1u);
+    i = __shfl_sync(kFull, k, 0);
+    if (i < n_wc) {
+      p = __ldg(P.prime_p + i);
+      ip = __ldg(P.prime_inv + i);
+    }
+  };
+  uint32_t wi, wp = 0;
+  double wip = 0.0;
+  claim(wi, wp, wip);
+  while (wi < n_wc) {
+    const uint32_t i = wi, p = wp;
+    const double ip = wip;
+    claim(wi, wp, wip);
     uint32_t rel1, rel5;
-    if (!prime_offsets(p, i, P.prime_inv, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
+    if (!prime_offsets_inv(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
     mark_strided(a1, rel1, p, len, lane);
     mark_strided(a5, rel5, p, len, lane);
   }
