@@ -332,6 +332,12 @@ __device__ __forceinline__ bool prime_offsets(uint32_t p, uint32_t i, const doub
   return true;
 }
 
+// ... if h < len, branch-free: a miss ORs 0 into the word picked by h's own
+// bits under wmask (spread over the banks, always inside the bitmap)
+__device__ __forceinline__ void mark_or(uint32_t a0, uint32_t h, uint32_t len, uint32_t wmask) {
+  atom_or_shared(a0 + (((h >> 5) & wmask) << 2), h < len ? 1u << (h & 31u) : 0u);
+}
+
 // cross off bit h of the bitmap at shared address a0
 __device__ __forceinline__ void mark(uint32_t a0, uint32_t h) {
   atom_or_shared(a0 + ((h >> 5) << 2), 1u << (h & 31u));
@@ -461,8 +467,8 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       if (__shfl_sync(kFull, p, 0) > t_hi) break;
       uint32_t rel1 = len, rel5 = len;
       prime_offsets_inv(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
-      mark_if(a1, rel1, len);
-      mark_if(a5, rel5, len);
+      mark_or(a1, rel1, len, P.S / 32 - 1);
+      mark_or(a5, rel5, len, P.S / 32 - 1);
     }
   }
   if (use_bucket) {
