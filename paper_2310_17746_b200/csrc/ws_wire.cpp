@@ -148,6 +148,19 @@ struct LaneTables {
 const LaneTables kLanes;
 
 template <bool IFMA>
+__attribute__((target("avx512f,avx512bw,avx512vl,avx512ifma"))) inline __m512i widen8(
+    __m128i raw, __m512i base1) {
+  const __m512i x = _mm512_cvtepu8_epi64(raw);
+  const __m512i one = _mm512_set1_epi64(1);
+  if constexpr (IFMA)
+    return _mm512_madd52lo_epu64(_mm512_add_epi64(_mm512_and_si512(x, one), base1), x,
+                                 _mm512_set1_epi64(3));
+  else
+    return _mm512_add_epi64(_mm512_add_epi64(_mm512_slli_epi64(x, 1), x),
+                            _mm512_add_epi64(_mm512_and_si512(x, one), base1));
+}
+
+template <bool IFMA>
 __attribute__((target("avx512f,avx512bw,avx512vl,avx512ifma"))) void expand_avx512(
     const WireChunk& ch, const uint8_t* e, uint64_t skip, uint64_t n, uint64_t* out) {
   if (n == 0) return;
@@ -155,29 +168,45 @@ __attribute__((target("avx512f,avx512bw,avx512vl,avx512ifma"))) void expand_avx5
   locate(ch, skip, b, off);
   uint64_t* line = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(out) & ~uintptr_t{63});
   const uint32_t head = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(out) >> 3) & 7u);
-  uint32_t na = head;  // carry lanes in use (the head lanes are not ours)
+  // carry: the current output line's first na values (lanes 0 .. na-1); the
+  // head lanes of the first line are not ours and are never stored
+  uint32_t na = head;
   bool first = true;
   __m512i carry = _mm512_setzero_si512();
-  const __m512i one = _mm512_set1_epi64(1), three = _mm512_set1_epi64(3);
   uint64_t left = n;
   for (; left; ++b) {
     const uint64_t m = std::min<uint64_t>(ch.cnt[b] - off, left);
-    const uint8_t* p = e;
     const __m512i base1 =
         _mm512_set1_epi64(static_cast<long long>(6 * (ch.slot0 + b * kBlockSlots) + 1));
-    for (uint64_t i = 0; i < m; i += 8) {
-      const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(8, m - i));
-      const __m128i raw = k == 8 ? _mm_loadl_epi64(reinterpret_cast<const __m128i*>(p + i))
-                                 : _mm_maskz_loadu_epi8(static_cast<__mmask16>((1u << k) - 1), p + i);
-      const __m512i x = _mm512_cvtepu8_epi64(raw);
-      __m512i v;
-      if constexpr (IFMA)
-        v = _mm512_madd52lo_epu64(_mm512_add_epi64(_mm512_and_si512(x, one), base1), x, three);
-      else
-        v = _mm512_add_epi64(_mm512_add_epi64(_mm512_slli_epi64(x, 1), x),
-                             _mm512_add_epi64(_mm512_and_si512(x, one), base1));
-      const __m512i comb = _mm512_permutex2var_epi64(
-          carry, _mm512_load_si512(kLanes.merge[na]), v);
+    uint64_t i = 0;
+    if (m >= 8) {
+      // full vectors keep na fixed: the lane maps are loaded once per block
+      const __m512i im = _mm512_load_si512(kLanes.merge[na]);
+      const __m512i ir = _mm512_load_si512(kLanes.rest[na]);
+      if (first) {  // the head line is shared with the caller's preceding data
+        const __m512i v = widen8<IFMA>(_mm_loadl_epi64(reinterpret_cast<const __m128i*>(e)), base1);
+        _mm512_mask_storeu_epi64(line, static_cast<__mmask8>(0xFFu << head),
+                                 _mm512_permutex2var_epi64(carry, im, v));
+        carry = _mm512_permutexvar_epi64(ir, v);
+        line += 8;
+        first = false;
+        i = 8;
+      }
+      for (; i + 8 <= m; i += 8) {
+        const __m512i v =
+            widen8<IFMA>(_mm_loadl_epi64(reinterpret_cast<const __m128i*>(e + i)), base1);
+        _mm512_stream_si512(reinterpret_cast<__m512i*>(line),
+                            _mm512_permutex2var_epi64(carry, im, v));
+        carry = _mm512_permutexvar_epi64(ir, v);
+        line += 8;
+      }
+    }
+    if (i < m) {  // the block's ragged tail: k < 8 values
+      const uint32_t k = static_cast<uint32_t>(m - i);
+      const __m512i v = widen8<IFMA>(
+          _mm_maskz_loadu_epi8(static_cast<__mmask16>((1u << k) - 1), e + i), base1);
+      const __m512i comb =
+          _mm512_permutex2var_epi64(carry, _mm512_load_si512(kLanes.merge[na]), v);
       if (na + k >= 8) {
         if (first)
           _mm512_mask_storeu_epi64(line, static_cast<__mmask8>(0xFFu << head), comb);
