@@ -720,12 +720,9 @@ void enumerate_wire(ws_ctx* c, uint64_t nseg, uint64_t nch, const std::vector<ui
   try {
     for (uint64_t r = 0; r + 1 < ring && issue_next(); ++r) {
     }
-    Timer TT;
-    std::vector<double> tl;
     for (size_t j = 0; j < issued.size(); ++j) {
       const Piece pc = issued[j];
       ck(cudaEventSynchronize(c->ring_ev[pc.slot]), "wire d2h");
-      tl.push_back(TT.ms());
       // the piece holds entries [a, a + m) of chunk k
       wswire::submit_expand(c->pool, chunks[pc.k], slots + pc.slot * piece, pc.a, pc.m,
                             out + opos[pc.k] + pc.a, &tickets[pc.slot]);
@@ -733,12 +730,6 @@ void enumerate_wire(ws_ctx* c, uint64_t nseg, uint64_t nch, const std::vector<ui
     }
     ck(cudaStreamSynchronize(c->stream), "sync");
     ck(cudaGetLastError(), "kernel");
-    wswire::pool_wait(c->pool);
-    tl.push_back(TT.ms());
-    if (std::getenv("WS_TL")) {
-      for (size_t q = 0; q < tl.size(); q += 8) fprintf(stderr, "%.1f ", tl[q]);
-      fprintf(stderr, "| n=%zu end %.1f\n", tl.size() - 1, tl.back());
-    }
   } catch (...) {
     wswire::pool_wait(c->pool);  // no task may outlive the call
     throw;
