@@ -3,7 +3,8 @@
 // Reference hot path (CPU, scalar): sieve_segment (segment.cpp:164-188) ->
 // FlagArray::clear_stride (segment.cpp:49-69) per base prime and residue
 // class, then count_surviving / for_each_surviving (segment.cpp:141-162,
-// segment.hpp:123-146).  Here one thread block owns one segment at a time:
+// segment.hpp:123-146).  Here one thread block owns one segment at a time
+// (persistent CTAs, 3 per SM in every mode, segments claimed from a ticket):
 //
 //   shared memory:  two uint32 bitmaps (6k+1 and 6k+5 classes), S/32 words each,
 //                   bit k of class c <-> value 6*(ks + k) + c (LSB-first, the
@@ -13,15 +14,17 @@
 //                   measured conflicts of the strided loop are lower with the
 //                   natural layout (2.4-way vs 2.8-way for p in [53, 1024)).
 //   stamp:          primes 5..47 are never looped: their combined periodic
-//                   patterns (5*7*11*13, 17*19*23, 29*31, 37*41, 43*47) live in
-//                   shared tables and each word is initialised by five
-//                   funnel-shifted table reads ANDed with the [L, R) trim mask.
+//                   patterns (5*7*11*13, 17*19*23, 29*31, 37*41, 43*47) are
+//                   read through L1 and each word is five funnel-shifted table
+//                   reads ANDed with the [L, R) trim mask.
 //   medium primes:  53 <= p < wc_limit: warp-cooperative strided clear (lane l
 //                   takes hits rel + l*p, rel + (l+32)*p, ...).
-//   other primes:   one thread per prime.
+//   other primes:   one thread per prime (p < S: hit loop; p >= S: at most one
+//                   hit per class), p and 1/p loaded one iteration ahead;
+//                   p >= 2S from bucket lists when the base table is large.
 //   offsets:        the first hit of p in each class is recomputed per
-//                   (prime, segment) from ks mod p with a 64-bit Barrett
-//                   reduction -- no 64-bit divide, no carried state, so
+//                   (prime, segment) from ks mod p by one FP64 FMA (64-bit
+//                   Barrett above 2^53) -- no divide, no carried state, so
 //                   segments can be claimed dynamically (ticket counter),
 //                   which the ordered enumeration look-back relies on.  The
 //                   reference's activation rule (first hit at p*p,
@@ -29,7 +32,8 @@
 //   finish:         __popc + warp/block reductions (count), optional
 //                   sum/xor checksums, or ordered enumeration: per-warp
 //                   prefix sums + a decoupled look-back across segments for
-//                   the global output offset, then uint64 stores.
+//                   the global output offset, then coalesced uint64 stores
+//                   (or the 8-bit host wire format, ws_wire.cpp).
 #include <cstdint>
 
 #include "ws_internal.h"
@@ -412,7 +416,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;
   const uint32_t lp_end = use_bucket ? n_mid : nprimes;
   const uint32_t warp = threadIdx.x >> 5;
-  // p < S: one thread per prime, static warp-sized chunks; both classes
+  // p < S: one thread per prime, static warp-sized chunks (round robin); both classes
   // advance together (their hits are the same stride p apart)
   const uint32_t mid_end = n_S < lp_end ? n_S : lp_end;
   // The per-thread prime loops below load p and 1/p one iteration ahead: the
@@ -429,7 +433,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       ip = 0.0;
     }
   };
-  // p < S: one thread per prime, static warp-sized chunks; both classes
+  // p < S: one thread per prime, static warp-sized chunks (round robin); both classes
   // advance together (their hits are the same stride p apart)
   {
     uint32_t base = n_wc + 32 * warp;
