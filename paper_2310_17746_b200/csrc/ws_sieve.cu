@@ -416,8 +416,6 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;
   const uint32_t lp_end = use_bucket ? n_mid : nprimes;
   const uint32_t warp = threadIdx.x >> 5;
-  // p < S: one thread per prime, static warp-sized chunks (round robin); both classes
-  // advance together (their hits are the same stride p apart)
   const uint32_t mid_end = n_S < lp_end ? n_S : lp_end;
   // The per-thread prime loops below load p and 1/p one iteration ahead: the
   // loads are independent of the segment, and issuing them together and early
@@ -433,8 +431,8 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       ip = 0.0;
     }
   };
-  // p < S: one thread per prime, static warp-sized chunks (round robin); both classes
-  // advance together (their hits are the same stride p apart)
+  // p < S: one thread per prime, static warp-sized chunks (round robin);
+  // both classes advance together (their hits are the same stride p apart)
   {
     uint32_t base = n_wc + 32 * warp;
     uint32_t pn;
