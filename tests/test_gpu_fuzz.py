@@ -134,3 +134,36 @@ def test_context_lifecycle_releases_device_memory():
         cycle()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 64 << 20, (free0, free1)
+
+
+def test_concurrent_contexts_in_threads():
+    """One context per host thread (the ABI's threading rule): four threads
+    enumerating (wire path) and counting concurrently get exactly the results
+    a single thread gets."""
+    import threading
+
+    jobs = [(10**12 + k * 10**9, 3 * 10**8) for k in range(4)]
+    want = {}
+    with ws.Sieve() as s:
+        for L, W in jobs:
+            v, n, c = s.enumerate_range(L, L + W)
+            want[L] = (n, c.sum, c.xor, int(v.sum(dtype=np.uint64)), s.count_range(L, L + W).count)
+    got, errs = {}, []
+
+    def work(L, W):
+        try:
+            with ws.Sieve() as s:
+                for _ in range(2):
+                    v, n, c = s.enumerate_range(L, L + W)
+                    cnt = s.count_range(L, L + W).count
+                got[L] = (n, c.sum, c.xor, int(v.sum(dtype=np.uint64)), cnt)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=j) for j in jobs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    assert got == want
