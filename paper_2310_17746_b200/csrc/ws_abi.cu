@@ -67,6 +67,24 @@ struct DevBuf {
     ptr = nullptr;
     cap = 0;
   }
+  // grow to n elements keeping the first `keep` (stream-ordered copy)
+  void grow(size_t n, size_t keep, cudaStream_t st, const char* what) {
+    if (n <= cap) return;
+    T* q = nullptr;
+    ck(cudaMalloc(&q, n * sizeof(T)), what);
+    if (keep && ptr) {
+      const cudaError_t e = cudaMemcpyAsync(q, ptr, std::min(keep, cap) * sizeof(T),
+                                            cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) {
+        cudaFree(q);
+        ck(e, what);
+      }
+      ck(cudaStreamSynchronize(st), what);  // the old buffer is freed next
+    }
+    release();
+    ptr = q;
+    cap = n;
+  }
 };
 
 // Growable page-locked host staging (async H2D/D2H without staging copies).
@@ -142,6 +160,8 @@ struct ws_ctx {
   PinnedArena pin_up;  // async upload staging (jobs, runs), reset per call
   PinnedBuf pin_out;   // results, read after the call's synchronisation
   DevBuf<uint32_t> d_tabn;  // exact base-table size, written on device by prepare_table
+  DevBuf<uint32_t> d_tabn_old;  // its value before an extension (append_table reads it)
+  bool base_extend = true;      // grow the table incrementally (WHEELSIEVE_BASE_EXTEND=0: rebuild)
   DevBuf<uint32_t> small_tab;  // small-prime pattern tables
 
   // resident base-prime table: every prime in [53, base_B]
@@ -215,6 +235,7 @@ struct ws_ctx {
     tab_inv.release();
     l0_inv.release();
     d_tabn.release();
+    d_tabn_old.release();
     small_tab.release();
     pin_up.release();
     pin_out.release();
@@ -481,9 +502,52 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
 // Make the resident table cover every prime in [37, B].  No host round
 // trip: the level-0 count and the table size stay on the device and the
 // kernels read them (SieveParams::nprimes_dev); the host keeps upper bounds.
+// Device-side BasePrimeStore::extend (base_store.cpp:44-69): the resident
+// table [53, base_B] already covers sqrt(B), so only (base_B, B] is sieved --
+// with that table -- and appended; the table size stays on the device.
+void extend_base(ws_ctx* c, uint64_t B) {
+  ck(cudaEventRecord(c->ev[0], c->stream), "event");
+  const uint64_t lo = c->base_B + 1;
+  const uint64_t cap = prime_count_bound(lo, B + 1);
+  const uint64_t need = static_cast<uint64_t>(c->nprimes) + cap;
+  c->tab_p.grow(need, c->nprimes, c->stream, "base table");
+  c->tab_m.grow(need, c->nprimes, c->stream, "base table");
+  c->tab_inv.grow(need, c->nprimes, c->stream, "base table");
+  c->vals.reserve(std::max<uint64_t>(cap, 1), "base values");
+  c->d_tabn_old.reserve(1, "table size");
+  // the extension's segments are small so a short range spreads over the GPU
+  const uint32_t S_main = c->S;
+  uint32_t S_ext = 1u << 12;
+  while (S_ext < S_main && ((B - lo) / 6) / S_ext > 4ull * c->sms) S_ext <<= 1;
+  c->S = S_ext;
+  c->h_jobs.assign(1, make_job(lo, B + 1, c->S, 0));
+  try {
+    run_sieve(c, wsk::kEnumerate, nullptr, c->vals.ptr, cap, false);
+  } catch (...) {
+    c->S = S_main;
+    throw;
+  }
+  c->S = S_main;
+  ck(cudaMemcpyAsync(c->d_tabn_old.ptr, c->nprimes_dev, sizeof(uint32_t),
+                     cudaMemcpyDeviceToDevice, c->stream), "table size");
+  ck(wsk::launch_append_table(c->vals.ptr, &c->acc.ptr[0].count, cap, c->tab_p.ptr, c->tab_m.ptr,
+                              c->tab_inv.ptr, c->d_tabn.ptr, c->d_tabn_old.ptr, c->stream),
+     "append table");
+  c->timing.launches += 1;
+  c->nprimes = static_cast<uint32_t>(need);
+  c->base_B = B;
+  c->base_built = true;
+  c->base_valid = true;
+  ck(cudaEventRecord(c->ev[1], c->stream), "event");
+}
+
 void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
   c->base_built = false;
   if (c->base_valid && c->base_B >= B && !fresh) return;
+  if (c->base_extend && c->base_valid && !fresh && c->nprimes_dev == c->d_tabn.ptr &&
+      c->base_B >= wsk::kFirstTablePrime && isqrt_u64(B) <= c->base_B && B <= 0xFFFFFFFFull &&
+      static_cast<uint64_t>(c->nprimes) + prime_count_bound(c->base_B + 1, B + 1) < 0xFFFFFFFFull)
+    return extend_base(c, B);
   c->base_built = true;
   ck(cudaEventRecord(c->ev[0], c->stream), "event");
   c->base_valid = false;
@@ -884,6 +948,7 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CTAS")) c->bucket_ctas_per_sm = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_CTAS_PER_SM")) c->ctas_per_sm = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_HOST_WIRE")) c->host_wire = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_BASE_EXTEND")) c->base_extend = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
     c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_RING"))

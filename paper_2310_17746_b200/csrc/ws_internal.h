@@ -114,6 +114,13 @@ constexpr int kFillPrimesPerBlock = kFillThreads * kFillPrimesPerThread;
 constexpr uint32_t kMaxWindow = 2048;  // segments per window (<= fill histogram size)
 cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st);
 
+// Appends the enumerated primes vals[0, min(*n_dev, cap)) to a table of
+// *old_n_dev entries and sets *out_n (device-side BasePrimeStore::extend).
+cudaError_t launch_append_table(const unsigned long long* vals, const unsigned long long* n_dev,
+                                uint64_t cap, uint32_t* out_p, unsigned long long* out_m,
+                                double* out_inv, uint32_t* out_n, const uint32_t* old_n_dev,
+                                cudaStream_t st);
+
 // Level-0 base primes: all primes in [37, n] (n <= 65536 + 1) in one block.
 cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
                                double* out_inv, uint32_t* out_count, cudaStream_t st);

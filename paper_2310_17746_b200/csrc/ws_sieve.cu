@@ -1091,6 +1091,36 @@ cudaError_t launch_u32_to_host(const uint32_t* src, uint32_t* host_mapped, uint3
   return cudaGetLastError();
 }
 
+// BasePrimeStore::extend (base_store.cpp:44-69) on the device: the primes
+// enumerated from (old bound, new bound] are appended to the resident table
+// after its old_n entries (old_n read from a device copy, so the update of
+// out_n cannot race with the readers).
+__global__ void append_table_kernel(const unsigned long long* vals,
+                                    const unsigned long long* n_dev, uint64_t cap,
+                                    uint32_t* out_p, unsigned long long* out_m, double* out_inv,
+                                    uint32_t* out_n, const uint32_t* old_n_dev) {
+  const uint64_t n = *n_dev < cap ? static_cast<uint64_t>(*n_dev) : cap;
+  const uint64_t base = *old_n_dev;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_n = static_cast<uint32_t>(base + n);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t p = static_cast<uint32_t>(vals[i]);
+    out_p[base + i] = p;
+    out_m[base + i] = ~0ull / p;
+    out_inv[base + i] = 1.0 / static_cast<double>(p);
+  }
+}
+
+cudaError_t launch_append_table(const unsigned long long* vals, const unsigned long long* n_dev,
+                                uint64_t cap, uint32_t* out_p, unsigned long long* out_m,
+                                double* out_inv, uint32_t* out_n, const uint32_t* old_n_dev,
+                                cudaStream_t st) {
+  const int grid = static_cast<int>(cap / 256 + 1 < 4096 ? cap / 256 + 1 : 4096);
+  append_table_kernel<<<grid, 256, 0, st>>>(vals, n_dev, cap, out_p, out_m, out_inv, out_n,
+                                            old_n_dev);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
                                double* out_inv, uint32_t* out_count, cudaStream_t st) {
   tiny_primes_kernel<<<1, 1024, 0, st>>>(n, out_p, out_m, out_inv, out_count);

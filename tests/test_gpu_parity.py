@@ -335,3 +335,30 @@ def test_published_prime_counts(sieve, N, pi):
     """Beyond the reference goldens (which stop at 1e12): standard published
     values of pi(x) (e.g. OEIS A006880 / A007053), up to 1e14."""
     assert sieve.count_range(0, N + 1).count == pi
+
+
+EXTEND_CODE = r"""
+import sys, json
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2310_17746_b200 as ws
+s = ws.Sieve()
+out = []
+# bounds grow 1e3 -> 1e5 -> 1e6 -> 3.2e7: each call extends the resident table
+for L, R in [(0, 10**6), (0, 10**10), (10**12 - 10**8, 10**12 + 10**8),
+             (10**15, 10**15 + 3 * 10**8), (2**40, 2**40 + 10**8)]:
+    c = s.count_range(L, R, checks=True)
+    v, n, ce = s.enumerate_range(L, min(R, L + 10**8))
+    out.append([c.count, c.sum, c.xor, c.largest, n, ce.sum, int(v[-1])])
+print(json.dumps(out))
+"""
+
+
+def test_base_extension_matches_rebuild():
+    """Device-side BasePrimeStore::extend (the table grows by sieving only the
+    new range) gives exactly the results of rebuilding the table each time."""
+    import json
+    a = json.loads(_run_isolated(EXTEND_CODE, {"WHEELSIEVE_BASE_EXTEND": "1"}).strip().splitlines()[-1])
+    b = json.loads(_run_isolated(EXTEND_CODE, {"WHEELSIEVE_BASE_EXTEND": "0"}).strip().splitlines()[-1])
+    assert a == b
+    assert a[1][0] == 455_052_511  # pi(1e10 - 1)
