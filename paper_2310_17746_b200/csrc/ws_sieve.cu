@@ -757,11 +757,18 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
         }
         if (rtotal == 0) continue;
         // The round's survivors go out in windows of kStage positions: each
-        // pass, lanes drop the positions (64*lane + bit) that fall in the
-        // window into the stage, then lane i writes window entries i, i+32, ...
-        // coalesced.  Almost every round is one window; dense ones (small
-        // values) take a few.
+        // pass, lanes drop their survivors that fall in the window into the
+        // stage (in ascending order), then lane i writes window entries i,
+        // i+32, ... coalesced.  Almost every round is one window; dense ones
+        // (small values) take a few.  The stage holds positions 64*lane + b
+        // (bit b of the interleaved masks); a survivor's value offset from
+        // rbase is 192*lane + 3b + 1 + (b & 1) < 6144.
         const uint32_t eb = lane << 6;
+        // the round's values share rbase's high word unless its low word is
+        // within 6144 of wrapping (once in ~7e5 rounds): 32-bit arithmetic
+        const uint32_t rlo = static_cast<uint32_t>(rbase);
+        const uint32_t rhi = static_cast<uint32_t>(rbase >> 32);
+        const bool nocarry = rlo < 0xFFFFFFFFu - 6144u;
 #pragma unroll 1
         for (uint32_t wlo = 0; wlo < rtotal; wlo += kStage) {
           const uint32_t wn = min(kStage, rtotal - wlo);
@@ -782,7 +789,9 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
           }
           __syncwarp();
           const unsigned long long wpos = pos + wlo;
-          uint32_t soff = 0, n = 0;
+          // values this lane writes in the window: i = lane, lane + 32, ... < wn
+          const uint32_t n = wn > lane ? (wn - 1 - lane) / 32 + 1 : 0u;
+          uint32_t soff = 0;
           if (kWire) {
             // entry = the survivor's bit position in its 4-word block's
             // interleaved masks: the low byte of 64 * lane + bit
@@ -794,45 +803,60 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
               const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
               if (seg_fits || wpos + i < P.out_cap) dst8[i] = static_cast<uint8_t>(e);
               soff += off;
-              ++n;
               xr ^= rbase + off;
             }
+          } else if (seg_fits && nocarry) {
+            uint2* dst = reinterpret_cast<uint2*>(P.out + wpos);
+            uint32_t xlo = 0;
+#pragma unroll 4
+            for (uint32_t i = lane; i < wn; i += 32) {
+              const uint32_t e = stage[i];
+              const uint32_t bb = e & 63u;
+              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+              const uint32_t vlo = rlo + off;
+              dst[i] = make_uint2(vlo, rhi);
+              soff += off;
+              xlo ^= vlo;
+            }
+            xr ^= (static_cast<unsigned long long>(n & 1u ? rhi : 0u) << 32) | xlo;
           } else {
             unsigned long long* dst = P.out + wpos;
-            if (seg_fits) {
-#pragma unroll 4
-              for (uint32_t i = lane; i < wn; i += 32) {
-                const uint32_t e = stage[i];
-                const uint32_t bb = e & 63u;
-                const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
-                const unsigned long long v = rbase + off;
-                dst[i] = v;
-                soff += off;
-                ++n;
-                xr ^= v;
-              }
-            } else {
-              for (uint32_t i = lane; i < wn; i += 32) {
-                const uint32_t e = stage[i];
-                const uint32_t bb = e & 63u;
-                const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
-                const unsigned long long v = rbase + off;
-                if (wpos + i < P.out_cap) dst[i] = v;
-                soff += off;
-                ++n;
-                xr ^= v;
-              }
+            for (uint32_t i = lane; i < wn; i += 32) {
+              const uint32_t e = stage[i];
+              const uint32_t bb = e & 63u;
+              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+              const unsigned long long v = rbase + off;
+              if (seg_fits || wpos + i < P.out_cap) dst[i] = v;
+              soff += off;
+              xr ^= v;
             }
           }
           sum += rbase * n + soff;
-          if (wlo + wn == rtotal) {  // the round's largest survivor
-            const uint32_t e = stage[wn - 1];
-            const uint32_t bb = e & 63u;
-            lg = rbase + (192u * (e >> 6) + 3u * bb + 1u + (bb & 1u));
-          }
           __syncwarp();
         }
         pos += rtotal;
+      }
+      // the segment's largest survivor (the job's largest is its last
+      // segment's): warp 0 scans the bitmap's top words
+      if (warp == 0) {
+        for (int32_t top = static_cast<int32_t>(si.nwords) - 1; top >= 0; top -= 32) {
+          const int32_t w = top - static_cast<int32_t>(lane);
+          uint32_t m1 = 0, m5 = 0;
+          if (w >= 0) {
+            m1 = ~bm1[w];
+            m5 = ~bm5[w];
+          }
+          const uint32_t any = __ballot_sync(kFull, (m1 | m5) != 0u);
+          if (any) {
+            if (lane == static_cast<uint32_t>(__ffs(any) - 1)) {
+              const unsigned long long wb = vbase + 192ull * static_cast<uint32_t>(w);
+              const unsigned long long v1 = m1 ? wb + 6ull * (31 - __clz(m1)) + 1 : 0;
+              const unsigned long long v5 = m5 ? wb + 6ull * (31 - __clz(m5)) + 5 : 0;
+              lg = max(v1, v5);
+            }
+            break;
+          }
+        }
       }
       sum = warp_sum64(sum);
       xr = warp_xor64(xr);
