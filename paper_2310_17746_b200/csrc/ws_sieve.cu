@@ -981,6 +981,13 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
 // ---------------------------------------------------------------------------
 // Level-0 base primes: a dense sieve of [0, n] (n <= 65537) in one block,
 // writing the primes >= 53 in ascending order with their Barrett constants.
+// the 54 primes below 256 (sqrt of the level-0 bound 65537)
+constexpr uint32_t kTinyPrimeCount = 54;
+__constant__ uint32_t kTinyPrimes[kTinyPrimeCount] = {
+    2,   3,   5,   7,   11,  13,  17,  19,  23,  29,  31,  37,  41,  43,  47,  53,  59,  61,
+    67,  71,  73,  79,  83,  89,  97,  101, 103, 107, 109, 113, 127, 131, 137, 139, 149, 151,
+    157, 163, 167, 173, 179, 181, 191, 193, 197, 199, 211, 223, 227, 229, 233, 239, 241, 251};
+
 __global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t* out_p,
                                                            unsigned long long* out_m,
                                                            double* out_inv,
@@ -990,14 +997,16 @@ __global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t*
   const uint32_t words = n / 32 + 1;
   for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) comp[i] = 0;
   __syncthreads();
-  for (uint32_t i = 2; i * i <= n; ++i) {
-    const bool is_prime = !((comp[i >> 5] >> (i & 31)) & 1u);
-    __syncthreads();
-    if (is_prime)
-      for (uint32_t j = i * i + threadIdx.x * i; j <= n; j += blockDim.x * i)
-        atomicOr(&comp[j >> 5], 1u << (j & 31));
-    __syncthreads();
+  // the primes up to sqrt(n) <= 256 cross off their multiples concurrently
+  // (no barrier per prime); 0 and 1 are excluded below by x >= 53
+#pragma unroll 1
+  for (uint32_t k = 0; k < kTinyPrimeCount; ++k) {
+    const uint32_t q = kTinyPrimes[k];
+    if (q * q > n) break;
+    for (uint32_t j = q * q + threadIdx.x * q; j <= n; j += blockDim.x * q)
+      atomicOr(&comp[j >> 5], 1u << (j & 31));
   }
+  __syncthreads();
   // ordered compaction: thread t owns numbers [t*chunk, (t+1)*chunk)
   const uint32_t chunk = (n + 1 + blockDim.x - 1) / blockDim.x;
   const uint32_t a = threadIdx.x * chunk;
