@@ -194,7 +194,6 @@ struct ws_ctx {
   cudaEvent_t ev_order = nullptr;
   static constexpr int kMaxChunks = 16;
   cudaEvent_t chunk_done[kMaxChunks] = {};
-  cudaEvent_t wire_done[kMaxChunks] = {};
   // host-bound enumeration through the 8-bit wire format (ws_wire.cpp);
   // WHEELSIEVE_HOST_WIRE=0 ships uint64 values instead
   bool host_wire = true;
@@ -226,8 +225,6 @@ struct ws_ctx {
     wblk.release();
     pin_wire.release();
     pin_wblk.release();
-    for (cudaEvent_t e : wire_done)
-      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ring_ev) cudaEventDestroy(e);
     for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n, &bucket[0], &bucket[1], &bcount[0], &bcount[1]})
       b->release();
@@ -970,8 +967,7 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
             cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) == cudaSuccess;
   for (int i = 0; i < ws_ctx::kMaxChunks && ok; ++i)
-    ok = cudaEventCreateWithFlags(&c->chunk_done[i], cudaEventDisableTiming) == cudaSuccess &&
-         cudaEventCreateWithFlags(&c->wire_done[i], cudaEventDisableTiming) == cudaSuccess;
+    ok = cudaEventCreateWithFlags(&c->chunk_done[i], cudaEventDisableTiming) == cudaSuccess;
   if (ok) {
     std::vector<uint32_t> tab(wsk::small_table_words());
     wsk::build_small_tables(tab.data());

@@ -87,17 +87,6 @@ __device__ __forceinline__ ModCtx mod_ctx(uint64_t ks) {
   return c;
 }
 
-__device__ __forceinline__ uint32_t mod_p(const ModCtx& c, uint32_t p, const double* inv,
-                                          const unsigned long long* m, uint32_t i) {
-  if (c.fast) {
-    const double t = __fma_rn(c.ksd, __ldg(inv + i), 6755399441055744.0);
-    const uint32_t q = static_cast<uint32_t>(__double2loint(t));
-    uint32_t r = c.kslo - q * p;
-    if (static_cast<int32_t>(r) < 0) r += p;
-    return r;
-  }
-  return mod_barrett(c.ks, p, __ldg(m + i));
-}
 
 // 32-bit shared-window address of a shared-memory pointer
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -280,14 +269,10 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
   }
 }
 
-// First hits (segment-relative) of prime p in both classes, or false when
-// p is not yet active in this segment (p*p beyond its end; since primes
-// ascend, no later prime is active either).  The activation test is two
-// 32-bit compares against the segment's thresholds.
-// ks mod p with 1/p already in a register (the per-thread prime loops load
-// it together with p, one iteration ahead)
-__device__ __forceinline__ uint32_t mod_p_inv(const ModCtx& c, uint32_t p, double inv_p,
-                                              const unsigned long long* m, uint32_t i) {
+// ks mod p from the FP64 quotient estimate (1/p comes preloaded: the prime
+// loops load it together with p, one iteration ahead); Barrett above 2^53
+__device__ __forceinline__ uint32_t mod_p(const ModCtx& c, uint32_t p, double inv_p,
+                                          const unsigned long long* m, uint32_t i) {
   if (c.fast) {
     const double t = __fma_rn(c.ksd, inv_p, 6755399441055744.0);
     const uint32_t q = static_cast<uint32_t>(__double2loint(t));
@@ -298,25 +283,11 @@ __device__ __forceinline__ uint32_t mod_p_inv(const ModCtx& c, uint32_t p, doubl
   return mod_barrett(c.ks, p, __ldg(m + i));
 }
 
-__device__ __forceinline__ bool prime_offsets_inv(uint32_t p, double inv_p, uint32_t i,
-                                                  const unsigned long long* m, const ModCtx& mc,
-                                                  uint32_t t_lo, uint32_t t_hi, uint32_t& rel1,
-                                                  uint32_t& rel5) {
-  if (p > t_hi) return false;
-  const uint32_t t1 = target1(p), t5 = target5(p);
-  if (p > t_lo) {  // activation segment (see prime_offsets)
-    const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;
-    rel1 = static_cast<uint32_t>(ksq - mc.ks);
-    rel5 = rel1 + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
-  } else {
-    const uint32_t r = mod_p_inv(mc, p, inv_p, m, i);
-    rel1 = t1 >= r ? t1 - r : t1 + p - r;
-    rel5 = t5 >= r ? t5 - r : t5 + p - r;
-  }
-  return true;
-}
-
-__device__ __forceinline__ bool prime_offsets(uint32_t p, uint32_t i, const double* inv,
+// First hits (segment-relative) of prime p in both classes, or false when
+// p is not yet active in this segment (p*p beyond its end; since primes
+// ascend, no later prime is active either).  The activation test is two
+// 32-bit compares against the segment's thresholds.
+__device__ __forceinline__ bool prime_offsets(uint32_t p, double inv_p, uint32_t i,
                                               const unsigned long long* m, const ModCtx& mc,
                                               uint32_t t_lo, uint32_t t_hi, uint32_t& rel1,
                                               uint32_t& rel5) {
@@ -329,12 +300,13 @@ __device__ __forceinline__ bool prime_offsets(uint32_t p, uint32_t i, const doub
     rel1 = static_cast<uint32_t>(ksq - mc.ks);
     rel5 = rel1 + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
   } else {
-    const uint32_t r = mod_p(mc, p, inv, m, i);
+    const uint32_t r = mod_p(mc, p, inv_p, m, i);
     rel1 = t1 >= r ? t1 - r : t1 + p - r;
     rel5 = t5 >= r ? t5 - r : t5 + p - r;
   }
   return true;
 }
+
 
 // ... if h < len, branch-free: a miss ORs 0 into the word picked by h's own
 // bits under wmask (spread over the banks, always inside the bitmap)
@@ -408,7 +380,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     const double ip = wip;
     claim(wi, wp, wip);
     uint32_t rel1, rel5;
-    if (!prime_offsets_inv(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
+    if (!prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
     mark_strided(a1, rel1, p, len, lane);
     mark_strided(a5, rel5, p, len, lane);
   }
@@ -444,7 +416,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       load(base + kStride + lane, mid_end, pn, ipn);
       if (__shfl_sync(kFull, p, 0) > t_hi) break;  // primes ascend: the rest is inactive
       uint32_t rel1, rel5;
-      if (!prime_offsets_inv(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) continue;
+      if (!prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) continue;
       const int32_t d = static_cast<int32_t>(rel5 - rel1);
       const uint32_t dpos = d > 0 ? static_cast<uint32_t>(d) : 0u;
       uint32_t h = rel1;
@@ -468,7 +440,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       load(base + kStride + lane, lp_end, pn, ipn);
       if (__shfl_sync(kFull, p, 0) > t_hi) break;
       uint32_t rel1 = len, rel5 = len;
-      prime_offsets_inv(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
+      prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
       mark_or(a1, rel1, len, P.S / 32 - 1);
       mark_or(a5, rel5, len, P.S / 32 - 1);
     }
@@ -928,7 +900,7 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
     }
     if (i < p_end) {
       uint32_t q1, q5;
-      if (prime_offsets_inv(p, ip, i, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
+      if (prime_offsets(p, ip, i, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
         if (q1 < span) r1 = q1;
         if (q5 < span) r5 = q5;
         if (p <= 0xFFFFFFFFu - span) {  // 32-bit stepping cannot wrap
