@@ -242,7 +242,10 @@ class Sieve:
         _check(lib.ws_enumerate_range(self._h, L, R, flags, _ptr(out), cap, C.byref(n),
                                       C.byref(chk)), self._h, "enumerate_range")
         if own:
-            return out[: n.value].copy(), n.value, Checks.of(chk)
+            # a view (no multi-GB copy) unless the capacity bound was much
+            # larger than the result
+            v = out[: n.value]
+            return (v if 2 * n.value >= out.size else v.copy()), n.value, Checks.of(chk)
         return out, n.value, Checks.of(chk)
 
     def count_intervals(self, Ls, width: int, want_sums: bool = True, want_xors: bool = True,
