@@ -115,6 +115,23 @@ def smem_bytes(L: int, R: int, S: int = SEG) -> float:
     return 4.0 * (2 * W + float(np.minimum(hits, W).sum()))
 
 
+def bucket_hits(L: int, R: int, S: int = SEG) -> int:
+    """Hits the library routes through HBM bucket lists for [L, R): every
+    multiple coprime to 6 of a base prime p >= 2S, when the range buckets at
+    all (largest base prime >= 8S -- the library's default policy).  Each is
+    8 B of HBM traffic: a 4-byte entry written by the fill, read back by the
+    window sieve ("bucket spill")."""
+    B = math.isqrt(R - 1)
+    if B < 8 * S:
+        return 0
+    P = small_primes(B)
+    P = P[P >= 2 * S]
+    lo = np.maximum(np.int64(L), P * P)
+    klo = -(-lo // P)
+    khi = (R - 1) // P
+    return int(np.where(khi >= klo, cop6(khi) - cop6(klo - 1), 0).sum())
+
+
 def smem_peak_gbs(sm_count: int, sm_mhz: float) -> float:
     return sm_count * 128 * sm_mhz * 1e6 / 1e9  # 32 banks x 4 B per clock per SM
 
@@ -367,17 +384,27 @@ def run_ours(args, cfg, world, rank, local):
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get(args.config, {}).get("traffic_bytes_per_launch")
-    if kind == "enumerate":
-        alg = 8.0 * units_local
+    # HBM model: the enumeration output (8 B per prime) plus the bucket-list
+    # round trip of the large primes (8 B per bucketed hit) when the range
+    # buckets; per step, against the step's kernel time
+    if kind == "intervals":
+        hits = sum(bucket_hits(int(L), int(L) + 2**24) for L in Ls[:64]) * (Ls.size / 64)
+    else:
+        hits = bucket_hits(lo, hi)
+    alg = (8.0 * units_local if kind == "enumerate" else 0.0) + 8.0 * hits
+    roof = None
+    if alg > 0:
         achieved = alg / (avg_sieve_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "kernel": "sieve_kernel<kEnumerate>",
+                "kernel": ("sieve_kernel<kEnumerate>" if kind == "enumerate" else "sieve_kernel")
+                          + (" + bucket_fill_kernel" if hits else ""),
                 "algorithmic_bytes_per_launch": alg,
+                "model": ("8 B x primes written" if kind == "enumerate" else "")
+                         + (" + " if kind == "enumerate" and hits else "")
+                         + (f"8 B x {hits:.4g} bucketed hits (p >= 2S)" if hits else ""),
                 "avg_launch_ms": avg_sieve_ms,
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs (copy)"}
-    else:
-        roof = None
     # shared-memory roofline: the sieve phase of every config
     if kind != "intervals":
         b_smem = smem_bytes(lo, hi)
@@ -391,7 +418,9 @@ def run_ours(args, cfg, world, rank, local):
                  "traffic": traffic if kind != "enumerate" else None,
                  "avg_launch_ms": avg_sieve_ms,
                  "peak_source": f"{props.multi_processor_count} SMs x 128 B/clk x {smax} MHz"}
-    if roof is None:
+    # the binding roofline: the model with the larger floor time
+    roof_hbm = roof
+    if roof is None or (b_smem / speak > alg / peaks["hbm_gbs"]):
         roof = roof_smem
     line = {
         "metric": cfg["metric"], "value": value, "unit": cfg["unit"], "n_gpus": world,
@@ -406,7 +435,7 @@ def run_ours(args, cfg, world, rank, local):
                    "sum": checks.sum if kind != "count" else None,
                    "xor": checks.xor if kind != "count" else None,
                    "largest": checks.largest if kind != "intervals" else None},
-        "e2e": e2e, "roofline": roof, "roofline_smem": roof_smem,
+        "e2e": e2e, "roofline": roof, "roofline_smem": roof_smem, "roofline_hbm": roof_hbm,
         "gpu_launches": launches, "clocks": clocks,
         "integers_per_s": (total_units if kind != "enumerate" else (hi - lo) * world)
                           / (ms_per_step / 1e3),
