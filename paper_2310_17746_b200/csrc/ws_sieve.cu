@@ -566,6 +566,36 @@ __device__ unsigned long long lookback(unsigned long long* status, uint64_t s,
 // 10 KiB stage + static + reserved) <= 228 KiB); a C2 round averages ~280.
 constexpr uint32_t kStage = 320;
 
+// The segment's largest survivor (0 if none), in every lane of the calling
+// warp: the top nonzero word of the bitmap, found 32 words at a time from the
+// end (the job's largest is its last segment's; one step almost always).
+__device__ __forceinline__ unsigned long long segment_largest(const SegInfo& si,
+                                                              const uint32_t* bm1,
+                                                              const uint32_t* bm5,
+                                                              unsigned long long vbase,
+                                                              uint32_t lane) {
+  for (int32_t top = static_cast<int32_t>(si.nwords) - 1; top >= 0; top -= 32) {
+    const int32_t w = top - static_cast<int32_t>(lane);
+    uint32_t m1 = 0, m5 = 0;
+    if (w >= 0) {
+      m1 = ~bm1[w];
+      m5 = ~bm5[w];
+    }
+    const uint32_t any = __ballot_sync(0xffffffffu, (m1 | m5) != 0u);
+    if (any) {
+      unsigned long long lg = 0;
+      if (lane == static_cast<uint32_t>(__ffs(any) - 1)) {
+        const unsigned long long wb = vbase + 192ull * static_cast<uint32_t>(w);
+        const unsigned long long v1 = m1 ? wb + 6ull * (31 - __clz(m1)) + 1 : 0;
+        const unsigned long long v5 = m5 ? wb + 6ull * (31 - __clz(m5)) + 5 : 0;
+        lg = v1 > v5 ? v1 : v5;
+      }
+      return __shfl_sync(0xffffffffu, lg, __ffs(any) - 1);
+    }
+  }
+  return 0;
+}
+
 template <int MODE>
 constexpr size_t mode_smem_extra() {
   return MODE >= kEnumerate ? kWarps * kStage * sizeof(uint16_t) : 0;
@@ -618,28 +648,22 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
       for (uint32_t wp = threadIdx.x; wp < si.nwords; wp += kThreads) {
         const uint32_t m1 = ~bm1[wp], m5 = ~bm5[wp];
         cnt += __popc(m1) + __popc(m5);
-        if (m1 | m5) {
-          const uint32_t w = wp;
-          const unsigned long long wb = vbase + 192ull * w;
-          const unsigned long long v1 = m1 ? wb + 6ull * (31 - __clz(m1)) + 1 : 0;
-          const unsigned long long v5 = m5 ? wb + 6ull * (31 - __clz(m5)) + 5 : 0;
-          lg = max(lg, max(v1, v5));
-          if (MODE == kCountChecks) {
-            for (uint32_t x = m1; x; x &= x - 1) {
-              const unsigned long long v = wb + 6ull * (__ffs(x) - 1) + 1;
-              sum += v;
-              xr ^= v;
-            }
-            for (uint32_t x = m5; x; x &= x - 1) {
-              const unsigned long long v = wb + 6ull * (__ffs(x) - 1) + 5;
-              sum += v;
-              xr ^= v;
-            }
+        if (MODE == kCountChecks && (m1 | m5)) {
+          const unsigned long long wb = vbase + 192ull * wp;
+          for (uint32_t x = m1; x; x &= x - 1) {
+            const unsigned long long v = wb + 6ull * (__ffs(x) - 1) + 1;
+            sum += v;
+            xr ^= v;
+          }
+          for (uint32_t x = m5; x; x &= x - 1) {
+            const unsigned long long v = wb + 6ull * (__ffs(x) - 1) + 5;
+            sum += v;
+            xr ^= v;
           }
         }
       }
       cnt = __reduce_add_sync(kFull, cnt);
-      lg = warp_max64(lg);
+      if (warp == 0) lg = segment_largest(si, bm1, bm5, vbase, lane);
       if (MODE == kCountChecks) {
         sum = warp_sum64(sum);
         xr = warp_xor64(xr);
@@ -808,28 +832,7 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
         }
         pos += rtotal;
       }
-      // the segment's largest survivor (the job's largest is its last
-      // segment's): warp 0 scans the bitmap's top words
-      if (warp == 0) {
-        for (int32_t top = static_cast<int32_t>(si.nwords) - 1; top >= 0; top -= 32) {
-          const int32_t w = top - static_cast<int32_t>(lane);
-          uint32_t m1 = 0, m5 = 0;
-          if (w >= 0) {
-            m1 = ~bm1[w];
-            m5 = ~bm5[w];
-          }
-          const uint32_t any = __ballot_sync(kFull, (m1 | m5) != 0u);
-          if (any) {
-            if (lane == static_cast<uint32_t>(__ffs(any) - 1)) {
-              const unsigned long long wb = vbase + 192ull * static_cast<uint32_t>(w);
-              const unsigned long long v1 = m1 ? wb + 6ull * (31 - __clz(m1)) + 1 : 0;
-              const unsigned long long v5 = m5 ? wb + 6ull * (31 - __clz(m5)) + 5 : 0;
-              lg = max(v1, v5);
-            }
-            break;
-          }
-        }
-      }
+      if (warp == 0) lg = segment_largest(si, bm1, bm5, vbase, lane);
       sum = warp_sum64(sum);
       xr = warp_xor64(xr);
       lg = warp_max64(lg);
