@@ -244,6 +244,10 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
   uint32_t a4 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 2021u);
   const uint32_t* t1 = tab;
   const uint32_t* t5 = tab + kTabPerClass;
+  // only a range's first and last segments are trimmed: an interior one keeps
+  // every slot of both classes (block-uniform test, the mask is skipped)
+  const uint32_t full = 32u * si.nwords;
+  const bool trim = si.lo1 != 0 || si.lo5 != 0 || si.hi1 != full || si.hi5 != full;
   for (uint32_t w = threadIdx.x; w < si.nwords; w += kThreads) {
     uint32_t m1 = tab_read(t1, a0) & tab_read(t1 + tab_off(1), a1) & tab_read(t1 + tab_off(2), a2) &
                   tab_read(t1 + tab_off(3), a3) & tab_read(t1 + tab_off(4), a4);
@@ -261,9 +265,11 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
       m1 |= 0xEEu >> si.ks;
       m5 |= 0xDFu >> si.ks;
     }
-    const int64_t base = 32 * static_cast<int64_t>(w);
-    m1 &= range_mask(static_cast<int64_t>(si.lo1) - base, static_cast<int64_t>(si.hi1) - base);
-    m5 &= range_mask(static_cast<int64_t>(si.lo5) - base, static_cast<int64_t>(si.hi5) - base);
+    if (trim) {
+      const int64_t base = 32 * static_cast<int64_t>(w);
+      m1 &= range_mask(static_cast<int64_t>(si.lo1) - base, static_cast<int64_t>(si.hi1) - base);
+      m5 &= range_mask(static_cast<int64_t>(si.lo5) - base, static_cast<int64_t>(si.hi5) - base);
+    }
     bm1[w] = ~m1;
     bm5[w] = ~m5;
   }
