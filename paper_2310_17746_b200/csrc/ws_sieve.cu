@@ -154,9 +154,11 @@ __host__ __device__ uint32_t table_word(uint32_t idx) {
   return word;
 }
 
-__device__ __forceinline__ uint32_t tab_read(const uint32_t* t, uint32_t off) {
-  const uint32_t i = off >> 5;
-  return __funnelshift_r(__ldg(t + i), __ldg(t + i + 1), off & 31u);
+// The device copy stores each table word together with its successor (one
+// 64-bit load per read); 32 bits at any bit offset < Q are one funnel shift.
+__device__ __forceinline__ uint32_t tab_read(const uint2* t, uint32_t off) {
+  const uint2 v = __ldg(t + (off >> 5));
+  return __funnelshift_r(v.x, v.y, off & 31u);
 }
 
 // ---------------------------------------------------------------------------
@@ -234,7 +236,7 @@ __device__ __forceinline__ uint32_t phase_step(uint32_t a, uint32_t step, uint32
   return a >= Q ? a - Q : a;
 }
 
-__device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* tab, uint32_t* bm1,
+__device__ __forceinline__ void init_words(const SegInfo& si, const uint2* tab, uint32_t* bm1,
                                            uint32_t* bm5) {
   constexpr uint32_t kStride = 32u * kThreads;
   uint32_t a0 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 5005u);
@@ -242,12 +244,14 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
   uint32_t a2 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 899u);
   uint32_t a3 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 1517u);
   uint32_t a4 = static_cast<uint32_t>((si.ks + 32u * threadIdx.x) % 2021u);
-  const uint32_t* t1 = tab;
-  const uint32_t* t5 = tab + kTabPerClass;
-  // only a range's first and last segments are trimmed: an interior one keeps
-  // every slot of both classes (block-uniform test, the mask is skipped)
+  const uint2* t1 = tab;
+  const uint2* t5 = tab + kTabPerClass;
+  // only a range's first and last segments are trimmed (and only the first
+  // segment of [0, ...) keeps the stamped primes): interior segments skip
+  // both with one block-uniform test
   const uint32_t full = 32u * si.nwords;
-  const bool trim = si.lo1 != 0 || si.lo5 != 0 || si.hi1 != full || si.hi5 != full;
+  const bool edge =
+      si.lo1 != 0 || si.lo5 != 0 || si.hi1 != full || si.hi5 != full || si.ks < 8;
   for (uint32_t w = threadIdx.x; w < si.nwords; w += kThreads) {
     uint32_t m1 = tab_read(t1, a0) & tab_read(t1 + tab_off(1), a1) & tab_read(t1 + tab_off(2), a2) &
                   tab_read(t1 + tab_off(3), a3) & tab_read(t1 + tab_off(4), a4);
@@ -258,14 +262,14 @@ __device__ __forceinline__ void init_words(const SegInfo& si, const uint32_t* ta
     a2 = phase_step(a2, kStride % 899u, 899u);
     a3 = phase_step(a3, kStride % 1517u, 1517u);
     a4 = phase_step(a4, kStride % 2021u, 2021u);
-    if (w == 0 && si.ks < 8) {
-      // the stamped primes themselves survive: 7, 13, 19, 31, 37, 43 at
-      // class-1 indices 1, 2, 3, 5, 6, 7 and 5, 11, 17, 23, 29, 41, 47 at
-      // class-5 indices 0..4, 6, 7
-      m1 |= 0xEEu >> si.ks;
-      m5 |= 0xDFu >> si.ks;
-    }
-    if (trim) {
+    if (edge) {
+      if (w == 0 && si.ks < 8) {
+        // the stamped primes themselves survive: 7, 13, 19, 31, 37, 43 at
+        // class-1 indices 1, 2, 3, 5, 6, 7 and 5, 11, 17, 23, 29, 41, 47 at
+        // class-5 indices 0..4, 6, 7
+        m1 |= 0xEEu >> si.ks;
+        m5 |= 0xDFu >> si.ks;
+      }
       const int64_t base = 32 * static_cast<int64_t>(w);
       m1 &= range_mask(static_cast<int64_t>(si.lo1) - base, static_cast<int64_t>(si.hi1) - base);
       m5 &= range_mask(static_cast<int64_t>(si.lo5) - base, static_cast<int64_t>(si.hi5) - base);
@@ -613,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bm1 = smem;
   uint32_t* bm5 = smem + P.S / 32;
-  const uint32_t* tab = P.small_tab;  // 4.4 KB, L1-resident
+  const uint2* tab = reinterpret_cast<const uint2*>(P.small_tab);  // 8.7 KB, L1-resident
   uint16_t* stage_all = reinterpret_cast<uint16_t*>(smem + 2 * (P.S / 32));
   __shared__ SegInfo si;
   __shared__ unsigned long long red_a[kWarps], red_b[kWarps], red_c[kWarps];
@@ -1030,9 +1034,13 @@ __global__ void prepare_table_kernel(const unsigned long long* vals, uint64_t sk
 
 }  // namespace
 
-uint32_t small_table_words() { return kTabWords; }
+// device layout: (word i, word i + 1) pairs, 2 * kTabWords uint32
+uint32_t small_table_words() { return 2 * kTabWords; }
 void build_small_tables(uint32_t* out) {
-  for (uint32_t i = 0; i < kTabWords; ++i) out[i] = table_word(i);
+  for (uint32_t i = 0; i < kTabWords; ++i) {
+    out[2 * i] = table_word(i);
+    out[2 * i + 1] = i + 1 < kTabWords ? table_word(i + 1) : 0u;
+  }
 }
 
 size_t sieve_smem_bytes(uint32_t S, int mode) {
