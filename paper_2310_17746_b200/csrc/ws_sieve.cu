@@ -35,6 +35,7 @@
 //                   the global output offset, then coalesced uint64 stores
 //                   (or the 8-bit host wire format, ws_wire.cpp).
 #include <cstdint>
+#include <type_traits>
 
 #include "ws_internal.h"
 
@@ -317,6 +318,34 @@ __device__ __forceinline__ bool prime_offsets(uint32_t p, double inv_p, uint32_t
   return true;
 }
 
+// prime_offsets with the quotient path fixed at compile time (FAST: the FP64
+// estimate, ks < 2^53), for loops unswitched on the segment-uniform flag
+template <bool FAST>
+__device__ __forceinline__ bool prime_offsets_t(uint32_t p, double inv_p, uint32_t i,
+                                                const unsigned long long* m, const ModCtx& mc,
+                                                uint32_t t_lo, uint32_t t_hi, uint32_t& rel1,
+                                                uint32_t& rel5) {
+  if (p > t_hi) return false;
+  const uint32_t t1 = target1(p), t5 = target5(p);
+  if (p > t_lo) {  // activation segment (see prime_offsets)
+    const uint64_t ksq = (static_cast<uint64_t>(p) * p - 1) / 6;
+    rel1 = static_cast<uint32_t>(ksq - mc.ks);
+    rel5 = rel1 + (t5 >= t1 ? t5 - t1 : t5 + p - t1);
+  } else {
+    uint32_t r;
+    if constexpr (FAST) {
+      const double t = __fma_rn(mc.ksd, inv_p, 6755399441055744.0);
+      r = mc.kslo - static_cast<uint32_t>(__double2loint(t)) * p;
+      if (static_cast<int32_t>(r) < 0) r += p;
+    } else {
+      r = mod_barrett(mc.ks, p, __ldg(m + i));
+    }
+    rel1 = t1 >= r ? t1 - r : t1 + p - r;
+    rel5 = t5 >= r ? t5 - r : t5 + p - r;
+  }
+  return true;
+}
+
 
 // ... if h < len, branch-free: a miss ORs 0 into the word picked by h's own
 // bits under wmask (spread over the banks, always inside the bitmap)
@@ -438,8 +467,9 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       mark_if(a5, h + d, d < 0 ? len : 0u);
     }
   }
-  // p >= S (no bucket list): at most one hit per class -- no loop, no branch
-  {
+  // p >= S (no bucket list): at most one hit per class -- no loop, no branch;
+  // unswitched on the quotient path (ks < 2^53 everywhere but the very top)
+  auto single_hits = [&](auto fast) {
     uint32_t base = mid_end + 32 * warp;
     uint32_t pn;
     double ipn;
@@ -450,11 +480,15 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       load(base + kStride + lane, lp_end, pn, ipn);
       if (__shfl_sync(kFull, p, 0) > t_hi) break;
       uint32_t rel1 = len, rel5 = len;
-      prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
+      prime_offsets_t<decltype(fast)::value>(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
       mark_or(a1, rel1, len, P.S / 32 - 1);
       mark_or(a5, rel5, len, P.S / 32 - 1);
     }
-  }
+  };
+  if (mc.fast)
+    single_hits(std::true_type{});
+  else
+    single_hits(std::false_type{});
   if (use_bucket) {
     // an entry is the bit index into [bm1 | bm5] (class at bit log2 S), so a
     // hit is shift + atomic; lists are read 4 entries per 128-bit streamed
