@@ -557,6 +557,23 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
     return;
   }
   if (B > 0xFFFFFFFFull) throw Fail{WS_OVERFLOW, "base bound exceeds 2^32"};
+  if (B <= wsk::kTinyMax) {  // the whole table from one one-block sieve
+    const uint64_t cap = prime_count_bound(0, B + 1);
+    c->tab_p.reserve(cap, "base table");
+    c->tab_m.reserve(cap, "base table");
+    c->tab_inv.reserve(cap, "base table");
+    c->d_tabn.reserve(1, "table size");
+    ck(wsk::launch_tiny_primes(static_cast<uint32_t>(B), c->tab_p.ptr, c->tab_m.ptr,
+                               c->tab_inv.ptr, c->d_tabn.ptr, c->stream), "tiny primes");
+    c->timing.launches += 1;
+    const uint64_t skip = small_primes_upto(B);
+    c->nprimes = static_cast<uint32_t>(cap > skip ? cap - skip : 0);
+    c->nprimes_dev = c->d_tabn.ptr;
+    c->base_B = B;
+    c->base_valid = true;
+    ck(cudaEventRecord(c->ev[1], c->stream), "event");
+    return;
+  }
   // level 0: primes in [37, isqrt(B)] (isqrt(B) < 2^16: at most 6542 - 11)
   const uint64_t B0 = isqrt_u64(B);
   c->l0_p.reserve(7000, "l0");

@@ -10,6 +10,7 @@ namespace wsk {
 constexpr int kThreads = 512;            // threads per sieve block
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kFirstTablePrime = 53; // primes 5..47 are stamped from pattern tables
+constexpr uint32_t kTinyMax = 1u << 18;  // one-block base sieve bound (tiny_primes_kernel)
 
 // One half-open value range [L, R) sieved as nseg segments of S wheel slots
 // per residue class starting at wheel index K0 = floor(L / 6)
@@ -121,7 +122,7 @@ cudaError_t launch_append_table(const unsigned long long* vals, const unsigned l
                                 double* out_inv, uint32_t* out_n, const uint32_t* old_n_dev,
                                 cudaStream_t st);
 
-// Level-0 base primes: all primes in [37, n] (n <= 65536 + 1) in one block.
+// Base primes in one block: all primes in [53, n] (n <= kTinyMax), ascending.
 cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
                                double* out_inv, uint32_t* out_count, cudaStream_t st);
 // Table preparation: vals[i] (uint64 primes, ascending) -> p / Barrett m for

@@ -998,40 +998,66 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
 }
 
 // ---------------------------------------------------------------------------
-// Level-0 base primes: a dense sieve of [0, n] (n <= 65537) in one block,
+// Base primes in one block: a dense sieve of [0, n] (n <= kTinyMax = 2^18)
 // writing the primes >= 53 in ascending order with their Barrett constants.
-// the 54 primes below 256 (sqrt of the level-0 bound 65537)
-constexpr uint32_t kTinyPrimeCount = 54;
+// Used as level 0 of the two-level base build and, when the whole base bound
+// fits, as the entire build (naive_sieve, wheel.cpp:40-54).
+// the 95 primes in [5, 512) (sqrt of kTinyMax); 2 and 3 never need marking
+// because the compaction keeps only 6k +- 1
+constexpr uint32_t kTinyPrimeCount = 95;
 __constant__ uint32_t kTinyPrimes[kTinyPrimeCount] = {
-    2,   3,   5,   7,   11,  13,  17,  19,  23,  29,  31,  37,  41,  43,  47,  53,  59,  61,
-    67,  71,  73,  79,  83,  89,  97,  101, 103, 107, 109, 113, 127, 131, 137, 139, 149, 151,
-    157, 163, 167, 173, 179, 181, 191, 193, 197, 199, 211, 223, 227, 229, 233, 239, 241, 251};
+      5,   7,  11,  13,  17,  19,  23,  29,  31,  37,  41,  43,  47,  53,  59,  61,
+     67,  71,  73,  79,  83,  89,  97, 101, 103, 107, 109, 113, 127, 131, 137, 139,
+    149, 151, 157, 163, 167, 173, 179, 181, 191, 193, 197, 199, 211, 223, 227, 229,
+    233, 239, 241, 251, 257, 263, 269, 271, 277, 281, 283, 293, 307, 311, 313, 317,
+    331, 337, 347, 349, 353, 359, 367, 373, 379, 383, 389, 397, 401, 409, 419, 421,
+    431, 433, 439, 443, 449, 457, 461, 463, 467, 479, 487, 491, 499, 503, 509,};
+
+// bit b of word w <-> x = 32 w + b; 32 w = 2 w (mod 6), so the 6k +- 1 mask
+// depends on w mod 3
+constexpr uint32_t wheel_mask(uint32_t ph) {
+  uint32_t m = 0;
+  for (uint32_t b = 0; b < 32; ++b) {
+    const uint32_t r = (2 * ph + b) % 6;
+    if (r == 1 || r == 5) m |= 1u << b;
+  }
+  return m;
+}
+constexpr uint32_t kWheelMask0 = wheel_mask(0), kWheelMask1 = wheel_mask(1),
+                   kWheelMask2 = wheel_mask(2);
 
 __global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t* out_p,
                                                            unsigned long long* out_m,
                                                            double* out_inv,
                                                            uint32_t* out_count) {
-  __shared__ uint32_t comp[(65536 + 64) / 32 + 1];
+  __shared__ uint32_t comp[kTinyMax / 32 + 1];
   __shared__ uint32_t scan[1024];
   const uint32_t words = n / 32 + 1;
   for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) comp[i] = 0;
   __syncthreads();
-  // the primes up to sqrt(n) <= 256 cross off their multiples concurrently
-  // (no barrier per prime); 0 and 1 are excluded below by x >= 53
+  // the primes up to sqrt(n) cross off their odd multiples from q*q
+  // concurrently (no barrier per prime)
 #pragma unroll 1
   for (uint32_t k = 0; k < kTinyPrimeCount; ++k) {
     const uint32_t q = kTinyPrimes[k];
     if (q * q > n) break;
-    for (uint32_t j = q * q + threadIdx.x * q; j <= n; j += blockDim.x * q)
+    for (uint32_t j = q * q + threadIdx.x * 2 * q; j <= n; j += blockDim.x * 2 * q)
       atomicOr(&comp[j >> 5], 1u << (j & 31));
   }
   __syncthreads();
-  // ordered compaction: thread t owns numbers [t*chunk, (t+1)*chunk)
-  const uint32_t chunk = (n + 1 + blockDim.x - 1) / blockDim.x;
-  const uint32_t a = threadIdx.x * chunk;
+  // ordered compaction: thread t owns words [t * wpt, (t + 1) * wpt)
+  const uint32_t wpt = (words + blockDim.x - 1) / blockDim.x;
+  const uint32_t w0 = min(words, threadIdx.x * wpt), w1 = min(words, w0 + wpt);
+  auto survivors = [&](uint32_t w) {
+    const uint32_t ph = w % 3;
+    uint32_t v = ~comp[w] & (ph == 0 ? kWheelMask0 : ph == 1 ? kWheelMask1 : kWheelMask2);
+    if (w == 1) v &= ~((1u << (kFirstTablePrime - 32)) - 1);  // x >= 53
+    if (w == 0) v = 0;
+    if (w == words - 1 && (n & 31) != 31) v &= (2u << (n & 31)) - 1;  // x <= n
+    return v;
+  };
   uint32_t c = 0;
-  for (uint32_t x = a; x < a + chunk && x <= n; ++x)
-    c += (x >= kFirstTablePrime) && !((comp[x >> 5] >> (x & 31)) & 1u);
+  for (uint32_t w = w0; w < w1; ++w) c += __popc(survivors(w));
   scan[threadIdx.x] = c;
   __syncthreads();
   for (uint32_t o = 1; o < blockDim.x; o <<= 1) {
@@ -1041,8 +1067,9 @@ __global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t*
     __syncthreads();
   }
   uint32_t pos = scan[threadIdx.x] - c;
-  for (uint32_t x = a; x < a + chunk && x <= n; ++x)
-    if (x >= kFirstTablePrime && !((comp[x >> 5] >> (x & 31)) & 1u)) {
+  for (uint32_t w = w0; w < w1; ++w)
+    for (uint32_t v = survivors(w); v; v &= v - 1) {
+      const uint32_t x = 32 * w + __ffs(v) - 1;
       out_p[pos] = x;
       out_m[pos] = ~0ull / x;
       out_inv[pos] = 1.0 / static_cast<double>(x);

@@ -282,6 +282,36 @@ def test_base_primes_match_bootstrap(sieve):
     assert e.value.code == ws.Errc.EmptyRange
 
 
+@pytest.mark.parametrize("B", [53, 54, 1000, 31623, 2**18 - 1, 2**18, 2**18 + 1, 10**6])
+def test_base_table_one_block_and_two_level_builds(B, port):
+    """Fresh table builds either side of the one-block bound (kTinyMax = 2^18)
+    against a numpy sieve, and a prime count that uses each table."""
+    import paper_2310_17746_b200 as ws
+    comp = np.zeros(B + 1, dtype=bool)
+    comp[:2] = True
+    for q in range(2, int(B**0.5) + 1):
+        if not comp[q]:
+            comp[q * q::q] = True
+    want = np.nonzero(~comp)[0]
+    want = want[want >= 5]
+    s = ws.Sieve()
+    try:
+        got = s.base_primes(B)
+        assert got.size == want.size and np.array_equal(got.astype(np.int64), want)
+    finally:
+        s.close()
+    # a window whose base bound is about B: [B^2 - 10^6, B^2)
+    R = B * B
+    L = max(0, R - 10**6)
+    s = ws.Sieve()
+    try:
+        c = s.count_range(L, R, checks=True)
+    finally:
+        s.close()
+    o = port.range(L, R)
+    assert (c.count, c.sum, c.xor, c.largest) == (o["count"], o["sum"], o["xor"], o["largest"])
+
+
 def test_repeated_fresh_base_with_buckets():
     """Regression: repeated WS_FRESH_BASE calls on a bucketed range (the base
     sieve and the main launch stage their uploads through pinned memory)."""
