@@ -190,6 +190,13 @@ struct ws_ctx {
   DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)
   DevBuf<uint32_t> bcount[2];
   cudaStream_t fstream = nullptr;  // bucket-fill stream
+  // one-block base builds run on their own stream, overlapping the call's
+  // uploads and resets; the first launch that reads the table joins it
+  cudaStream_t bstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_base = nullptr;
+  bool base_pending = false;
+  const unsigned long long* ticket_zeroed = nullptr;  // ticket buffer known to be zero
+  size_t ticket_zeroed_cap = 0;
   cudaStream_t cstream = nullptr;  // device->host copy stream (chunked enumeration)
   cudaEvent_t ev_order = nullptr;
   static constexpr int kMaxChunks = 16;
@@ -241,6 +248,9 @@ struct ws_ctx {
       if (sieve_done[i]) cudaEventDestroy(sieve_done[i]);
     }
     if (fstream) cudaStreamDestroy(fstream);
+    if (bstream) cudaStreamDestroy(bstream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_base) cudaEventDestroy(ev_base);
     if (cstream) cudaStreamDestroy(cstream);
     if (ev_order) cudaEventDestroy(ev_order);
     for (cudaEvent_t e : chunk_done)
@@ -322,6 +332,13 @@ double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
 // The segment kernel over every segment of ctx->h_jobs.  Without large
 // primes this is one launch; otherwise the segments are processed in windows
 // of W segments: bucket_fill (large-prime hit lists) then the sieve kernel.
+// Order the main stream after a pending one-block base build (bstream).
+void join_base(ws_ctx* c) {
+  if (!c->base_pending) return;
+  ck(cudaStreamWaitEvent(c->stream, c->ev_base, 0), "base join");
+  c->base_pending = false;
+}
+
 struct WireArgs {  // kEnumWire outputs
   uint8_t* entries;
   uint8_t* blk8;
@@ -334,20 +351,23 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   for (const auto& j : c->h_jobs) nseg += j.nseg;
   const size_t nj = c->h_jobs.size();
   c->jobs.reserve(nj, "jobs");
-  if (c->acc.cap < acc_base + nj) {  // grow without losing accumulators of earlier chunks
+  // + 1: the slot after the accumulators receives the exact table size
+  if (c->acc.cap < acc_base + nj + 1) {  // grow without losing accumulators of earlier chunks
     if (acc_base) ck(cudaStreamSynchronize(c->stream), "sync");
     DevBuf<wsk::JobAcc> bigger;
-    bigger.reserve(std::max<size_t>(acc_base + nj, 16), "acc");
+    bigger.reserve(std::max<size_t>(acc_base + nj + 1, 16), "acc");
     if (acc_base)
       ck(cudaMemcpy(bigger.ptr, c->acc.ptr, acc_base * sizeof(wsk::JobAcc), cudaMemcpyDeviceToDevice),
          "acc");
     std::swap(c->acc, bigger);
     bigger.release();
   }
-  void* hj = c->pin_up.alloc(nj * sizeof(wsk::Job), "pinned jobs");
-  std::memcpy(hj, c->h_jobs.data(), nj * sizeof(wsk::Job));
-  ck(copy_async(c, c->jobs.ptr, hj, nj * sizeof(wsk::Job), cudaMemcpyHostToDevice, c->stream),
-     "upload jobs");
+  if (nj > 1) {  // a single job travels in the kernel parameters
+    void* hj = c->pin_up.alloc(nj * sizeof(wsk::Job), "pinned jobs");
+    std::memcpy(hj, c->h_jobs.data(), nj * sizeof(wsk::Job));
+    ck(copy_async(c, c->jobs.ptr, hj, nj * sizeof(wsk::Job), cudaMemcpyHostToDevice, c->stream),
+       "upload jobs");
+  }
   ck(cudaMemsetAsync(c->acc.ptr + acc_base, 0, nj * sizeof(wsk::JobAcc), c->stream), "zero acc");
   if (mode >= wsk::kEnumerate) {
     c->status.reserve(nseg, "status");
@@ -357,8 +377,10 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   if (nseg == 0) return;
   wsk::SieveParams p{};
   p.small_tab = c->small_tab.ptr;
-  p.jobs = c->jobs.ptr;
+  p.jobs = nj > 1 ? c->jobs.ptr : nullptr;
+  if (nj == 1) p.job0 = c->h_jobs[0];
   p.njobs = static_cast<uint32_t>(nj);
+  p.tabn_out = reinterpret_cast<uint32_t*>(c->acc.ptr + acc_base + nj);
   p.nseg_total = nseg;
   p.S = c->S;
   p.prime_p = c->tab_p.ptr;
@@ -408,9 +430,14 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     }
   }
   const uint64_t nwin = (nseg + W - 1) / W;
-  c->ticket.reserve(nwin, "tickets");
-  ck(cudaMemsetAsync(c->ticket.ptr, 0, nwin * sizeof(unsigned long long), c->stream),
-     "zero tickets");
+  // one {counter, exits} pair per window; kernels leave them zero
+  c->ticket.reserve(2 * nwin, "tickets");
+  if (c->ticket_zeroed != c->ticket.ptr || c->ticket_zeroed_cap != c->ticket.cap) {
+    ck(cudaMemsetAsync(c->ticket.ptr, 0, c->ticket.cap * sizeof(unsigned long long), c->stream),
+       "zero tickets");
+    c->ticket_zeroed = c->ticket.ptr;
+    c->ticket_zeroed_cap = c->ticket.cap;
+  }
   // runs of every window, uploaded once
   std::vector<wsk::Run> runs;
   std::vector<uint32_t> run_off(nwin + 1, 0);
@@ -451,6 +478,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
                   c->stream), "upload runs");
   }
   // ev[2] (call start) / ev[4] order the fill stream after everything queued so far
+  join_base(c);
   if (record_start) ck(cudaEventRecord(c->ev[2], c->stream), "event");
   ck(cudaEventRecord(c->ev_order, c->stream), "event");
   if (buckets) ck(cudaStreamWaitEvent(c->fstream, c->ev_order, 0), "fill wait");
@@ -485,7 +513,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     }
     p.s_begin = ws;
     p.s_count = we - ws;
-    p.ticket = c->ticket.ptr + w;
+    p.ticket = c->ticket.ptr + 2 * w;
     const int grid = static_cast<int>(std::min<uint64_t>(we - ws, max_grid));
     ck(wsk::launch_sieve(mode, p, grid, c->stream), "sieve launch");
     if (buckets) ck(cudaEventRecord(c->sieve_done[b], c->stream), "event");
@@ -503,6 +531,7 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
 // table [53, base_B] already covers sqrt(B), so only (base_B, B] is sieved --
 // with that table -- and appended; the table size stays on the device.
 void extend_base(ws_ctx* c, uint64_t B) {
+  join_base(c);
   ck(cudaEventRecord(c->ev[0], c->stream), "event");
   const uint64_t lo = c->base_B + 1;
   const uint64_t cap = prime_count_bound(lo, B + 1);
@@ -540,6 +569,7 @@ void extend_base(ws_ctx* c, uint64_t B) {
 
 void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
   c->base_built = false;
+  join_base(c);
   if (c->base_valid && c->base_B >= B && !fresh) return;
   if (c->base_extend && c->base_valid && !fresh && c->nprimes_dev == c->d_tabn.ptr &&
       c->base_B >= wsk::kFirstTablePrime && isqrt_u64(B) <= c->base_B && B <= 0xFFFFFFFFull &&
@@ -557,21 +587,27 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
     return;
   }
   if (B > 0xFFFFFFFFull) throw Fail{WS_OVERFLOW, "base bound exceeds 2^32"};
-  if (B <= wsk::kTinyMax) {  // the whole table from one one-block sieve
+  if (B <= wsk::kTinyMax) {  // the whole table from one one-block sieve, on bstream
     const uint64_t cap = prime_count_bound(0, B + 1);
     c->tab_p.reserve(cap, "base table");
     c->tab_m.reserve(cap, "base table");
     c->tab_inv.reserve(cap, "base table");
     c->d_tabn.reserve(1, "table size");
+    // after everything queued so far (earlier launches read the old table)
+    ck(cudaEventRecord(c->ev_fork, c->stream), "event");
+    ck(cudaStreamWaitEvent(c->bstream, c->ev_fork, 0), "base fork");
+    ck(cudaEventRecord(c->ev[0], c->bstream), "event");
     ck(wsk::launch_tiny_primes(static_cast<uint32_t>(B), c->tab_p.ptr, c->tab_m.ptr,
-                               c->tab_inv.ptr, c->d_tabn.ptr, c->stream), "tiny primes");
+                               c->tab_inv.ptr, c->d_tabn.ptr, c->bstream), "tiny primes");
+    ck(cudaEventRecord(c->ev[1], c->bstream), "event");
+    ck(cudaEventRecord(c->ev_base, c->bstream), "event");
+    c->base_pending = true;
     c->timing.launches += 1;
     const uint64_t skip = small_primes_upto(B);
     c->nprimes = static_cast<uint32_t>(cap > skip ? cap - skip : 0);
     c->nprimes_dev = c->d_tabn.ptr;
     c->base_B = B;
     c->base_valid = true;
-    ck(cudaEventRecord(c->ev[1], c->stream), "event");
     return;
   }
   // level 0: primes in [37, isqrt(B)] (isqrt(B) < 2^16: at most 6542 - 11)
@@ -623,19 +659,17 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
   ck(cudaEventRecord(c->ev[1], c->stream), "event");
 }
 
-// Copy the n job accumulators (and the exact table size) to pinned host
-// memory and wait: the one synchronisation of a call.
+// Copy the n job accumulators and, from the slot after them, the exact table
+// size (stored by the kernel: run_sieve's tabn_out) to pinned host memory in
+// one copy, and wait: the one synchronisation of a call.
 const wsk::JobAcc* fetch_results(ws_ctx* c, size_t n) {
-  char* h = static_cast<char*>(c->pin_out.reserve(n * sizeof(wsk::JobAcc) + 16, "pinned out"));
-  ck(copy_async(c, h, c->acc.ptr, n * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost, c->stream),
-     "results");
-  uint32_t* tabn = reinterpret_cast<uint32_t*>(h + n * sizeof(wsk::JobAcc));
-  *tabn = c->nprimes;
-  if (c->nprimes_dev)
-    ck(copy_async(c, tabn, c->nprimes_dev, 4, cudaMemcpyDeviceToHost, c->stream), "table size");
+  char* h = static_cast<char*>(c->pin_out.reserve((n + 1) * sizeof(wsk::JobAcc), "pinned out"));
+  ck(copy_async(c, h, c->acc.ptr, (n + 1) * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost,
+                c->stream), "results");
   ck(cudaStreamSynchronize(c->stream), "sync");
   ck(cudaGetLastError(), "kernel");
-  c->timing.base_primes = *tabn + small_primes_upto(c->base_B);
+  const uint32_t tabn = *reinterpret_cast<const uint32_t*>(h + n * sizeof(wsk::JobAcc));
+  c->timing.base_primes = tabn + small_primes_upto(c->base_B);
   return reinterpret_cast<const wsk::JobAcc*>(h);
 }
 
@@ -981,6 +1015,9 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
       return WS_CUDA;
     }
   bool ok = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->bstream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_base, cudaEventDisableTiming) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) == cudaSuccess;
   for (int i = 0; i < ws_ctx::kMaxChunks && ok; ++i)

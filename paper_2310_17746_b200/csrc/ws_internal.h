@@ -53,8 +53,10 @@ struct Run {             // a maximal run of window segments of one job
 
 struct SieveParams {
   const uint32_t* small_tab;  // small-prime pattern tables (built once per context)
-  const Job* jobs;
+  const Job* jobs;                   // njobs > 1 (device copy)
+  Job job0;                          // njobs == 1: the job itself (no upload)
   uint32_t njobs;
+  uint32_t* tabn_out;                // nullable: CTA 0 stores the exact table size
   uint64_t nseg_total;   // segments of all jobs
   uint64_t s_begin;      // this launch sieves segments [s_begin, s_begin + s_count)
   uint64_t s_count;
@@ -71,7 +73,8 @@ struct SieveParams {
   const uint32_t* bucket;            // window lists: bucket[(s - s_begin) * bcap + i]
   uint32_t* bcount;                  // entries per window segment (reset after use)
   uint32_t bcap;
-  unsigned long long* ticket;        // dynamic segment counter (zeroed per launch)
+  unsigned long long* ticket;        // {segment counter, exits}: zero at launch; the last
+                                     // CTA out resets both for the next launch
   JobAcc* acc;                       // njobs accumulators (zeroed per launch)
   uint32_t* per_seg;                 // nullable, nseg_total counts
   unsigned long long* status;        // enumeration look-back words (zeroed)

@@ -197,14 +197,28 @@ __device__ __forceinline__ uint32_t end_valid(uint64_t ks, uint32_t c, uint64_t 
 __device__ void fetch_segment(const SieveParams& P, SegInfo& si) {
   const unsigned long long t = atomicAdd(P.ticket, 1ull);
   si.s = t < P.s_count ? P.s_begin + t : ~0ull;
-  if (t >= P.s_count) return;
-  const uint64_t s = si.s;
-  uint32_t lo = 0, hi = P.njobs;  // last job with seg_begin <= s
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) / 2;
-    if (P.jobs[mid].seg_begin <= s) lo = mid; else hi = mid;
+  if (t >= P.s_count) {
+    // every CTA draws exactly one failing ticket; after the last one no CTA
+    // draws again, so it resets the pair for the next launch (no memset)
+    if (atomicAdd(P.ticket + 1, 1ull) == gridDim.x - 1) {
+      P.ticket[0] = 0;
+      P.ticket[1] = 0;
+    }
+    return;
   }
-  const Job& J = P.jobs[lo];
+  const uint64_t s = si.s;
+  uint32_t lo = 0;
+  Job J;
+  if (P.njobs == 1) {
+    J = P.job0;
+  } else {
+    uint32_t hi = P.njobs;  // last job with seg_begin <= s
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) / 2;
+      if (P.jobs[mid].seg_begin <= s) lo = mid; else hi = mid;
+    }
+    J = P.jobs[lo];
+  }
   si.job = lo;
   const uint64_t local = s - J.seg_begin;
   si.ks = J.K0 + local * P.S;
@@ -663,6 +677,7 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 
   const uint32_t nprimes = P.nprimes_dev ? min(P.nprimes, *P.nprimes_dev) : P.nprimes;
+  if (P.tabn_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *P.tabn_out = nprimes;
   for (;;) {
     __syncthreads();  // bitmap / si reuse guard
     if (threadIdx.x == 0) {
