@@ -99,6 +99,9 @@ unsigned default_threads() {
   unsigned h = 0;
   if (sched_getaffinity(0, sizeof set, &set) == 0) h = static_cast<unsigned>(CPU_COUNT(&set));
   if (!h) h = std::thread::hardware_concurrency();
+  // one CPU stays with the calling thread, which spins on the ring's copy
+  // events (c2 e2e on 16 vCPUs: 24.3 ms with 16 expanders, 23.2-23.7 with 14-15)
+  if (h > 4) --h;
   return std::max(1u, std::min(h ? h : 4u, 64u));
 }
 
