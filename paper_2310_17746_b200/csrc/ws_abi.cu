@@ -2,9 +2,10 @@
 //
 // Orchestration that the reference does in run_loop (engine.cpp:149-307) and
 // BasePrimeStore::bootstrap (base_store.cpp:34-42) is redone device-first:
-//   1. base primes <= isqrt(R - 1) are sieved on the device (level 0: one
-//      block, dense, primes <= 2^16; level 1: the main sieve kernel itself
-//      enumerating [0, B]); the table is kept resident and only re-sieved
+//   1. base primes <= isqrt(R - 1) are sieved on the device (bounds up to
+//      2^18 by small_base_kernel alone; above, it gives level 0, the primes
+//      <= sqrt(B), and the main sieve kernel enumerates [0, B] as level 1);
+//      the table is kept resident and only re-sieved
 //      when a call needs a larger bound (the reference's incremental base
 //      store, base_store.cpp:44-76) or WS_FRESH_BASE is set;
 //   2. one launch of the segment kernel covers every segment of every
@@ -190,11 +191,13 @@ struct ws_ctx {
   DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)
   DevBuf<uint32_t> bcount[2];
   cudaStream_t fstream = nullptr;  // bucket-fill stream
-  // one-block base builds run on their own stream, overlapping the call's
+  // small base builds (B <= 2^18) run on their own stream, overlapping the call's
   // uploads and resets; the first launch that reads the table joins it
   cudaStream_t bstream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_base = nullptr;
   bool base_pending = false;
+  DevBuf<unsigned long long> base_scratch;  // small_base_kernel's epoch-tagged block counts
+  uint32_t base_epoch = 0;
   const unsigned long long* ticket_zeroed = nullptr;  // ticket buffer known to be zero
   size_t ticket_zeroed_cap = 0;
   cudaStream_t cstream = nullptr;  // device->host copy stream (chunked enumeration)
@@ -251,6 +254,7 @@ struct ws_ctx {
     }
     if (fstream) cudaStreamDestroy(fstream);
     if (bstream) cudaStreamDestroy(bstream);
+    base_scratch.release();
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_base) cudaEventDestroy(ev_base);
     if (cstream) cudaStreamDestroy(cstream);
@@ -334,7 +338,7 @@ double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
 // The segment kernel over every segment of ctx->h_jobs.  Without large
 // primes this is one launch; otherwise the segments are processed in windows
 // of W segments: bucket_fill (large-prime hit lists) then the sieve kernel.
-// Order the main stream after a pending one-block base build (bstream).
+// Order the main stream after a pending small base build (bstream).
 void join_base(ws_ctx* c) {
   if (!c->base_pending) return;
   ck(cudaStreamWaitEvent(c->stream, c->ev_base, 0), "base join");
@@ -569,6 +573,16 @@ void extend_base(ws_ctx* c, uint64_t B) {
   ck(cudaEventRecord(c->ev[1], c->stream), "event");
 }
 
+cudaError_t launch_small_base(ws_ctx* c, uint32_t n, uint32_t* p, unsigned long long* m,
+                              double* inv, uint32_t* count, cudaStream_t st) {
+  if (!c->base_scratch.ptr) {
+    c->base_scratch.reserve(64, "base scratch");
+    ck(cudaMemset(c->base_scratch.ptr, 0, 64 * sizeof(unsigned long long)), "base scratch");
+  }
+  if (++c->base_epoch == 0) ++c->base_epoch;  // 0 marks "never written"
+  return wsk::launch_small_base(n, p, m, inv, count, c->base_scratch.ptr, c->base_epoch, st);
+}
+
 void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
   c->base_built = false;
   join_base(c);
@@ -589,7 +603,7 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
     return;
   }
   if (B > 0xFFFFFFFFull) throw Fail{WS_OVERFLOW, "base bound exceeds 2^32"};
-  if (B <= wsk::kTinyMax) {  // the whole table from one one-block sieve, on bstream
+  if (B <= wsk::kTinyMax) {  // the whole table from one small_base launch, on bstream
     const uint64_t cap = prime_count_bound(0, B + 1);
     c->tab_p.reserve(cap, "base table");
     c->tab_m.reserve(cap, "base table");
@@ -599,8 +613,8 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
     ck(cudaEventRecord(c->ev_fork, c->stream), "event");
     ck(cudaStreamWaitEvent(c->bstream, c->ev_fork, 0), "base fork");
     ck(cudaEventRecord(c->ev[0], c->bstream), "event");
-    ck(wsk::launch_tiny_primes(static_cast<uint32_t>(B), c->tab_p.ptr, c->tab_m.ptr,
-                               c->tab_inv.ptr, c->d_tabn.ptr, c->bstream), "tiny primes");
+    ck(launch_small_base(c, static_cast<uint32_t>(B), c->tab_p.ptr, c->tab_m.ptr, c->tab_inv.ptr,
+                         c->d_tabn.ptr, c->bstream), "small base");
     ck(cudaEventRecord(c->ev[1], c->bstream), "event");
     ck(cudaEventRecord(c->ev_base, c->bstream), "event");
     c->base_pending = true;
@@ -618,8 +632,8 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
   c->l0_m.reserve(7000, "l0");
   c->l0_inv.reserve(7000, "l0");
   c->l0_n.reserve(1, "l0");
-  ck(wsk::launch_tiny_primes(static_cast<uint32_t>(B0), c->l0_p.ptr, c->l0_m.ptr, c->l0_inv.ptr,
-                             c->l0_n.ptr, c->stream), "tiny primes");
+  ck(launch_small_base(c, static_cast<uint32_t>(B0), c->l0_p.ptr, c->l0_m.ptr, c->l0_inv.ptr,
+                       c->l0_n.ptr, c->stream), "small base");
   c->timing.launches += 1;
   // level 1: enumerate [0, B + 1) with the level-0 table
   const uint64_t cap = prime_count_bound(0, B + 1);

@@ -10,7 +10,7 @@ namespace wsk {
 constexpr int kThreads = 512;            // threads per sieve block
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kFirstTablePrime = 53; // primes 5..47 are stamped from pattern tables
-constexpr uint32_t kTinyMax = 1u << 18;  // one-block base sieve bound (tiny_primes_kernel)
+constexpr uint32_t kTinyMax = 1u << 18;  // small_base_kernel bound (at most 33 blocks)
 
 // One half-open value range [L, R) sieved as nseg segments of S wheel slots
 // per residue class starting at wheel index K0 = floor(L / 6)
@@ -125,9 +125,12 @@ cudaError_t launch_append_table(const unsigned long long* vals, const unsigned l
                                 double* out_inv, uint32_t* out_n, const uint32_t* old_n_dev,
                                 cudaStream_t st);
 
-// Base primes in one block: all primes in [53, n] (n <= kTinyMax), ascending.
-cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
-                               double* out_inv, uint32_t* out_count, cudaStream_t st);
+// Small base tables: all primes in [53, n] (n <= kTinyMax), ascending, with
+// their Barrett constants; scratch holds >= 64 words (zeroed once), epoch is
+// nonzero and differs from the previous launch's on the same scratch.
+cudaError_t launch_small_base(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
+                              double* out_inv, uint32_t* out_count, unsigned long long* scratch,
+                              uint32_t epoch, cudaStream_t st);
 // Table preparation: vals[i] (uint64 primes, ascending) -> p / Barrett m for
 // i in [skip, n).
 // n_dev: number of values (device); out_n = n - skip (device).  cap bounds n.

@@ -1013,10 +1013,10 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
 }
 
 // ---------------------------------------------------------------------------
-// Base primes in one block: a dense sieve of [0, n] (n <= kTinyMax = 2^18)
-// writing the primes >= 53 in ascending order with their Barrett constants.
-// Used as level 0 of the two-level base build and, when the whole base bound
-// fits, as the entire build (naive_sieve, wheel.cpp:40-54).
+// Small base tables: a dense sieve of [0, n] (n <= kTinyMax = 2^18) writing
+// the primes >= 53 in ascending order with their Barrett constants
+// (naive_sieve, wheel.cpp:40-54).  Used as level 0 of the two-level base build
+// and, when the whole base bound fits, as the entire build.
 // the 95 primes in [5, 512) (sqrt of kTinyMax); 2 and 3 never need marking
 // because the compaction keeps only 6k +- 1
 constexpr uint32_t kTinyPrimeCount = 95;
@@ -1041,56 +1041,89 @@ constexpr uint32_t wheel_mask(uint32_t ph) {
 constexpr uint32_t kWheelMask0 = wheel_mask(0), kWheelMask1 = wheel_mask(1),
                    kWheelMask2 = wheel_mask(2);
 
-__global__ void __launch_bounds__(1024) tiny_primes_kernel(uint32_t n, uint32_t* out_p,
-                                                           unsigned long long* out_m,
-                                                           double* out_inv,
-                                                           uint32_t* out_count) {
-  __shared__ uint32_t comp[kTinyMax / 32 + 1];
-  __shared__ uint32_t scan[1024];
-  const uint32_t words = n / 32 + 1;
-  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) comp[i] = 0;
+// Block b owns the 8192 numbers [8192 b, 8192 (b + 1)): it crosses off odd
+// multiples of the primes up to sqrt(n) in a shared-memory bitmap (one warp
+// per prime, lanes on consecutive multiples), publishes its survivor count,
+// sums its predecessors' counts (all blocks publish without waiting, so
+// there is no chain) and writes its primes at that offset.  Counts are tagged
+// with the call's epoch, so the scratch words never need clearing.
+constexpr uint32_t kBaseBlockWords = 256;  // 8192 numbers per block, one word per thread
+
+__global__ void __launch_bounds__(kBaseBlockWords) small_base_kernel(
+    uint32_t n, uint32_t* out_p, unsigned long long* out_m, double* out_inv,
+    uint32_t* out_count, unsigned long long* scratch, uint32_t epoch) {
+  __shared__ uint32_t comp[kBaseBlockWords];
+  __shared__ uint32_t wsum[kBaseBlockWords / 32];
+  __shared__ uint32_t s_prefix;
+  const uint32_t b = blockIdx.x, t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+  const uint32_t lo = b * 32u * kBaseBlockWords;
+  const uint32_t hi = min(lo + 32u * kBaseBlockWords, n + 1);  // numbers [lo, hi)
+  comp[t] = 0;
   __syncthreads();
-  // the primes up to sqrt(n) cross off their odd multiples from q*q
-  // concurrently (no barrier per prime)
 #pragma unroll 1
-  for (uint32_t k = 0; k < kTinyPrimeCount; ++k) {
+  for (uint32_t k = warp; k < kTinyPrimeCount; k += kBaseBlockWords / 32) {
     const uint32_t q = kTinyPrimes[k];
     if (q * q > n) break;
-    for (uint32_t j = q * q + threadIdx.x * 2 * q; j <= n; j += blockDim.x * 2 * q)
-      atomicOr(&comp[j >> 5], 1u << (j & 31));
+    uint32_t j = (lo + q - 1) / q * q;  // first multiple >= lo, made odd, at least q*q
+    if (!(j & 1u)) j += q;
+    j = max(j, q * q);
+    for (j += 2 * q * lane; j < hi; j += 64 * q) atomicOr(&comp[(j - lo) >> 5], 1u << (j & 31u));
   }
   __syncthreads();
-  // ordered compaction: thread t owns words [t * wpt, (t + 1) * wpt)
-  const uint32_t wpt = (words + blockDim.x - 1) / blockDim.x;
-  const uint32_t w0 = min(words, threadIdx.x * wpt), w1 = min(words, w0 + wpt);
-  auto survivors = [&](uint32_t w) {
+  const uint32_t w = lo / 32 + t;  // global word of this thread
+  uint32_t v = 0;
+  if (32 * w <= n) {
     const uint32_t ph = w % 3;
-    uint32_t v = ~comp[w] & (ph == 0 ? kWheelMask0 : ph == 1 ? kWheelMask1 : kWheelMask2);
-    if (w == 1) v &= ~((1u << (kFirstTablePrime - 32)) - 1);  // x >= 53
+    v = ~comp[t] & (ph == 0 ? kWheelMask0 : ph == 1 ? kWheelMask1 : kWheelMask2);
     if (w == 0) v = 0;
-    if (w == words - 1 && (n & 31) != 31) v &= (2u << (n & 31)) - 1;  // x <= n
-    return v;
-  };
-  uint32_t c = 0;
-  for (uint32_t w = w0; w < w1; ++w) c += __popc(survivors(w));
-  scan[threadIdx.x] = c;
-  __syncthreads();
-  for (uint32_t o = 1; o < blockDim.x; o <<= 1) {
-    const uint32_t u = threadIdx.x >= o ? scan[threadIdx.x - o] : 0u;
-    __syncthreads();
-    scan[threadIdx.x] += u;
-    __syncthreads();
+    if (w == 1) v &= ~((1u << (kFirstTablePrime - 32)) - 1);  // x >= 53
+    if (w == n / 32) v &= (2u << (n & 31)) - 1;              // x <= n
   }
-  uint32_t pos = scan[threadIdx.x] - c;
-  for (uint32_t w = w0; w < w1; ++w)
-    for (uint32_t v = survivors(w); v; v &= v - 1) {
-      const uint32_t x = 32 * w + __ffs(v) - 1;
-      out_p[pos] = x;
-      out_m[pos] = ~0ull / x;
-      out_inv[pos] = 1.0 / static_cast<double>(x);
-      ++pos;
+  const uint32_t c = __popc(v);
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += u;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t ws = lane < kBaseBlockWords / 32 ? wsum[lane] : 0u;
+    uint32_t wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= static_cast<uint32_t>(o)) wi += u;
     }
-  if (threadIdx.x == blockDim.x - 1) *out_count = scan[threadIdx.x];
+    const uint32_t total = __shfl_sync(0xffffffffu, wi, 31);
+    if (lane < kBaseBlockWords / 32) wsum[lane] = wi - ws;  // exclusive warp offsets
+    if (lane == 0)
+      st_release(scratch + b, (static_cast<unsigned long long>(epoch) << 32) | total);
+    // predecessors' counts (at most 32 blocks precede: n <= 2^18)
+    uint32_t pc = 0;
+    if (lane < b) {
+      unsigned long long x;
+      do {
+        x = ld_acquire(scratch + lane);
+      } while (static_cast<uint32_t>(x >> 32) != epoch);
+      pc = static_cast<uint32_t>(x);
+    }
+    pc = __reduce_add_sync(0xffffffffu, pc);
+    if (lane == 0) {
+      s_prefix = pc;
+      if (b == gridDim.x - 1) *out_count = pc + total;
+    }
+  }
+  __syncthreads();
+  uint32_t pos = s_prefix + wsum[warp] + incl - c;
+  for (; v; v &= v - 1) {
+    const uint32_t x = 32 * w + __ffs(v) - 1;
+    out_p[pos] = x;
+    out_m[pos] = ~0ull / x;
+    out_inv[pos] = 1.0 / static_cast<double>(x);
+    ++pos;
+  }
 }
 
 __global__ void prepare_table_kernel(const unsigned long long* vals, uint64_t skip,
@@ -1219,9 +1252,13 @@ cudaError_t launch_append_table(const unsigned long long* vals, const unsigned l
   return cudaGetLastError();
 }
 
-cudaError_t launch_tiny_primes(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
-                               double* out_inv, uint32_t* out_count, cudaStream_t st) {
-  tiny_primes_kernel<<<1, 1024, 0, st>>>(n, out_p, out_m, out_inv, out_count);
+cudaError_t launch_small_base(uint32_t n, uint32_t* out_p, unsigned long long* out_m,
+                              double* out_inv, uint32_t* out_count, unsigned long long* scratch,
+                              uint32_t epoch, cudaStream_t st) {
+  if (n > kTinyMax || epoch == 0) return cudaErrorInvalidValue;
+  const uint32_t grid = n / (32 * kBaseBlockWords) + 1;
+  small_base_kernel<<<grid, kBaseBlockWords, 0, st>>>(n, out_p, out_m, out_inv, out_count,
+                                                      scratch, epoch);
   return cudaGetLastError();
 }
 
