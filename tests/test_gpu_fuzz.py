@@ -167,3 +167,33 @@ def test_concurrent_contexts_in_threads():
         t.join()
     assert not errs, errs
     assert got == want
+
+
+def test_repeated_calls_reuse_launch_state(port):
+    """Launch state that kernels reset themselves (segment tickets: the last
+    CTA out zeroes them) and epoch-tagged small-base counts stay consistent
+    over many back-to-back calls whose grids, windows, job counts and base
+    builds differ from call to call."""
+    rng = np.random.default_rng(77)
+    cases = [(0, 10**6 + 1), (10**9, 10**9 + 3 * 10**7), (10**15, 10**15 + 10**8),
+             (2**40, 2**40 + 5 * 10**6), (12345, 12346 + 6 * 2**18 * 7), (10**12 - 7, 10**12 + 10**7)]
+    want = {}
+    for L, R in cases:
+        r = port.range(L, R)
+        want[(L, R)] = (r["count"], r["sum"], r["xor"], r["largest"])
+    Ls = np.array([2**33 + 977 * k for k in range(37)], np.uint64)
+    ic, isum, ixor = port.intervals(Ls, 10**5)
+    with ws.Sieve() as s:
+        for it in range(60):
+            L, R = cases[int(rng.integers(len(cases)))]
+            fresh = bool(rng.integers(2))
+            if it % 5 == 4:
+                c, sm, x = s.count_intervals(Ls, 10**5, fresh_base=fresh)
+                assert [int(v) for v in c] == [int(v) for v in ic], it
+                assert [int(v) for v in sm] == [int(v) for v in isum], it
+            elif it % 3 == 0 and R - L <= 3 * 10**7:
+                v, n, c = s.enumerate_range(L, R, fresh_base=fresh)
+                assert (n, c.sum, c.xor) == want[(L, R)][:3], (it, L, R)
+            else:
+                c = s.count_range(L, R, checks=True, fresh_base=fresh)
+                assert _t(c) == want[(L, R)], (it, L, R, fresh)
