@@ -708,12 +708,15 @@ ws_status guarded(ws_ctx* c, F&& f) {
   } catch (const Fail& e) {
     c->err = e.msg;
     cudaGetLastError();
+    c->ticket_zeroed = nullptr;  // a failed call may leave launch state behind: re-zero
     return e.code;
   } catch (const std::bad_alloc&) {
     c->err = "host allocation failed";
+    c->ticket_zeroed = nullptr;
     return WS_OUT_OF_MEMORY;
   } catch (...) {
     c->err = "unknown failure";
+    c->ticket_zeroed = nullptr;
     return WS_CUDA;
   }
   c->timing.total_ms = t.ms();
