@@ -183,6 +183,10 @@ struct ws_ctx {
   size_t bucket_budget = 1ull << 30;  // bytes of bucket lists per window
   uint32_t cap_override = 0;           // test knob (WHEELSIEVE_BUCKET_CAP)
   uint32_t piece_override = 0;         // tuning knob (WHEELSIEVE_FILL_PIECE)
+  bool fill_huge = true;               // carried-offset fill for p >= run length (WHEELSIEVE_FILL_HUGE)
+  uint32_t huge_step = 1;              // runs per histogram step there (WHEELSIEVE_HUGE_STEP)
+  uint64_t huge_thr = 0;               // the run length in slots the count below is for
+  uint32_t n_below_huge = 0;           // table primes (>= 53) below huge_thr
   uint32_t bucket_min_ratio = 8;       // buckets iff largest base prime >= ratio * S
   uint32_t bucket_ctas_per_sm = 0;     // tuning knob (WHEELSIEVE_BUCKET_CTAS)
   uint32_t ctas_per_sm = 0;            // tuning knob, all launches (WHEELSIEVE_CTAS_PER_SM)
@@ -338,6 +342,22 @@ double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
 // The segment kernel over every segment of ctx->h_jobs.  Without large
 // primes this is one launch; otherwise the segments are processed in windows
 // of W segments: bucket_fill (large-prime hit lists) then the sieve kernel.
+// Table primes (>= 53) below x, by a host sieve; cached per context (x is the
+// fill's run length in slots, 2^23 at the default 32 x 2^18).
+uint32_t table_primes_below(ws_ctx* c, uint64_t x) {
+  if (c->huge_thr == x) return c->n_below_huge;
+  std::vector<uint8_t> comp(x, 0);
+  uint32_t n = 0;
+  for (uint64_t i = 2; i < x; ++i) {
+    if (comp[i]) continue;
+    if (i >= wsk::kFirstTablePrime) ++n;
+    for (uint64_t j = i * i; j < x; j += i) comp[j] = 1;
+  }
+  c->huge_thr = x;
+  c->n_below_huge = n;
+  return n;
+}
+
 // Order the main stream after a pending small base build (bstream).
 void join_base(ws_ctx* c) {
   if (!c->base_pending) return;
@@ -488,6 +508,11 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   if (record_start) ck(cudaEventRecord(c->ev[2], c->stream), "event");
   ck(cudaEventRecord(c->ev_order, c->stream), "event");
   if (buckets) ck(cudaStreamWaitEvent(c->fstream, c->ev_order, 0), "fill wait");
+  // primes of at least the run length take the carried-offset fill when every
+  // run is a piece of the one job (consecutive in wheel slots)
+  uint32_t huge_begin = c->nprimes;
+  if (buckets && c->fill_huge && nj == 1 && c->base_B >= piece * c->S)
+    huge_begin = std::max(p.n_mid, table_primes_below(c, piece * c->S));
   for (uint64_t w = 0; w < nwin; ++w) {
     const uint64_t ws = w * W, we = std::min(nseg, ws + W);
     const int b = static_cast<int>(w & 1);
@@ -509,6 +534,25 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
       f.bcount = c->bcount[b].ptr;
       f.bcap = cap;
       f.max_run_segs = static_cast<uint32_t>(piece);
+      if (huge_begin < c->nprimes) {
+        // p >= run length: at most one hit per class per run; offsets are
+        // carried across runs (bucket_fill_huge_kernel)
+        wsk::FillParams fh = f;
+        fh.p_begin = huge_begin;
+        f.p_end = huge_begin;
+        const uint32_t nbx = (c->nprimes - huge_begin + wsk::kFillPrimesPerBlock - 1) /
+                             wsk::kFillPrimesPerBlock;
+        // enough block rows to cover the GPU ~12 blocks per SM, and a group
+        // span below 2^31 slots
+        const uint32_t rows = std::max<uint32_t>(1, (12u * c->sms + nbx - 1) / nbx);
+        uint32_t g = (fh.nruns + rows - 1) / rows;
+        g = std::max<uint32_t>(1, std::min<uint32_t>(g, ((1u << 31) - 1) / (piece * c->S)));
+        fh.group_runs = g;
+        fh.huge_step = c->huge_step;
+        fh.max_run_segs = static_cast<uint32_t>(piece) * c->huge_step;
+        ck(wsk::launch_bucket_fill_huge(fh, c->fstream), "bucket fill (huge primes)");
+        c->timing.launches += 1;
+      }
       ck(wsk::launch_bucket_fill(f, c->fstream), "bucket fill");
       ck(cudaEventRecord(c->fill_done[b], c->fstream), "event");
       ck(cudaStreamWaitEvent(c->stream, c->fill_done[b], 0), "sieve wait");
@@ -1011,6 +1055,9 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CAP")) c->cap_override = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_BUDGET")) c->bucket_budget = std::strtoull(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_FILL_PIECE")) c->piece_override = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_FILL_HUGE")) c->fill_huge = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_HUGE_STEP"))
+    c->huge_step = std::max<uint32_t>(1, std::min<uint32_t>(64, std::strtoul(e, nullptr, 10)));
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_RATIO")) c->bucket_min_ratio = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_CTAS")) c->bucket_ctas_per_sm = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_CTAS_PER_SM")) c->ctas_per_sm = std::strtoul(e, nullptr, 10);

@@ -111,12 +111,18 @@ struct FillParams {
   uint32_t* bcount;
   uint32_t bcap;
   uint32_t max_run_segs;    // histogram size (dynamic shared memory)
+  uint32_t group_runs;      // bucket_fill_huge_kernel: consecutive runs per block row
+  uint32_t huge_step;       // ... and runs per histogram step (max_run_segs covers them)
 };
 constexpr int kFillThreads = 256;
 constexpr int kFillPrimesPerThread = 16;
 constexpr int kFillPrimesPerBlock = kFillThreads * kFillPrimesPerThread;
 constexpr uint32_t kMaxWindow = 2048;  // segments per window (<= fill histogram size)
 cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st);
+// Primes of at least the run length (at most one hit per class per run) over
+// runs that are consecutive pieces of one job: first hits computed once per
+// group of runs and carried from run to run in shared memory.
+cudaError_t launch_bucket_fill_huge(const FillParams& f, cudaStream_t st);
 
 // Appends the enumerated primes vals[0, min(*n_dev, cap)) to a table of
 // *old_n_dev entries and sets *out_n (device-side BasePrimeStore::extend).

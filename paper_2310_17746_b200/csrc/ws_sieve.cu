@@ -1013,6 +1013,96 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
 }
 
 // ---------------------------------------------------------------------------
+// Bucket fill for primes p >= the run length (runs of 32 segments: p >= 32 S),
+// which hit a run at most once per class.  bucket_fill_kernel would redo the
+// per-(prime, run) setup -- loads, first-hit arithmetic, two passes of loop
+// control -- for ~1 hit; here blockIdx.y takes F.group_runs consecutive runs
+// of one job, the first hits are computed once at the group's start, kept in
+// shared memory and advanced by p after each hit.  Per run: a histogram pass,
+// one reservation per segment, a write pass -- the same per-run write locality
+// as bucket_fill_kernel.
+__global__ void __launch_bounds__(kFillThreads) bucket_fill_huge_kernel(const FillParams F) {
+  extern __shared__ uint32_t fill_smem[];
+  uint32_t* hist = fill_smem;                       // max_run_segs counters
+  uint32_t* next1 = fill_smem + F.max_run_segs;     // per prime: next hit (group-relative)
+  uint32_t* next5 = next1 + kFillPrimesPerBlock;    // UINT32_MAX = none in this group
+  const uint32_t r_begin = blockIdx.y * F.group_runs;
+  const uint32_t r_end = min(F.nruns, r_begin + F.group_runs);
+  const uint64_t g_lo = F.runs[r_begin].k_lo, g_hi = F.runs[r_end - 1].k_hi;
+  const uint32_t S = 1u << F.log2S;
+  const uint32_t t_lo = isqrt64(6 * g_lo), t_hi = isqrt64(6 * g_hi);
+  const ModCtx mc = mod_ctx(g_lo);
+  const uint32_t gspan = static_cast<uint32_t>(g_hi - g_lo);  // < 2^31 (host bound)
+  const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
+  const uint32_t p_end = F.nprimes_dev ? min(F.p_end, *F.nprimes_dev) : F.p_end;
+  uint32_t pp[kFillPrimesPerThread];  // the thread's primes stay in registers
+#pragma unroll
+  for (int j = 0; j < kFillPrimesPerThread; ++j) {
+    const uint32_t li = j * kFillThreads + threadIdx.x;
+    const uint32_t i = first + li;
+    uint32_t r1 = 0xFFFFFFFFu, r5 = 0xFFFFFFFFu;
+    pp[j] = 0;
+    if (i < p_end) {
+      pp[j] = __ldg(F.prime_p + i);
+      uint32_t q1, q5;
+      if (prime_offsets(pp[j], __ldg(F.prime_inv + i), i, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
+        if (q1 < gspan) r1 = q1;
+        if (q5 < gspan) r5 = q5;
+      }
+    }
+    next1[li] = r1;
+    next5[li] = r5;
+  }
+  // F.huge_step consecutive runs at a time (one histogram over their
+  // segments): at most huge_step hits per class per step
+#pragma unroll 1
+  for (uint32_t r = r_begin; r < r_end; r += F.huge_step) {
+    const uint32_t r2 = min(r_end, r + F.huge_step) - 1;
+    Run run = F.runs[r];
+    run.k_hi = F.runs[r2].k_hi;
+    run.nseg = F.runs[r2].seg0 + F.runs[r2].nseg - run.seg0;
+    const uint32_t lo = static_cast<uint32_t>(run.k_lo - g_lo);
+    const uint32_t hi = static_cast<uint32_t>(run.k_hi - g_lo);
+    for (uint32_t k = threadIdx.x; k < run.nseg; k += kFillThreads) hist[k] = 0;
+    __syncthreads();  // also orders the previous step's reservations
+#pragma unroll
+    for (int j = 0; j < kFillPrimesPerThread; ++j) {
+      const uint32_t li = j * kFillThreads + threadIdx.x;
+      // h < hi < 2^31 and p < 2^32: the 64-bit step cannot wrap
+      for (uint64_t h = next1[li]; h < hi; h += pp[j]) atomicAdd(hist + ((h - lo) >> F.log2S), 1u);
+      for (uint64_t h = next5[li]; h < hi; h += pp[j]) atomicAdd(hist + ((h - lo) >> F.log2S), 1u);
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < run.nseg; k += kFillThreads) {
+      const uint32_t c = hist[k];
+      hist[k] = (run.seg0 + k) * F.bcap + (c ? atomicAdd(F.bcount + run.seg0 + k, c) : 0u);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kFillPrimesPerThread; ++j) {
+      const uint32_t li = j * kFillThreads + threadIdx.x;
+#pragma unroll
+      for (int cls = 0; cls < 2; ++cls) {
+        uint32_t* slot = (cls ? next5 : next1) + li;
+        uint32_t h = *slot;
+        if (h < hi) {
+          do {
+            const uint32_t seg = (h - lo) >> F.log2S;
+            const uint32_t idx = atomicAdd(hist + seg, 1u);
+            if (idx < (run.seg0 + seg + 1) * F.bcap)
+              F.bucket[idx] = ((h - lo) & (S - 1)) | (cls ? S : 0u);
+            const uint32_t n = h + pp[j];  // next hit, or none in this group
+            h = n >= h && n < gspan ? n : 0xFFFFFFFFu;
+          } while (h < hi);
+          *slot = h;
+        }
+      }
+    }
+    __syncthreads();  // hist is reset for the next run
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Small base tables: a dense sieve of [0, n] (n <= kTinyMax = 2^18) writing
 // the primes >= 53 in ascending order with their Barrett constants
 // (naive_sieve, wheel.cpp:40-54).  Used as level 0 of the two-level base build
@@ -1184,6 +1274,16 @@ cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t 
     case kEnumerate: sieve_kernel<kEnumerate><<<grid, kThreads, smem, st>>>(p); break;
     default: sieve_kernel<kEnumWire><<<grid, kThreads, smem, st>>>(p); break;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_fill_huge(const FillParams& f, cudaStream_t st) {
+  const uint32_t per_block = kFillThreads * kFillPrimesPerThread;
+  const uint32_t nb = f.p_end > f.p_begin ? (f.p_end - f.p_begin + per_block - 1) / per_block : 0;
+  if (nb == 0 || f.nruns == 0 || f.group_runs == 0) return cudaSuccess;
+  dim3 grid(nb, (f.nruns + f.group_runs - 1) / f.group_runs);
+  const size_t smem = (f.max_run_segs + 2 * kFillPrimesPerBlock) * sizeof(uint32_t);
+  bucket_fill_huge_kernel<<<grid, kFillThreads, smem, st>>>(f);
   return cudaGetLastError();
 }
 

@@ -77,7 +77,13 @@ print("ok")
                                   "WHEELSIEVE_FILL_PIECE": "7",
                                   "WHEELSIEVE_BUCKET_BUDGET": str(3 << 20)},
                                  {"WHEELSIEVE_BUCKET_RATIO": "1", "WHEELSIEVE_BUCKET_CAP": "100",
-                                  "WHEELSIEVE_BUCKET_CTAS": "1"}])
+                                  "WHEELSIEVE_BUCKET_CTAS": "1"},
+                                 # the carried-offset fill for p >= run length: off, and
+                                 # with short runs taken three at a time
+                                 {"WHEELSIEVE_BUCKET_RATIO": "1", "WHEELSIEVE_FILL_HUGE": "0"},
+                                 {"WHEELSIEVE_BUCKET_RATIO": "1", "WHEELSIEVE_FILL_PIECE": "5",
+                                  "WHEELSIEVE_HUGE_STEP": "3",
+                                  "WHEELSIEVE_BUCKET_BUDGET": str(5 << 20)}])
 def test_fuzz_bucket_policies(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", BUCKET_FUZZ], cwd=ROOT, env=e, capture_output=True,
