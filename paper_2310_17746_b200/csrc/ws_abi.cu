@@ -185,6 +185,7 @@ struct ws_ctx {
   uint32_t piece_override = 0;         // tuning knob (WHEELSIEVE_FILL_PIECE)
   bool fill_huge = true;               // carried-offset fill for p >= run length (WHEELSIEVE_FILL_HUGE)
   uint32_t huge_step = 1;              // runs per histogram step there (WHEELSIEVE_HUGE_STEP)
+  uint32_t huge_from = 0;              // its lower bound in units of S (0: the run length)
   uint64_t huge_thr = 0;               // the run length in slots the count below is for
   uint32_t n_below_huge = 0;           // table primes (>= 53) below huge_thr
   uint32_t bucket_min_ratio = 8;       // buckets iff largest base prime >= ratio * S
@@ -511,8 +512,9 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   // primes of at least the run length take the carried-offset fill when every
   // run is a piece of the one job (consecutive in wheel slots)
   uint32_t huge_begin = c->nprimes;
-  if (buckets && c->fill_huge && nj == 1 && c->base_B >= piece * c->S)
-    huge_begin = std::max(p.n_mid, table_primes_below(c, piece * c->S));
+  const uint64_t huge_from = (c->huge_from ? c->huge_from : piece) * c->S;
+  if (buckets && c->fill_huge && nj == 1 && c->base_B >= huge_from)
+    huge_begin = std::max(p.n_mid, table_primes_below(c, huge_from));
   for (uint64_t w = 0; w < nwin; ++w) {
     const uint64_t ws = w * W, we = std::min(nseg, ws + W);
     const int b = static_cast<int>(w & 1);
@@ -1056,6 +1058,7 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_BUDGET")) c->bucket_budget = std::strtoull(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_FILL_PIECE")) c->piece_override = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_FILL_HUGE")) c->fill_huge = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_HUGE_FROM")) c->huge_from = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_HUGE_STEP"))
     c->huge_step = std::max<uint32_t>(1, std::min<uint32_t>(64, std::strtoul(e, nullptr, 10)));
   if (const char* e = std::getenv("WHEELSIEVE_BUCKET_RATIO")) c->bucket_min_ratio = std::strtoul(e, nullptr, 10);
