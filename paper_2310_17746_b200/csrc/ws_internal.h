@@ -117,7 +117,7 @@ struct FillParams {
 constexpr int kFillThreads = 256;
 constexpr int kFillPrimesPerThread = 16;
 constexpr int kFillPrimesPerBlock = kFillThreads * kFillPrimesPerThread;
-constexpr uint32_t kMaxWindow = 2048;  // segments per window (<= fill histogram size)
+constexpr uint32_t kMaxWindow = 16384;  // segments per window (run spans stay below 2^32 slots)
 cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st);
 // Primes of at least the run length (at most one hit per class per run) over
 // runs that are consecutive pieces of one job: first hits computed once per
