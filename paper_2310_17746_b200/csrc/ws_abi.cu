@@ -202,7 +202,7 @@ struct ws_ctx {
   // small base builds (B <= 2^18) run on their own stream, overlapping the call's
   // uploads and resets; the first launch that reads the table joins it
   cudaStream_t bstream = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_base = nullptr;
+  cudaEvent_t ev_fork = nullptr;
   bool base_pending = false;
   DevBuf<unsigned long long> base_scratch;  // small_base_kernel's epoch-tagged block counts
   uint32_t base_epoch = 0;
@@ -264,7 +264,6 @@ struct ws_ctx {
     if (bstream) cudaStreamDestroy(bstream);
     base_scratch.release();
     if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_base) cudaEventDestroy(ev_base);
     if (cstream) cudaStreamDestroy(cstream);
     if (ev_order) cudaEventDestroy(ev_order);
     for (cudaEvent_t e : chunk_done)
@@ -365,7 +364,7 @@ uint32_t table_primes_below(ws_ctx* c, uint64_t x) {
 // Order the main stream after a pending small base build (bstream).
 void join_base(ws_ctx* c) {
   if (!c->base_pending) return;
-  ck(cudaStreamWaitEvent(c->stream, c->ev_base, 0), "base join");
+  ck(cudaStreamWaitEvent(c->stream, c->ev[1], 0), "base join");
   c->base_pending = false;
 }
 
@@ -510,8 +509,10 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   // ev[2] (call start) / ev[4] order the fill stream after everything queued so far
   join_base(c);
   if (record_start) ck(cudaEventRecord(c->ev[2], c->stream), "event");
-  ck(cudaEventRecord(c->ev_order, c->stream), "event");
-  if (buckets) ck(cudaStreamWaitEvent(c->fstream, c->ev_order, 0), "fill wait");
+  if (buckets) {
+    ck(cudaEventRecord(c->ev_order, c->stream), "event");
+    ck(cudaStreamWaitEvent(c->fstream, c->ev_order, 0), "fill wait");
+  }
   // primes of at least the run length take the carried-offset fill when every
   // run is a piece of the one job (consecutive in wheel slots)
   uint32_t huge_begin = c->nprimes;
@@ -641,9 +642,9 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
       static_cast<uint64_t>(c->nprimes) + prime_count_bound(c->base_B + 1, B + 1) < 0xFFFFFFFFull)
     return extend_base(c, B);
   c->base_built = true;
-  ck(cudaEventRecord(c->ev[0], c->stream), "event");
   c->base_valid = false;
   if (B < wsk::kFirstTablePrime) {
+    ck(cudaEventRecord(c->ev[0], c->stream), "event");
     c->nprimes = 0;
     c->nprimes_dev = nullptr;
     c->base_B = B;
@@ -652,20 +653,21 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
     return;
   }
   if (B > 0xFFFFFFFFull) throw Fail{WS_OVERFLOW, "base bound exceeds 2^32"};
+  if (B > wsk::kTinyMax) ck(cudaEventRecord(c->ev[0], c->stream), "event");
   if (B <= wsk::kTinyMax) {  // the whole table from one small_base launch, on bstream
     const uint64_t cap = prime_count_bound(0, B + 1);
     c->tab_p.reserve(cap, "base table");
     c->tab_m.reserve(cap, "base table");
     c->tab_inv.reserve(cap, "base table");
     c->d_tabn.reserve(1, "table size");
-    // after everything queued so far (earlier launches read the old table)
+    // after everything queued so far (earlier launches read the old table);
+    // ev[1] (the build's end, for base_ms) is also what the first reader joins
     ck(cudaEventRecord(c->ev_fork, c->stream), "event");
     ck(cudaStreamWaitEvent(c->bstream, c->ev_fork, 0), "base fork");
     ck(cudaEventRecord(c->ev[0], c->bstream), "event");
     ck(launch_small_base(c, static_cast<uint32_t>(B), c->tab_p.ptr, c->tab_m.ptr, c->tab_inv.ptr,
                          c->d_tabn.ptr, c->bstream), "small base");
     ck(cudaEventRecord(c->ev[1], c->bstream), "event");
-    ck(cudaEventRecord(c->ev_base, c->bstream), "event");
     c->base_pending = true;
     c->timing.launches += 1;
     const uint64_t skip = small_primes_upto(B);
@@ -1089,7 +1091,6 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   bool ok = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->bstream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-            cudaEventCreateWithFlags(&c->ev_base, cudaEventDisableTiming) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) == cudaSuccess;
   for (int i = 0; i < ws_ctx::kMaxChunks && ok; ++i)
