@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -345,16 +346,29 @@ double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
 // The segment kernel over every segment of ctx->h_jobs.  Without large
 // primes this is one launch; otherwise the segments are processed in windows
 // of W segments: bucket_fill (large-prime hit lists) then the sieve kernel.
-// Table primes (>= 53) below x, by a host sieve; cached per context (x is the
-// fill's run length in slots, 2^23 at the default 32 x 2^18).
+// Table primes (>= 53) below x, by an odd-only host sieve; cached per context
+// and per process (x is the fill's run length in slots, 2^23 at the default
+// 32 x 2^18, so the sieve runs once).
 uint32_t table_primes_below(ws_ctx* c, uint64_t x) {
   if (c->huge_thr == x) return c->n_below_huge;
-  std::vector<uint8_t> comp(x, 0);
+  static std::mutex mu;
+  static std::vector<std::pair<uint64_t, uint32_t>> memo;
   uint32_t n = 0;
-  for (uint64_t i = 2; i < x; ++i) {
-    if (comp[i]) continue;
-    if (i >= wsk::kFirstTablePrime) ++n;
-    for (uint64_t j = i * i; j < x; j += i) comp[j] = 1;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    bool found = false;
+    for (const auto& e : memo)
+      if (e.first == x) n = e.second, found = true;
+    if (!found) {
+      std::vector<uint8_t> comp(x / 2 + 1, 0);  // comp[i] <-> 2i + 1
+      for (uint64_t i = 1; 2 * i + 1 < x; ++i) {
+        if (comp[i]) continue;
+        const uint64_t q = 2 * i + 1;
+        if (q >= wsk::kFirstTablePrime) ++n;
+        for (uint64_t j = q * q; j < x; j += 2 * q) comp[j / 2] = 1;
+      }
+      memo.emplace_back(x, n);
+    }
   }
   c->huge_thr = x;
   c->n_below_huge = n;
