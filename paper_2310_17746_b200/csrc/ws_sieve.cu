@@ -818,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
         // (small values) take a few.  The stage holds positions 64*lane + b
         // (bit b of the interleaved masks); a survivor's value offset from
         // rbase is 192*lane + 3b + 1 + (b & 1) < 6144.
-        const uint32_t eb = lane << 6;
+        const uint32_t eb = lane << 6, ob = 192u * lane;
         // the round's values share rbase's high word unless its low word is
         // within 6144 of wrapping (once in ~7e5 rounds): 32-bit arithmetic
         const uint32_t rlo = static_cast<uint32_t>(rbase);
@@ -827,20 +827,27 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
 #pragma unroll 1
         for (uint32_t wlo = 0; wlo < rtotal; wlo += kStage) {
           const uint32_t wn = min(kStage, rtotal - wlo);
+          // stage entry of interleaved bit position t (0..63) of this lane:
+          // the wire byte source (64 * lane + t) for the wire, else the value
+          // offset from rbase, 192 * lane + 3t + 1 + (t & 1) < 6144
+          auto enc = [&](uint32_t t) -> uint16_t {
+            if (kWire) return static_cast<uint16_t>(eb | t);
+            return static_cast<uint16_t>(ob + 3u * t + 1u + (t & 1u));
+          };
           if (rtotal <= kStage) {  // one window (warp-uniform): no position test
             uint16_t* sp = stage + (incl - c);
 #pragma unroll 1
-            for (uint32_t x = lo; x; x &= x - 1) *sp++ = static_cast<uint16_t>(eb | (__ffs(x) - 1));
+            for (uint32_t x = lo; x; x &= x - 1) *sp++ = enc(__ffs(x) - 1);
 #pragma unroll 1
-            for (uint32_t x = hi; x; x &= x - 1) *sp++ = static_cast<uint16_t>(eb | 31u + __ffs(x));
+            for (uint32_t x = hi; x; x &= x - 1) *sp++ = enc(31u + __ffs(x));
           } else if (incl > wlo && incl - c < wlo + wn) {  // lane has entries in the window
             uint32_t q = incl - c - wlo;  // window-relative position (wraps below 0)
 #pragma unroll 1
             for (uint32_t x = lo; x; x &= x - 1, ++q)
-              if (q < wn) stage[q] = static_cast<uint16_t>(eb | (__ffs(x) - 1));
+              if (q < wn) stage[q] = enc(__ffs(x) - 1);
 #pragma unroll 1
             for (uint32_t x = hi; x; x &= x - 1, ++q)
-              if (q < wn) stage[q] = static_cast<uint16_t>(eb | 31u + __ffs(x));
+              if (q < wn) stage[q] = enc(31u + __ffs(x));
           }
           __syncwarp();
           const unsigned long long wpos = pos + wlo;
@@ -865,9 +872,7 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
             uint32_t xlo = 0;
 #pragma unroll 4
             for (uint32_t i = lane; i < wn; i += 32) {
-              const uint32_t e = stage[i];
-              const uint32_t bb = e & 63u;
-              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+              const uint32_t off = stage[i];
               const uint32_t vlo = rlo + off;
               dst[i] = make_uint2(vlo, rhi);
               soff += off;
@@ -877,9 +882,7 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
           } else {
             unsigned long long* dst = P.out + wpos;
             for (uint32_t i = lane; i < wn; i += 32) {
-              const uint32_t e = stage[i];
-              const uint32_t bb = e & 63u;
-              const uint32_t off = 192u * (e >> 6) + 3u * bb + 1u + (bb & 1u);
+              const uint32_t off = stage[i];
               const unsigned long long v = rbase + off;
               if (seg_fits || wpos + i < P.out_cap) dst[i] = v;
               soff += off;
