@@ -34,6 +34,12 @@
 //                   prefix sums + a decoupled look-back across segments for
 //                   the global output offset, then coalesced uint64 stores
 //                   (or the 8-bit host wire format, ws_wire.cpp).
+//
+// Other kernels here: bucket_fill_kernel (large-prime hit lists per window,
+// one launch per window) and bucket_fill_huge_kernel (primes of at least the
+// run length, first hits carried across runs); small_base_kernel (base tables
+// up to 2^18 in one launch); prepare/append_table_kernel (table entries from
+// enumerated primes); acc/u32_to_host_kernel (results to mapped host memory).
 #include <cstdint>
 #include <type_traits>
 
