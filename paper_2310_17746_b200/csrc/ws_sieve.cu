@@ -945,11 +945,15 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
   const uint32_t span = static_cast<uint32_t>(run.k_hi - run.k_lo);  // <= kMaxWindow * S
   // activation thresholds of the run (see fetch_segment)
   const uint32_t t_lo = isqrt64(6 * run.k_lo), t_hi = isqrt64(6 * run.k_hi);
+  const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
+  const uint32_t p_end = F.nprimes_dev ? min(F.p_end, *F.nprimes_dev) : F.p_end;
+  // primes ascend: a block whose first prime is not active anywhere in the
+  // run (p*p beyond its end) has no hits -- common when the jobs of a window
+  // need different base bounds (c5's intervals)
+  if (first >= p_end || __ldg(F.prime_p + first) > t_hi) return;
   const ModCtx mc = mod_ctx(run.k_lo);
   for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) hist[i] = 0;
   __syncthreads();
-  const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
-  const uint32_t p_end = F.nprimes_dev ? min(F.p_end, *F.nprimes_dev) : F.p_end;
   // pass 1: first hits (Barrett, p*p activation) + per-segment histogram;
   // p and 1/p are loaded one prime ahead (independent of the run)
   uint32_t pn = 0;
