@@ -533,6 +533,11 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   const uint64_t huge_from = (c->huge_from ? c->huge_from : piece) * c->S;
   if (buckets && c->fill_huge && nj == 1 && c->base_B >= huge_from)
     huge_begin = std::max(p.n_mid, table_primes_below(c, huge_from));
+  // with the large-prime fill that heavy (half of a C4 window), two sieve CTAs
+  // per SM leave room for fill blocks to run alongside (C4 53.6 -> 53.1 ms,
+  // C4e 60.6 -> 58.3 ms; multi-job windows such as C5's lose with it)
+  if (huge_begin < c->nprimes && c->bucket_ctas_per_sm == 0)
+    max_grid = std::min<uint64_t>(max_grid, 2ull * c->sms);
   for (uint64_t w = 0; w < nwin; ++w) {
     const uint64_t ws = w * W, we = std::min(nseg, ws + W);
     const int b = static_cast<int>(w & 1);
