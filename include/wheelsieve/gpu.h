@@ -32,7 +32,23 @@
  *   - status codes are 1 + wheelsieve::Errc (errors.hpp:9-23), no exception
  *     ever crosses this ABI; device/runtime failures map to WS_CUDA etc.
  *   - one host thread per context (the engine is not reentrant per run,
- *     SPEC.md:268); a context owns its device buffers and CUDA stream.
+ *     SPEC.md:268); a context owns its device buffers and CUDA streams.
+ *
+ * Multi-GPU (SieveConfig::threads spreads one run() over worker threads,
+ * engine.hpp:13-29 / engine.cpp:179-262; here one call spreads over GPUs):
+ * a context created with ws_opts.n_devices = k >= 1 owns k devices, one
+ * worker thread and one NCCL communicator per device.  With world = W
+ * processes (each with the same k) the job is cut into W * k shards; local
+ * device i of process `rank` is shard (NCCL rank) rank * k + i.  A range
+ * [L, R) is split by ws_partition into contiguous per-shard super-ranges on
+ * segment borders, interval batches go interval i -> shard i mod (W k), and
+ * range batches (ws_count_ranges) in contiguous blocks.  Each device sieves
+ * its shard with no data-path exchange; the per-shard 32-byte records
+ * {count, sum, xor, largest} (per-interval records for batches) are
+ * combined after exactly one ncclAllGather over NVLink (NCCL has no XOR
+ * reduction) with the fold of ws_combine_checks.  Every process receives the
+ * combined totals; per-segment counts and enumerated values stay with the
+ * process that owns the shard (see ws_enumerate_range).
  */
 #ifndef WHEELSIEVE_GPU_H_
 #define WHEELSIEVE_GPU_H_
@@ -62,7 +78,8 @@ typedef enum ws_status {
   /* device side */
   WS_CUDA = 100,     /* a CUDA runtime call or kernel failed */
   WS_NO_DEVICE = 101, /* no usable sm_100 device */
-  WS_OUT_OF_MEMORY = 102
+  WS_OUT_OF_MEMORY = 102,
+  WS_NCCL = 103      /* an NCCL call failed (multi-device contexts) */
 } ws_status;
 
 /* Flags for the range calls. */
@@ -72,12 +89,23 @@ typedef enum ws_status {
 
 typedef struct ws_ctx ws_ctx;
 
+#define WS_MAX_DEVICES 16
+#define WS_NCCL_ID_BYTES 128 /* sizeof(ncclUniqueId) */
+
+/* Version 2 (sizeof(ws_opts)).  Version 1 -- the first 16 bytes, with
+ * n_devices then named `reserved` and required to be 0 -- is still accepted
+ * (struct_size == 16). */
 typedef struct ws_opts {
   uint32_t struct_size;   /* sizeof(ws_opts) */
   uint32_t segment_slots; /* wheel slots per class per segment: power of two in
                              [2^12, 2^18]; default 2^18 (64 KiB of flags) */
-  int32_t device;         /* CUDA device ordinal, -1 = current device */
-  uint32_t reserved;
+  int32_t device;         /* n_devices == 0: CUDA device ordinal, -1 = current device */
+  uint32_t n_devices;     /* 0: single-device context on `device`, no NCCL;
+                             k in [1, WS_MAX_DEVICES]: device_ids[0..k) with NCCL */
+  int32_t device_ids[WS_MAX_DEVICES];
+  uint32_t world;         /* processes sharing each job (0 or 1: this one alone) */
+  uint32_t rank;          /* this process's rank in [0, world) */
+  uint8_t nccl_id[WS_NCCL_ID_BYTES]; /* world > 1: the id ws_nccl_unique_id made on rank 0 */
 } ws_opts;
 
 typedef struct ws_checks {
@@ -106,20 +134,29 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out);
 void ws_ctx_destroy(ws_ctx* ctx);
 /* Message of the last failure on this context ("" if none). */
 const char* ws_last_error(const ws_ctx* ctx);
-/* The cudaStream_t the context launches on (for events / interop). */
+/* The cudaStream_t the context launches on (local device 0's; for events /
+ * interop). */
 void* ws_ctx_stream(ws_ctx* ctx);
 ws_status ws_last_timing(const ws_ctx* ctx, ws_timing* out);
 
 /* Count primes in [L, R).  Replaces run() with a CountSink (engine.hpp:83)
  * for L = 0, and the SURVEY §3.3 composition otherwise.
  * per_seg (nullable, host unless WS_OUT_DEVICE): survivor count per segment,
- * at most per_seg_cap written; *n_seg (nullable) = number of segments. */
+ * at most per_seg_cap written; *n_seg (nullable) = number of segments.
+ * Multi-device contexts: each shard writes its own segments' counts (with
+ * world > 1 only this process's shards are written); *out is the whole range. */
 ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws_checks* out,
                          uint32_t* per_seg, uint64_t per_seg_cap, uint64_t* n_seg);
 
 /* Enumerate the primes of [L, R) in ascending order into out[0 .. *n_out).
  * Replaces run() with a value sink (MemorySink, sink.hpp:55-66).  Σ and ⊕
- * are always computed.  If the primes do not fit in cap, nothing is written
+ * are always computed.  Multi-device contexts count every shard first (the
+ * one collective gives each shard's offset and the totals), then each device
+ * writes its shard at its offset -- host output in parallel pipelines,
+ * device output (any device's memory, UVA) by a device-to-device copy from
+ * devices that do not own `out`.  With world > 1, `out` receives this
+ * process's shards only (*n_out = their count) while *checks holds the
+ * whole range.  If the primes do not fit in cap, nothing is written
  * past cap, *n_out is the full count and WS_CAPACITY is returned.
  * Host output of more than one pipeline chunk (>= 128 segments) crosses PCIe
  * in an 8-bit wire format -- each prime as its bit position in its 128-slot
@@ -130,10 +167,23 @@ ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws
 ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, uint64_t* out,
                              uint64_t cap, uint64_t* n_out, ws_checks* checks);
 
+/* Multi-device contexts: every local device i enumerates its ws_partition
+ * shard of [L, R) into outs[i] (memory of that device, capacity caps[i];
+ * shard 0 starts with 2 and 3 when in range) -- the enumerated arrays stay
+ * on their GPU, in shard order the concatenation is the sorted enumeration.
+ * counts[i] = primes of local shard i; *checks (nullable) = the whole range
+ * after the one allgather.  WS_CAPACITY if a shard exceeds its capacity
+ * (nothing is written past it). */
+ws_status ws_enumerate_shards(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags,
+                              uint64_t* const* outs, const uint64_t* caps, uint64_t* counts,
+                              ws_checks* checks);
+
 /* Count primes in each interval [Ls[i], Ls[i] + width), i < n, each sieved
  * independently (BASELINE config 5).  counts/sums/xors (nullable sums/xors)
  * receive per-interval results; Ls and outputs are host arrays unless
- * WS_OUT_DEVICE. */
+ * WS_OUT_DEVICE (single-device contexts only).  Multi-device contexts sieve
+ * interval i on shard i mod (world * n_devices); every process receives all
+ * n results. */
 ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64_t width,
                              uint32_t flags, uint32_t* counts, uint64_t* sums, uint64_t* xors);
 
@@ -171,6 +221,37 @@ ws_status ws_read_back(const char* dir, uint64_t lo, uint64_t hi, uint64_t* out,
                        uint64_t* n_out);
 /* verify_store (sink.cpp:323-342): every file vs the manifest, global order. */
 ws_status ws_verify_store(const char* dir);
+
+/* Count each range [Ls[i], Rs[i]), i < n, independently (the per-worker-tile
+ * counts of run(), engine.cpp:233-288): out[i] receives count, Σ/⊕ (with
+ * WS_WANT_CHECKS) and the largest prime of range i, 2 and 3 included when in
+ * range.  Empty ranges (R <= L) give zeros.  Host arrays.  Multi-device
+ * contexts split the batch into contiguous blocks of ranges per shard. */
+ws_status ws_count_ranges(ws_ctx* ctx, const uint64_t* Ls, const uint64_t* Rs, uint64_t n,
+                          uint32_t flags, ws_checks* out);
+
+/* ---- multi-device contexts ---------------------------------------------- */
+/* Fills id (WS_NCCL_ID_BYTES) with a fresh ncclUniqueId, on rank 0 of a
+ * multi-process job; the caller broadcasts it to the other ranks' ws_opts. */
+ws_status ws_nccl_unique_id(uint8_t* id);
+/* Local devices of the context (1 for single-device contexts). */
+uint32_t ws_ctx_num_devices(const ws_ctx* ctx);
+/* Shards each job is split into (world * local devices; 1 without NCCL). */
+uint32_t ws_ctx_num_shards(const ws_ctx* ctx);
+/* CUDA ordinal and launch stream of local device i. */
+int32_t ws_ctx_device(const ws_ctx* ctx, uint32_t i);
+void* ws_ctx_device_stream(ws_ctx* ctx, uint32_t i);
+/* Timing of the last call on local device i alone (ws_last_timing reports
+ * the maximum device times and summed counters over the devices). */
+ws_status ws_device_timing(const ws_ctx* ctx, uint32_t i, ws_timing* out);
+/* NCCL communicator of local device i: ranks in the communicator and this
+ * device's rank (WS_BAD_CONFIG for contexts without NCCL). */
+ws_status ws_ctx_comm_info(const ws_ctx* ctx, uint32_t i, int32_t* nranks, int32_t* comm_rank);
+/* The fold applied to the gathered per-shard records: count and Σ add mod
+ * 2^64, ⊕ folds, largest is the maximum.  Pure function: combining the
+ * ws_checks of ws_partition's shards of [L, R) (each counted alone) gives
+ * exactly the ws_checks of [L, R). */
+ws_status ws_combine_checks(const ws_checks* records, uint64_t n, ws_checks* out);
 
 /* Upper bound on the number of primes in [L, R) (capacity helper). */
 uint64_t ws_prime_count_bound(uint64_t L, uint64_t R);

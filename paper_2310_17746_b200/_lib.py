@@ -20,7 +20,9 @@ EXPORTS = (
     "ws_ctx_stream", "ws_last_timing", "ws_count_range", "ws_enumerate_range",
     "ws_count_intervals", "ws_prime_count_bound", "ws_partition", "ws_start_offsets",
     "ws_isqrt", "ws_version", "ws_base_primes", "ws_sieve_segment", "ws_store_range",
-    "ws_read_back", "ws_verify_store",
+    "ws_read_back", "ws_verify_store", "ws_count_ranges", "ws_nccl_unique_id",
+    "ws_ctx_num_devices", "ws_ctx_num_shards", "ws_ctx_device", "ws_ctx_device_stream",
+    "ws_device_timing", "ws_ctx_comm_info", "ws_combine_checks", "ws_enumerate_shards",
 )
 
 WS_WANT_CHECKS = 0x1
@@ -33,9 +35,14 @@ P64 = C.POINTER(C.c_uint64)
 P32 = C.POINTER(C.c_uint32)
 
 
+WS_MAX_DEVICES = 16
+WS_NCCL_ID_BYTES = 128
+
+
 class WsOpts(C.Structure):
     _fields_ = [("struct_size", u32), ("segment_slots", u32), ("device", C.c_int32),
-                ("reserved", u32)]
+                ("n_devices", u32), ("device_ids", C.c_int32 * WS_MAX_DEVICES),
+                ("world", u32), ("rank", u32), ("nccl_id", C.c_uint8 * WS_NCCL_ID_BYTES)]
 
 
 class WsChecks(C.Structure):
@@ -76,6 +83,16 @@ def _load(path: str = LIB_PATH) -> C.CDLL:
         "ws_read_back": (C.c_int, [C.c_char_p, u64, u64, vp, u64, P64]),
         "ws_verify_store": (C.c_int, [C.c_char_p]),
         "ws_version": (C.c_char_p, []),
+        "ws_count_ranges": (C.c_int, [vp, vp, vp, u64, u32, vp]),
+        "ws_nccl_unique_id": (C.c_int, [vp]),
+        "ws_ctx_num_devices": (u32, [vp]),
+        "ws_ctx_num_shards": (u32, [vp]),
+        "ws_ctx_device": (C.c_int32, [vp, u32]),
+        "ws_ctx_device_stream": (vp, [vp, u32]),
+        "ws_device_timing": (C.c_int, [vp, u32, C.POINTER(WsTiming)]),
+        "ws_ctx_comm_info": (C.c_int, [vp, u32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "ws_combine_checks": (C.c_int, [vp, u64, C.POINTER(WsChecks)]),
+        "ws_enumerate_shards": (C.c_int, [vp, u64, u64, u32, vp, vp, vp, C.POINTER(WsChecks)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -27,268 +27,23 @@
 #include <vector>
 
 #include "wheelsieve/gpu.h"
+#include "ws_host.h"
 #include "ws_internal.h"
 #include "ws_wire.h"
 
-namespace {
-
-constexpr uint64_t kMaxWheelIndex = (UINT64_MAX - 5) / 6;       // wheel.hpp:33
-constexpr uint64_t kMaxSegmentEnd = 6 * (kMaxWheelIndex + 1);   // wheel.hpp:37
-
-uint64_t isqrt_u64(uint64_t n) {  // wheel.cpp:25-33 semantics (exact)
-  if (n == 0) return 0;
-  uint64_t r = static_cast<uint64_t>(std::sqrt(static_cast<double>(n)));
-  while (r > 0 && r > n / r) --r;
-  while (r + 1 <= n / (r + 1)) ++r;
-  return r;
-}
-
-struct Fail {
-  ws_status code;
-  std::string msg;
-};
-
-void ck(cudaError_t e, const char* what) {
-  if (e == cudaErrorMemoryAllocation)
-    throw Fail{WS_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e)};
-  if (e != cudaSuccess) throw Fail{WS_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
-}
-
-template <class T>
-struct DevBuf {
-  T* ptr = nullptr;
-  size_t cap = 0;  // elements
-  void reserve(size_t n, const char* what) {
-    if (n <= cap) return;
-    release();
-    ck(cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T)), what);
-    cap = n;
-  }
-  void release() {
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr;
-    cap = 0;
-  }
-  // grow to n elements keeping the first `keep` (stream-ordered copy)
-  void grow(size_t n, size_t keep, cudaStream_t st, const char* what) {
-    if (n <= cap) return;
-    T* q = nullptr;
-    ck(cudaMalloc(&q, n * sizeof(T)), what);
-    if (keep && ptr) {
-      const cudaError_t e = cudaMemcpyAsync(q, ptr, std::min(keep, cap) * sizeof(T),
-                                            cudaMemcpyDeviceToDevice, st);
-      if (e != cudaSuccess) {
-        cudaFree(q);
-        ck(e, what);
-      }
-      ck(cudaStreamSynchronize(st), what);  // the old buffer is freed next
-    }
-    release();
-    ptr = q;
-    cap = n;
-  }
-};
-
-// Growable page-locked host staging (async H2D/D2H without staging copies).
-struct PinnedBuf {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-  void* reserve(size_t n, const char* what) {
-    if (n <= bytes) return ptr;
-    release();
-    ck(cudaMallocHost(&ptr, std::max<size_t>(n, 64)), what);
-    bytes = n;
-    return ptr;
-  }
-  void release() {
-    if (ptr) cudaFreeHost(ptr);
-    ptr = nullptr;
-    bytes = 0;
-  }
-};
-
-// Per-call bump arena of pinned staging for async uploads.  A region is
-// never reused within a call (its copy may still be pending); offsets reset
-// at the start of the next call, which is safe because every call ends with
-// a stream synchronisation.
-struct PinnedArena {
-  std::vector<PinnedBuf> blocks;
-  size_t cur = 0, off = 0;
-  void reset() {
-    cur = 0;
-    off = 0;
-  }
-  void* alloc(size_t n, const char* what) {
-    n = (n + 255) / 256 * 256;
-    while (cur < blocks.size() && off + n > blocks[cur].bytes) {
-      ++cur;
-      off = 0;
-    }
-    if (cur == blocks.size()) {
-      blocks.emplace_back();
-      blocks.back().reserve(std::max<size_t>(n, 1 << 20), what);
-      off = 0;
-    }
-    void* p = static_cast<char*>(blocks[cur].ptr) + off;
-    off += n;
-    return p;
-  }
-  void release() {
-    for (auto& b : blocks) b.release();
-    blocks.clear();
-    reset();
-  }
-};
-
-uint64_t small_primes_upto(uint64_t B) {  // |{5,7,...,47} ∩ [5, B]| (the stamped primes)
-  static const uint32_t sp[] = {5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47};
-  uint64_t c = 0;
-  for (uint32_t q : sp) c += q <= B;
-  return c;
-}
-
-}  // namespace
-
-struct ws_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  uint32_t S = 1u << 18;
-  int sms = 148;
-  int bps[wsk::kNumModes] = {2, 2, 2, 2};  // resident blocks per SM per mode
-  std::string err;
-  ws_timing timing{};
-  cudaEvent_t ev[4] = {};
-
-  PinnedArena pin_up;  // async upload staging (jobs, runs), reset per call
-  PinnedBuf pin_out;   // results, read after the call's synchronisation
-  DevBuf<uint32_t> d_tabn;  // exact base-table size, written on device by prepare_table
-  DevBuf<uint32_t> d_tabn_old;  // its value before an extension (append_table reads it)
-  bool base_extend = true;      // grow the table incrementally (WHEELSIEVE_BASE_EXTEND=0: rebuild)
-  DevBuf<uint32_t> small_tab;  // small-prime pattern tables
-
-  // resident base-prime table: every prime in [53, base_B]
-  bool base_valid = false;
-  bool base_built = false;  // the last call (re)built the table
-  uint64_t base_B = 0;
-  uint32_t nprimes = 0;              // upper bound on the table size (host)
-  const uint32_t* nprimes_dev = nullptr;  // exact size on device (nullable)
-  DevBuf<uint32_t> tab_p;
-  DevBuf<unsigned long long> tab_m;
-  DevBuf<double> tab_inv;
-
-  uint32_t* words_out[2] = {nullptr, nullptr};  // SegmentBitmap export (ws_sieve_segment)
-  uint32_t n_below_S = 0;  // table primes (>= 37) below bucket_pmin: in-kernel; the rest bucketed
-  uint32_t bucket_pmin = 0;
-  uint32_t n_S = 0;        // table primes (>= 37) below S
-  uint32_t n_wc = 161;     // table primes below the warp-cooperative limit (1024)
-  // bytes of bucket lists per window buffer (two buffers): 8 GiB puts C4 in
-  // 7 windows instead of 41, with fewer fill / sieve tails (C4 56.8 -> 53.5 ms;
-  // 16 GiB is no faster: 32-bit entry indices cap a window near 2^32 entries)
-  size_t bucket_budget = 8ull << 30;
-  uint32_t cap_override = 0;           // test knob (WHEELSIEVE_BUCKET_CAP)
-  uint32_t piece_override = 0;         // tuning knob (WHEELSIEVE_FILL_PIECE)
-  bool fill_huge = true;               // carried-offset fill for p >= run length (WHEELSIEVE_FILL_HUGE)
-  uint32_t huge_step = 1;              // runs per histogram step there (WHEELSIEVE_HUGE_STEP)
-  uint32_t huge_from = 0;              // its lower bound in units of S (0: the run length)
-  uint64_t huge_thr = 0;               // the run length in slots the count below is for
-  uint32_t n_below_huge = 0;           // table primes (>= 53) below huge_thr
-  uint32_t bucket_min_ratio = 8;       // buckets iff largest base prime >= ratio * S
-  uint32_t bucket_ctas_per_sm = 0;     // tuning knob (WHEELSIEVE_BUCKET_CTAS)
-  uint32_t ctas_per_sm = 0;            // tuning knob, all launches (WHEELSIEVE_CTAS_PER_SM)
-
-  // scratch
-  DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)
-  DevBuf<uint32_t> bcount[2];
-  cudaStream_t fstream = nullptr;  // bucket-fill stream
-  // small base builds (B <= 2^18) run on their own stream, overlapping the call's
-  // uploads and resets; the first launch that reads the table joins it
-  cudaStream_t bstream = nullptr;
-  cudaEvent_t ev_fork = nullptr;
-  bool base_pending = false;
-  DevBuf<unsigned long long> base_scratch;  // small_base_kernel's epoch-tagged block counts
-  uint32_t base_epoch = 0;
-  const unsigned long long* ticket_zeroed = nullptr;  // ticket buffer known to be zero
-  size_t ticket_zeroed_cap = 0;
-  cudaStream_t cstream = nullptr;  // device->host copy stream (chunked enumeration)
-  cudaEvent_t ev_order = nullptr;
-  static constexpr int kMaxChunks = 16;
-  cudaEvent_t chunk_done[kMaxChunks] = {};
-  // host-bound enumeration through the 8-bit wire format (ws_wire.cpp);
-  // WHEELSIEVE_HOST_WIRE=0 ships uint64 values instead
-  bool host_wire = true;
-  wswire::Pool* pool = nullptr;  // host expansion threads (created on first use)
-  DevBuf<uint8_t> wire;          // wire entries of every chunk
-  DevBuf<uint8_t> wblk;          // survivors per wire block
-  PinnedBuf pin_wire, pin_wblk;
-  // a 6 MB ring stays in the host's last-level cache (60 MB L3 on the B200 box),
-  // so the payload crosses DRAM only once, as output (c2 e2e 26.4 -> 25.2 ms)
-  uint64_t wire_piece = 1u << 21;  // entries (bytes) per ring slot (WHEELSIEVE_WIRE_PIECE)
-  uint64_t wire_ring = 3;          // ring slots (WHEELSIEVE_WIRE_RING)
-  std::vector<cudaEvent_t> ring_ev;
-  cudaEvent_t fill_done[2] = {}, sieve_done[2] = {};
-  DevBuf<wsk::Run> runs;
-  DevBuf<wsk::Job> jobs;
-  DevBuf<wsk::JobAcc> acc;
-  DevBuf<unsigned long long> ticket;
-  DevBuf<uint32_t> per_seg;
-  DevBuf<unsigned long long> status;
-  DevBuf<unsigned long long> vals;  // enumeration scratch (base primes / host-bound output)
-  DevBuf<uint32_t> l0_p;
-  DevBuf<unsigned long long> l0_m;
-  DevBuf<double> l0_inv;
-  DevBuf<uint32_t> l0_n;
-  std::vector<wsk::Job> h_jobs;
-
-  ~ws_ctx() {
-    cudaSetDevice(device);
-    if (pool) wswire::pool_destroy(pool);
-    wire.release();
-    wblk.release();
-    pin_wire.release();
-    pin_wblk.release();
-    for (cudaEvent_t e : ring_ev) cudaEventDestroy(e);
-    for (auto* b : {&tab_p, &per_seg, &l0_p, &l0_n, &bucket[0], &bucket[1], &bcount[0], &bcount[1]})
-      b->release();
-    runs.release();
-    tab_inv.release();
-    l0_inv.release();
-    d_tabn.release();
-    d_tabn_old.release();
-    small_tab.release();
-    pin_up.release();
-    pin_out.release();
-    for (int i = 0; i < 2; ++i) {
-      if (fill_done[i]) cudaEventDestroy(fill_done[i]);
-      if (sieve_done[i]) cudaEventDestroy(sieve_done[i]);
-    }
-    if (fstream) cudaStreamDestroy(fstream);
-    if (bstream) cudaStreamDestroy(bstream);
-    base_scratch.release();
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (cstream) cudaStreamDestroy(cstream);
-    if (ev_order) cudaEventDestroy(ev_order);
-    for (cudaEvent_t e : chunk_done)
-      if (e) cudaEventDestroy(e);
-    for (auto* b : {&tab_m, &ticket, &status, &vals, &l0_m}) b->release();
-    jobs.release();
-    acc.release();
-    for (cudaEvent_t e : ev)
-      if (e) cudaEventDestroy(e);
-    if (stream) cudaStreamDestroy(stream);
-  }
-};
+using namespace wsh;
 
 namespace {
 
 // Every host<->device copy goes through these, so ws_timing reports the
 // bytes that crossed PCIe in the last call.
-cudaError_t copy_async(ws_ctx* c, void* dst, const void* src, size_t n, cudaMemcpyKind k,
+cudaError_t copy_async(DevCtx* c, void* dst, const void* src, size_t n, cudaMemcpyKind k,
                        cudaStream_t st) {
   if (k == cudaMemcpyHostToDevice) c->timing.h2d_bytes += n;
   if (k == cudaMemcpyDeviceToHost) c->timing.d2h_bytes += n;
   return cudaMemcpyAsync(dst, src, n, k, st);
 }
-cudaError_t copy_sync(ws_ctx* c, void* dst, const void* src, size_t n, cudaMemcpyKind k) {
+cudaError_t copy_sync(DevCtx* c, void* dst, const void* src, size_t n, cudaMemcpyKind k) {
   if (k == cudaMemcpyHostToDevice) c->timing.h2d_bytes += n;
   if (k == cudaMemcpyDeviceToHost) c->timing.d2h_bytes += n;
   return cudaMemcpy(dst, src, n, k);
@@ -349,7 +104,7 @@ double expected_large_hits(uint32_t pmin, uint32_t S, double pmax) {
 // Table primes (>= 53) below x, by an odd-only host sieve; cached per context
 // and per process (x is the fill's run length in slots, 2^23 at the default
 // 32 x 2^18, so the sieve runs once).
-uint32_t table_primes_below(ws_ctx* c, uint64_t x) {
+uint32_t table_primes_below(DevCtx* c, uint64_t x) {
   if (c->huge_thr == x) return c->n_below_huge;
   static std::mutex mu;
   static std::vector<std::pair<uint64_t, uint32_t>> memo;
@@ -376,7 +131,7 @@ uint32_t table_primes_below(ws_ctx* c, uint64_t x) {
 }
 
 // Order the main stream after a pending small base build (bstream).
-void join_base(ws_ctx* c) {
+void join_base(DevCtx* c) {
   if (!c->base_pending) return;
   ck(cudaStreamWaitEvent(c->stream, c->ev[1], 0), "base join");
   c->base_pending = false;
@@ -387,7 +142,7 @@ struct WireArgs {  // kEnumWire outputs
   uint8_t* blk8;
 };
 
-void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* out,
+void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* out,
                unsigned long long out_cap, bool timed, uint32_t acc_base = 0,
                bool record_start = true, const WireArgs* wire = nullptr) {
   uint64_t nseg = 0;
@@ -465,7 +220,9 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     W = std::max<uint64_t>(8, c->bucket_budget / (4ull * cap));
     W = std::min<uint64_t>({W, wsk::kMaxWindow, nseg});
     // the fill kernel indexes a window's lists with 32-bit entry indices
-    W = std::min<uint64_t>(W, ((1ull << 32) - (1ull << 26)) / cap - 1);
+    const uint64_t w32 = ((1ull << 32) - (1ull << 26)) / cap;
+    if (w32 < 2) throw Fail{WS_BAD_CONFIG, "bucket list capacity too large for 32-bit entry indices"};
+    W = std::max<uint64_t>(1, std::min<uint64_t>(W, w32 - 1));
     for (int b = 0; b < 2; ++b) {
       c->bucket[b].reserve(W * cap, "bucket lists");
       c->bcount[b].reserve(W, "bucket counts");
@@ -493,6 +250,8 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     // fill grid that covers the GPU (measured best for c4 and c5)
     piece = c->piece_override ? c->piece_override : 32;
     piece = std::min<uint64_t>(piece, W);
+    // a run's span in slots is indexed in 32 bits by the fill kernels
+    piece = std::max<uint64_t>(1, std::min<uint64_t>(piece, (0xFFFFFFFFull / c->S) - 1));
     size_t j = 0;
     for (uint64_t w = 0; w < nwin; ++w) {
       const uint64_t ws = w * W, we = std::min(nseg, ws + W);
@@ -599,13 +358,13 @@ void run_sieve(ws_ctx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   c->timing.segments += nseg;
 }
 
-// Make the resident table cover every prime in [37, B].  No host round
+// Make the resident table cover every prime in [53, B].  No host round
 // trip: the level-0 count and the table size stay on the device and the
 // kernels read them (SieveParams::nprimes_dev); the host keeps upper bounds.
 // Device-side BasePrimeStore::extend (base_store.cpp:44-69): the resident
 // table [53, base_B] already covers sqrt(B), so only (base_B, B] is sieved --
 // with that table -- and appended; the table size stays on the device.
-void extend_base(ws_ctx* c, uint64_t B) {
+void extend_base(DevCtx* c, uint64_t B) {
   join_base(c);
   ck(cudaEventRecord(c->ev[0], c->stream), "event");
   const uint64_t lo = c->base_B + 1;
@@ -642,7 +401,7 @@ void extend_base(ws_ctx* c, uint64_t B) {
   ck(cudaEventRecord(c->ev[1], c->stream), "event");
 }
 
-cudaError_t launch_small_base(ws_ctx* c, uint32_t n, uint32_t* p, unsigned long long* m,
+cudaError_t launch_small_base(DevCtx* c, uint32_t n, uint32_t* p, unsigned long long* m,
                               double* inv, uint32_t* count, cudaStream_t st) {
   if (!c->base_scratch.ptr) {
     c->base_scratch.reserve(64, "base scratch");
@@ -652,7 +411,7 @@ cudaError_t launch_small_base(ws_ctx* c, uint32_t n, uint32_t* p, unsigned long 
   return wsk::launch_small_base(n, p, m, inv, count, c->base_scratch.ptr, c->base_epoch, st);
 }
 
-void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
+void ensure_base(DevCtx* c, uint64_t B, bool fresh) {
   c->base_built = false;
   join_base(c);
   if (c->base_valid && c->base_B >= B && !fresh) return;
@@ -696,7 +455,7 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
     c->base_valid = true;
     return;
   }
-  // level 0: primes in [37, isqrt(B)] (isqrt(B) < 2^16: at most 6542 - 11)
+  // level 0: primes in [53, isqrt(B)] (isqrt(B) < 2^16: at most 6542 - 11)
   const uint64_t B0 = isqrt_u64(B);
   c->l0_p.reserve(7000, "l0");
   c->l0_m.reserve(7000, "l0");
@@ -748,7 +507,7 @@ void ensure_base(ws_ctx* c, uint64_t B, bool fresh) {
 // Copy the n job accumulators and, from the slot after them, the exact table
 // size (stored by the kernel: run_sieve's tabn_out) to pinned host memory in
 // one copy, and wait: the one synchronisation of a call.
-const wsk::JobAcc* fetch_results(ws_ctx* c, size_t n) {
+const wsk::JobAcc* fetch_results(DevCtx* c, size_t n) {
   char* h = static_cast<char*>(c->pin_out.reserve((n + 1) * sizeof(wsk::JobAcc), "pinned out"));
   ck(copy_async(c, h, c->acc.ptr, (n + 1) * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost,
                 c->stream), "results");
@@ -761,37 +520,152 @@ const wsk::JobAcc* fetch_results(ws_ctx* c, size_t n) {
 
 float event_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
-  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();  // an unrecorded event is not a failure of the next call
+    return 0;
+  }
   return ms;
 }
 
+void reset_after_failure(ws_ctx* ctx) {
+  cudaGetLastError();
+  // a failed call may leave launch state behind: re-zero the tickets
+  for (DevCtx* d : ctx->devs) d->ticket_zeroed = nullptr;
+}
+
+// Runs f() with the context's per-call state reset; a Fail (or any other
+// exception) becomes a status + ws_last_error.  The caller's current device
+// is restored on return.  ctx->timing aggregates the devices' timings (bytes,
+// launches and segments summed; device times the maximum over devices).
 template <class F>
-ws_status guarded(ws_ctx* c, F&& f) {
-  if (!c) return WS_BAD_CONFIG;
+ws_status guarded(ws_ctx* ctx, F&& f) {
+  if (!ctx || ctx->devs.empty()) return WS_BAD_CONFIG;
   Timer t;
-  c->err.clear();
-  c->timing = ws_timing{};
-  c->pin_up.reset();
+  ctx->err.clear();
+  ctx->timing = ws_timing{};
+  for (DevCtx* d : ctx->devs) {
+    d->err.clear();
+    d->timing = ws_timing{};
+    d->pin_up.reset();
+  }
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) {
+    cudaGetLastError();
+    prev = -1;
+  }
+  ws_status st = WS_OK;
   try {
-    if (cudaSetDevice(c->device) != cudaSuccess) throw Fail{WS_NO_DEVICE, "cudaSetDevice"};
+    if (cudaSetDevice(ctx->devs[0]->device) != cudaSuccess) throw Fail{WS_NO_DEVICE, "cudaSetDevice"};
     f();
   } catch (const Fail& e) {
-    c->err = e.msg;
-    cudaGetLastError();
-    c->ticket_zeroed = nullptr;  // a failed call may leave launch state behind: re-zero
-    return e.code;
+    ctx->err = e.msg;
+    st = e.code;
   } catch (const std::bad_alloc&) {
-    c->err = "host allocation failed";
-    c->ticket_zeroed = nullptr;
-    return WS_OUT_OF_MEMORY;
+    ctx->err = "host allocation failed";
+    st = WS_OUT_OF_MEMORY;
   } catch (...) {
-    c->err = "unknown failure";
-    c->ticket_zeroed = nullptr;
-    return WS_CUDA;
+    ctx->err = "unknown failure";
+    st = WS_CUDA;
   }
-  c->timing.total_ms = t.ms();
-  return WS_OK;
+  if (st != WS_OK) reset_after_failure(ctx);
+  ws_timing& T = ctx->timing;
+  for (DevCtx* d : ctx->devs) {
+    T.base_ms = std::max(T.base_ms, d->timing.base_ms);
+    T.sieve_ms = std::max(T.sieve_ms, d->timing.sieve_ms);
+    T.launches += d->timing.launches;
+    T.segments += d->timing.segments;
+    T.base_primes = std::max(T.base_primes, d->timing.base_primes);
+    T.h2d_bytes += d->timing.h2d_bytes;
+    T.d2h_bytes += d->timing.d2h_bytes;
+  }
+  T.total_ms = t.ms();
+  if (prev >= 0) cudaSetDevice(prev);
+  return st;
 }
+
+// fn(device context, local index) on every local device: inline for one
+// device, else concurrently on the per-device worker threads.  Every device
+// runs to completion before the first failure (by device order) is rethrown,
+// so no device is left inside a collective its peers never enter.
+void on_devices(ws_ctx* ctx, const std::function<void(DevCtx*, size_t)>& fn) {
+  const size_t n = ctx->devs.size();
+  if (n == 1 || !ctx->workers) {
+    for (size_t i = 0; i < n; ++i) {
+      ck(cudaSetDevice(ctx->devs[i]->device), "cudaSetDevice");
+      fn(ctx->devs[i], i);
+    }
+    return;
+  }
+  std::vector<std::exception_ptr> errs(n);
+  ctx->workers->run([&](size_t i) {
+    try {
+      ck(cudaSetDevice(ctx->devs[i]->device), "cudaSetDevice");
+      fn(ctx->devs[i], i);
+    } catch (...) {
+      errs[i] = std::current_exception();
+    }
+  });
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+void nccl_ck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Fail{WS_NCCL, std::string(what) + ": " + ncclGetErrorString(r)};
+}
+
+// The context's one collective: every shard contributes n_per 32-byte
+// JobAcc records (send[i]: device array of local device i, stream-ordered
+// after the kernels that wrote it) and every device receives all
+// nshards * n_per of them (shard-major) with one ncclAllGather per
+// communicator, issued as one NCCL group from this thread.  Returns the
+// gathered records on the host (device 0's copy).
+std::vector<wsk::JobAcc> allgather_records(ws_ctx* ctx, const std::vector<const wsk::JobAcc*>& send,
+                                           uint64_t n_per) {
+  const uint64_t total = n_per * ctx->nshards;
+  for (DevCtx* d : ctx->devs) {
+    ck(cudaSetDevice(d->device), "cudaSetDevice");
+    d->gather.reserve(total, "gather buffer");
+  }
+  nccl_ck(ncclGroupStart(), "ncclGroupStart");
+  for (size_t i = 0; i < ctx->devs.size(); ++i) {
+    DevCtx* d = ctx->devs[i];
+    ck(cudaSetDevice(d->device), "cudaSetDevice");
+    const ncclResult_t r = ncclAllGather(send[i], d->gather.ptr, 4 * n_per, ncclUint64,
+                                         ctx->comms[i], d->stream);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      nccl_ck(r, "ncclAllGather");
+    }
+  }
+  nccl_ck(ncclGroupEnd(), "ncclGroupEnd");
+  DevCtx* d0 = ctx->devs[0];
+  ck(cudaSetDevice(d0->device), "cudaSetDevice");
+  auto* h = static_cast<wsk::JobAcc*>(d0->pin_gather.reserve(total * sizeof(wsk::JobAcc), "pinned gather"));
+  ck(copy_async(d0, h, d0->gather.ptr, total * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost,
+                d0->stream), "gather readback");
+  for (DevCtx* d : ctx->devs) {
+    ck(cudaSetDevice(d->device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(d->stream), "collective sync");
+    ck(cudaGetLastError(), "kernel");
+  }
+  ck(cudaSetDevice(d0->device), "cudaSetDevice");
+  return std::vector<wsk::JobAcc>(h, h + total);
+}
+
+// ws_combine_checks: the fold applied to the gathered per-shard records
+// (count and sum wrap mod 2^64, xor folds, largest is the maximum).
+ws_checks combine(const ws_checks* r, uint64_t n) {
+  ws_checks o{};
+  for (uint64_t i = 0; i < n; ++i) {
+    o.count += r[i].count;
+    o.sum += r[i].sum;
+    o.xor_ ^= r[i].xor_;
+    o.largest = std::max(o.largest, r[i].largest);
+  }
+  return o;
+}
+
+ws_checks to_checks(const wsk::JobAcc& a) { return ws_checks{a.count, a.sum, a.xr, a.largest}; }
 
 void add_prelude(uint64_t L, uint64_t R, ws_checks* o) {  // engine.cpp:268-276
   for (uint64_t v : {uint64_t{2}, uint64_t{3}})
@@ -821,7 +695,7 @@ bool is_device_ptr(const void* p) {
 // byte per prime + one count byte per 128-slot block + per-segment totals;
 // each chunk crosses PCIe at ~1 byte per prime and the host pool widens it
 // into `out` while later pieces copy.
-void enumerate_wire(ws_ctx* c, uint64_t nseg, uint64_t nch, const std::vector<uint64_t>& lo,
+void enumerate_wire(DevCtx* c, uint64_t nseg, uint64_t nch, const std::vector<uint64_t>& lo,
                     const std::vector<uint64_t>& hi, const std::vector<uint64_t>& boff,
                     uint64_t* out, uint64_t cap, ws_checks* chk) {
   const uint64_t bps = c->S / wsk::kWireBlockSlots;
@@ -855,7 +729,7 @@ void enumerate_wire(ws_ctx* c, uint64_t nseg, uint64_t nch, const std::vector<ui
     c->timing.d2h_bytes += sizeof(wsk::JobAcc) + 4ull * ns;
     ck(cudaEventRecord(c->chunk_done[k], c->stream), "event");
   }
-  if (!c->pool) c->pool = wswire::pool_create(0);
+  if (!c->pool) c->pool = wswire::pool_create(c->host_threads);
   // Payload pieces of `piece` entries cross into a ring of `ring` pinned
   // slots, each expanded as soon as it lands and reused once expanded: a
   // small reused staging set instead of one buffer of the whole payload
@@ -939,11 +813,11 @@ void enumerate_wire(ws_ctx* c, uint64_t nseg, uint64_t nch, const std::vector<ui
   c->timing.base_primes = c->nprimes + small_primes_upto(c->base_B);
 }
 
-void enumerate_to_host(ws_ctx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_t cap,
+void enumerate_to_host(DevCtx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_t cap,
                        ws_checks* chk) {
   const wsk::Job whole = make_job(L, R, c->S, 0);
   const uint64_t nseg = whole.nseg;
-  const uint64_t nch = std::max<uint64_t>(1, std::min<uint64_t>(ws_ctx::kMaxChunks, nseg / 64));
+  const uint64_t nch = std::max<uint64_t>(1, std::min<uint64_t>(DevCtx::kMaxChunks, nseg / 64));
   std::vector<uint64_t> lo(nch), hi(nch), boff(nch + 1, 0);
   const uint64_t lo0 = L / 6 * 6;
   for (uint64_t k = 0; k < nch; ++k) {
@@ -989,71 +863,371 @@ void enumerate_to_host(ws_ctx* c, uint64_t L, uint64_t R, uint64_t* out, uint64_
   c->timing.base_primes = c->nprimes + small_primes_upto(c->base_B);
 }
 
-}  // namespace
+// ---- shared bodies of the entry points -----------------------------------
 
-extern "C" {
-
-const char* ws_version(void) { return "wheelsieve-b200 0.1 (sm_100a)"; }
-
-void ws_opts_default(ws_opts* o) {
-  if (!o) return;
-  std::memset(o, 0, sizeof *o);
-  o->struct_size = sizeof(ws_opts);
-  o->segment_slots = 1u << 18;
-  o->device = -1;
-}
-
-const char* ws_status_name(ws_status s) {
-  switch (s) {
-    case WS_OK: return "ok";
-    case WS_NOT_ON_WHEEL: return "NotOnWheel";
-    case WS_OVERFLOW: return "Overflow";
-    case WS_EMPTY_RANGE: return "EmptyRange";
-    case WS_CAPACITY: return "Capacity";
-    case WS_DOMAIN: return "Domain";
-    case WS_ALIGNMENT: return "Alignment";
-    case WS_BAD_CONFIG: return "BadConfig";
-    case WS_INCOMPLETE_BASE: return "IncompleteBase";
-    case WS_ORDERING: return "Ordering";
-    case WS_IO: return "Io";
-    case WS_BAD_MANIFEST: return "BadManifest";
-    case WS_CHECKSUM_MISMATCH: return "ChecksumMismatch";
-    case WS_BEYOND_FRONTIER: return "BeyondFrontier";
-    case WS_CUDA: return "Cuda";
-    case WS_NO_DEVICE: return "NoDevice";
-    case WS_OUT_OF_MEMORY: return "OutOfMemory";
+ws_status partition_impl(uint64_t L, uint64_t R, uint32_t S, uint32_t rank, uint32_t world,
+                         uint64_t* lo, uint64_t* hi) {
+  if (!lo || !hi || world == 0 || rank >= world || S == 0) return WS_BAD_CONFIG;
+  if (R <= L) {
+    *lo = *hi = L;
+    return WS_OK;
   }
-  return "unknown";
+  if (R > kMaxSegmentEnd) return WS_OVERFLOW;
+  const uint64_t lo0 = L / 6 * 6;
+  const uint64_t nslots = (R - lo0 + 5) / 6;
+  const uint64_t nseg = (nslots + S - 1) / S;
+  auto seg_at = [&](uint64_t r) {  // balanced: floor(r * nseg / world)
+    const unsigned __int128 x = static_cast<unsigned __int128>(r) * nseg / world;
+    return static_cast<uint64_t>(x);
+  };
+  const uint64_t a = seg_at(rank), b = seg_at(rank + 1ull);
+  *lo = rank == 0 ? L : std::min<uint64_t>(R, lo0 + 6ull * S * a);
+  *hi = rank + 1 == world ? R : std::min<uint64_t>(R, lo0 + 6ull * S * b);
+  if (*lo < L) *lo = L;
+  if (*hi < *lo) *hi = *lo;
+  return WS_OK;
 }
 
-ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
-  if (!out) return WS_BAD_CONFIG;
+// Shard g's share of [L, R) and the global index of its first segment.
+struct Shard {
+  uint64_t lo = 0, hi = 0, seg0 = 0, nseg = 0;
+};
+
+Shard shard_of(const ws_ctx* ctx, uint32_t g, uint64_t L, uint64_t R) {
+  Shard s;
+  const uint32_t S = ctx->devs[0]->S;
+  if (partition_impl(L, R, S, g, ctx->nshards, &s.lo, &s.hi) != WS_OK)
+    throw Fail{WS_OVERFLOW, "range end exceeds the sievable 64-bit range"};
+  if (s.hi > s.lo) {
+    s.seg0 = (s.lo - L / 6 * 6) / (6ull * S);
+    s.nseg = make_job(s.lo, s.hi, S, 0).nseg;
+  }
+  return s;
+}
+
+// Queues the count of [lo, hi) on one device (its accumulator d->acc[0]; the
+// per-segment counts into the device array dps when non-null).  An empty
+// range leaves a zero accumulator.
+void queue_count(DevCtx* d, uint64_t lo, uint64_t hi, int mode, bool fresh, uint32_t* dps) {
+  if (hi <= lo) {
+    d->acc.reserve(2, "acc");
+    ck(cudaEventRecord(d->ev[2], d->stream), "event");
+    ck(cudaMemsetAsync(d->acc.ptr, 0, sizeof(wsk::JobAcc), d->stream), "zero acc");
+    ck(cudaEventRecord(d->ev[3], d->stream), "event");
+    return;
+  }
+  validate_range(lo, hi);
+  ensure_base(d, hi >= 2 ? isqrt_u64(hi - 1) : 0, fresh);
+  d->h_jobs.assign(1, make_job(lo, hi, d->S, 0));
+  run_sieve(d, mode, dps, nullptr, 0, true);
+}
+
+void record_device_times(DevCtx* d) {
+  d->timing.base_ms = d->base_built ? event_ms(d->ev[0], d->ev[1]) : 0.0;
+  d->timing.sieve_ms = event_ms(d->ev[2], d->ev[3]);
+}
+
+void count_range_single(DevCtx* d, uint64_t L, uint64_t R, uint32_t flags, ws_checks* out,
+                        uint32_t* per_seg, uint64_t per_seg_cap, uint64_t* n_seg) {
+  validate_range(L, R);
+  const bool fresh = flags & WS_FRESH_BASE;
+  ensure_base(d, R >= 2 ? isqrt_u64(R - 1) : 0, fresh);
+  d->h_jobs.assign(1, make_job(L, R, d->S, 0));
+  const uint64_t nseg = d->h_jobs[0].nseg;
+  uint32_t* dps = nullptr;
+  const bool dev_out = flags & WS_OUT_DEVICE;
+  if (per_seg) {
+    if (dev_out) {
+      if (per_seg_cap < nseg) throw Fail{WS_CAPACITY, "per_seg capacity below segment count"};
+      dps = per_seg;
+    } else {
+      d->per_seg.reserve(nseg, "per_seg");
+      dps = d->per_seg.ptr;
+    }
+  }
+  const int mode = (flags & WS_WANT_CHECKS) ? wsk::kCountChecks : wsk::kCount;
+  run_sieve(d, mode, dps, nullptr, 0, true);
+  if (per_seg && !dev_out)
+    ck(copy_async(d, per_seg, dps, std::min(nseg, per_seg_cap) * sizeof(uint32_t),
+                  cudaMemcpyDeviceToHost, d->stream), "per_seg");
+  *out = to_checks(*fetch_results(d, 1));
+  add_prelude(L, R, out);
+  if (n_seg) *n_seg = nseg;
+  record_device_times(d);
+}
+
+// Multi-device count: shard g = ws_partition(L, R, g, nshards); one allgather.
+void count_range_multi(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws_checks* out,
+                       uint32_t* per_seg, uint64_t per_seg_cap, uint64_t* n_seg) {
+  validate_range(L, R);
+  const uint64_t nseg = make_job(L, R, ctx->devs[0]->S, 0).nseg;
+  const bool dev_out = flags & WS_OUT_DEVICE;
+  if (per_seg && dev_out && per_seg_cap < nseg)
+    throw Fail{WS_CAPACITY, "per_seg capacity below segment count"};
+  const int mode = (flags & WS_WANT_CHECKS) ? wsk::kCountChecks : wsk::kCount;
+  on_devices(ctx, [&](DevCtx* d, size_t i) {
+    const Shard sh = shard_of(ctx, ctx->shard_of(i), L, R);
+    uint32_t* dps = nullptr;
+    if (per_seg && sh.nseg) {
+      d->per_seg.reserve(sh.nseg, "per_seg");
+      dps = d->per_seg.ptr;
+    }
+    queue_count(d, sh.lo, sh.hi, mode, flags & WS_FRESH_BASE, dps);
+    if (dps && per_seg_cap > sh.seg0) {
+      const uint64_t n = std::min(sh.nseg, per_seg_cap - sh.seg0);
+      ck(copy_async(d, per_seg + sh.seg0, dps, n * sizeof(uint32_t),
+                    dev_out ? cudaMemcpyDefault : cudaMemcpyDeviceToHost, d->stream), "per_seg");
+    }
+  });
+  std::vector<const wsk::JobAcc*> send;
+  for (DevCtx* d : ctx->devs) send.push_back(d->acc.ptr);
+  const std::vector<wsk::JobAcc> rec = allgather_records(ctx, send, 1);
+  std::vector<ws_checks> c(rec.size());
+  for (size_t g = 0; g < rec.size(); ++g) c[g] = to_checks(rec[g]);
+  *out = combine(c.data(), c.size());
+  add_prelude(L, R, out);
+  if (n_seg) *n_seg = nseg;
+  for (DevCtx* d : ctx->devs) record_device_times(d);
+}
+
+// Per-job results of a batch (count_intervals / count_ranges): job j of the
+// batch is ranges[j]; shard g sieves the jobs of owner(j) == g.  Single
+// device: one launch, results straight from the accumulators.  Multi-device:
+// each shard's accumulators are padded to n_per records and gathered.
+void count_jobs(ws_ctx* ctx, const std::vector<std::pair<uint64_t, uint64_t>>& ranges, bool checks,
+                bool fresh, const std::function<uint32_t(uint64_t)>& owner, uint64_t n_per,
+                const std::function<uint64_t(uint64_t)>& slot, std::vector<ws_checks>& res) {
+  const uint64_t n = ranges.size();
+  res.assign(n, ws_checks{});
+  const int mode = checks ? wsk::kCountChecks : wsk::kCount;
+  std::vector<const wsk::JobAcc*> send(ctx->devs.size(), nullptr);
+  std::vector<std::vector<uint64_t>> mine(ctx->devs.size());
+  for (size_t i = 0; i < ctx->devs.size(); ++i) {
+    const uint32_t g = ctx->shard_of(i);
+    for (uint64_t j = 0; j < n; ++j)
+      if (owner(j) == g) mine[i].push_back(j);
+  }
+  on_devices(ctx, [&](DevCtx* d, size_t i) {
+    const std::vector<uint64_t>& js = mine[i];
+    uint64_t maxR = 0;
+    for (uint64_t j : js)
+      if (ranges[j].second > ranges[j].first) maxR = std::max(maxR, ranges[j].second);
+    auto build = [&] {
+      d->h_jobs.clear();
+      d->h_jobs.reserve(js.size());
+      uint64_t seg = 0;
+      for (uint64_t j : js) {
+        const auto [lo, hi] = ranges[j];
+        d->h_jobs.push_back(make_job(lo, std::max(lo, hi), d->S, seg));
+        seg += d->h_jobs.back().nseg;
+      }
+    };
+    if (!js.empty()) ensure_base(d, maxR >= 2 ? isqrt_u64(maxR - 1) : 0, fresh);
+    build();  // after ensure_base, which may sieve the base through h_jobs
+    if (js.empty()) {
+      d->acc.reserve(2, "acc");
+      ck(cudaEventRecord(d->ev[2], d->stream), "event");
+      ck(cudaEventRecord(d->ev[3], d->stream), "event");
+    } else {
+      run_sieve(d, mode, nullptr, nullptr, 0, true);
+    }
+    if (!ctx->nccl) return;
+    d->gsend.reserve(std::max<uint64_t>(n_per, 1), "gather send");
+    ck(cudaMemsetAsync(d->gsend.ptr, 0, n_per * sizeof(wsk::JobAcc), d->stream), "zero send");
+    if (!js.empty())
+      ck(cudaMemcpyAsync(d->gsend.ptr, d->acc.ptr, js.size() * sizeof(wsk::JobAcc),
+                         cudaMemcpyDeviceToDevice, d->stream), "send records");
+    send[i] = d->gsend.ptr;
+  });
+  if (!ctx->nccl) {
+    DevCtx* d = ctx->devs[0];
+    const wsk::JobAcc* acc = fetch_results(d, mine[0].size());
+    for (size_t k = 0; k < mine[0].size(); ++k) res[mine[0][k]] = to_checks(acc[k]);
+  } else {
+    const std::vector<wsk::JobAcc> rec = allgather_records(ctx, send, n_per);
+    for (uint64_t j = 0; j < n; ++j) res[j] = to_checks(rec[owner(j) * n_per + slot(j)]);
+  }
+  for (uint64_t j = 0; j < n; ++j) add_prelude(ranges[j].first, ranges[j].second, &res[j]);
+  for (DevCtx* d : ctx->devs) record_device_times(d);
+}
+
+void enumerate_single(DevCtx* d, uint64_t L, uint64_t R, uint32_t flags, uint64_t* out,
+                      uint64_t cap, uint64_t* n_out, ws_checks* checks) {
+  ws_checks chk{};
+  validate_range(L, R);
+  ensure_base(d, R >= 2 ? isqrt_u64(R - 1) : 0, flags & WS_FRESH_BASE);
+  uint64_t pre[2];
+  uint64_t npre = 0;
+  for (uint64_t v : {uint64_t{2}, uint64_t{3}})
+    if (v >= L && v < R) pre[npre++] = v;
+  d->h_jobs.assign(1, make_job(L, R, d->S, 0));
+  const bool dev_out = flags & WS_OUT_DEVICE;
+  if (dev_out && out && !is_device_ptr(out))
+    throw Fail{WS_BAD_CONFIG, "WS_OUT_DEVICE with a non-device pointer"};
+  if (!dev_out) {
+    for (uint64_t i = 0; i < npre && i < cap; ++i) out[i] = pre[i];
+    enumerate_to_host(d, L, R, out + std::min(npre, cap), cap > npre ? cap - npre : 0, &chk);
+  } else {
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(out) + std::min(npre, cap);
+    const uint64_t dcap = cap > npre ? cap - npre : 0;
+    if (npre && cap)
+      ck(copy_async(d, out, pre, std::min(npre, cap) * 8, cudaMemcpyHostToDevice, d->stream),
+         "prelude");
+    run_sieve(d, wsk::kEnumerate, nullptr, dst, dcap, true);
+    chk = to_checks(*fetch_results(d, 1));
+  }
+  add_prelude(L, R, &chk);
+  *n_out = chk.count;
+  if (checks) *checks = chk;
+  record_device_times(d);
+  if (chk.count > cap) throw Fail{WS_CAPACITY, "output capacity below the prime count"};
+}
+
+int device_of_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged ? a.device : -1;
+}
+
+// Multi-device enumeration: a count pass on every shard, one allgather of
+// the shard records (offsets and totals), then every device writes its shard
+// at its offset.
+void enumerate_multi(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, uint64_t* out,
+                     uint64_t cap, uint64_t* n_out, ws_checks* checks) {
+  validate_range(L, R);
+  const bool dev_out = flags & WS_OUT_DEVICE;
+  const int out_dev = dev_out && out ? device_of_ptr(out) : -1;
+  if (dev_out && out && out_dev < 0)
+    throw Fail{WS_BAD_CONFIG, "WS_OUT_DEVICE with a non-device pointer"};
+  on_devices(ctx, [&](DevCtx* d, size_t i) {
+    const Shard sh = shard_of(ctx, ctx->shard_of(i), L, R);
+    queue_count(d, sh.lo, sh.hi, wsk::kCountChecks, flags & WS_FRESH_BASE, nullptr);
+  });
+  std::vector<const wsk::JobAcc*> send;
+  for (DevCtx* d : ctx->devs) send.push_back(d->acc.ptr);
+  const std::vector<wsk::JobAcc> rec = allgather_records(ctx, send, 1);
+  std::vector<ws_checks> c(rec.size());
+  for (size_t g = 0; g < rec.size(); ++g) c[g] = to_checks(rec[g]);
+  ws_checks total = combine(c.data(), c.size());
+  add_prelude(L, R, &total);
+  uint64_t pre[2];
+  uint64_t npre = 0;
+  for (uint64_t v : {uint64_t{2}, uint64_t{3}})
+    if (v >= L && v < R) pre[npre++] = v;
+  // global offset of every shard; this process owns shards [first, first + k)
+  std::vector<uint64_t> off(ctx->nshards + 1, npre);
+  for (uint32_t g = 0; g < ctx->nshards; ++g) off[g + 1] = off[g] + c[g].count;
+  const uint32_t first = ctx->shard_of(0);
+  const uint64_t local_base = first == 0 ? 0 : off[first];
+  const uint64_t local_end = off[first + ctx->devs.size()];
+  const uint64_t local_n = local_end - local_base;
+  if (first == 0 && npre && cap) {
+    if (dev_out)
+      ck(cudaMemcpy(out, pre, std::min(npre, cap) * 8, cudaMemcpyHostToDevice), "prelude");
+    else
+      for (uint64_t i = 0; i < npre && i < cap; ++i) out[i] = pre[i];
+  }
+  on_devices(ctx, [&](DevCtx* d, size_t i) {
+    const uint32_t g = ctx->shard_of(i);
+    const Shard sh = shard_of(ctx, g, L, R);
+    const uint64_t pos = off[g] - local_base;
+    const uint64_t room = cap > pos ? cap - pos : 0;
+    if (sh.hi <= sh.lo || !out) return;
+    ws_checks chk{};
+    if (!dev_out) {
+      enumerate_to_host(d, sh.lo, sh.hi, out + pos, room, &chk);
+    } else {
+      d->h_jobs.assign(1, make_job(sh.lo, sh.hi, d->S, 0));
+      const uint64_t n = c[g].count;
+      if (out_dev == d->device) {
+        run_sieve(d, wsk::kEnumerate, nullptr, reinterpret_cast<unsigned long long*>(out + pos),
+                  room, true);
+      } else {  // another device's memory: enumerate locally, then one copy over NVLink
+        d->vals.reserve(std::max<uint64_t>(n, 1), "shard values");
+        run_sieve(d, wsk::kEnumerate, nullptr, d->vals.ptr, n, true);
+        if (room)
+          ck(cudaMemcpyAsync(out + pos, d->vals.ptr, std::min(n, room) * 8, cudaMemcpyDefault,
+                             d->stream), "shard copy");
+      }
+      chk = to_checks(*fetch_results(d, 1));
+    }
+    if (chk.count != c[g].count || chk.sum != c[g].sum || chk.xor_ != c[g].xor_)
+      throw Fail{WS_CUDA, "shard enumeration disagrees with its count pass"};
+  });
+  *n_out = local_n;
+  if (checks) *checks = total;
+  for (DevCtx* d : ctx->devs) record_device_times(d);
+  if (local_n > cap) throw Fail{WS_CAPACITY, "output capacity below the prime count"};
+}
+
+// Every local device enumerates its shard into its own memory: one pass,
+// then one allgather of the shard records for the totals.
+void enumerate_shards(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, uint64_t* const* outs,
+                      const uint64_t* caps, uint64_t* counts, ws_checks* checks) {
+  validate_range(L, R);
+  const uint32_t first = ctx->shard_of(0);
+  uint64_t npre = 0;
+  uint64_t pre[2];
+  for (uint64_t v : {uint64_t{2}, uint64_t{3}})
+    if (v >= L && v < R) pre[npre++] = v;
+  std::vector<uint64_t> got(ctx->devs.size(), 0);
+  on_devices(ctx, [&](DevCtx* d, size_t i) {
+    const uint32_t g = ctx->shard_of(i);
+    const Shard sh = shard_of(ctx, g, L, R);
+    if (outs[i] && device_of_ptr(outs[i]) != d->device)
+      throw Fail{WS_BAD_CONFIG, "outs[i] must be memory of local device i"};
+    if (!outs[i] && caps[i]) throw Fail{WS_BAD_CONFIG, "null output with nonzero capacity"};
+    // shard 0 carries the prelude 2, 3
+    const uint64_t np = g == 0 ? npre : 0;
+    if (np && caps[i])
+      ck(copy_async(d, outs[i], pre, std::min(np, caps[i]) * 8, cudaMemcpyHostToDevice, d->stream),
+         "prelude");
+    const uint64_t room = caps[i] > np ? caps[i] - np : 0;
+    if (sh.hi <= sh.lo) {
+      queue_count(d, sh.lo, sh.hi, wsk::kCount, false, nullptr);
+    } else {
+      ensure_base(d, sh.hi >= 2 ? isqrt_u64(sh.hi - 1) : 0, flags & WS_FRESH_BASE);
+      d->h_jobs.assign(1, make_job(sh.lo, sh.hi, d->S, 0));
+      run_sieve(d, wsk::kEnumerate, nullptr,
+                reinterpret_cast<unsigned long long*>(outs[i] + std::min(np, caps[i])), room, true);
+    }
+    got[i] = np;
+  });
+  std::vector<const wsk::JobAcc*> send;
+  for (DevCtx* d : ctx->devs) send.push_back(d->acc.ptr);
+  const std::vector<wsk::JobAcc> rec = allgather_records(ctx, send, 1);
+  std::vector<ws_checks> c(rec.size());
+  for (size_t g = 0; g < rec.size(); ++g) c[g] = to_checks(rec[g]);
+  ws_checks total = combine(c.data(), c.size());
+  add_prelude(L, R, &total);
+  bool short_cap = false;
+  for (size_t i = 0; i < ctx->devs.size(); ++i) {
+    counts[i] = got[i] + c[first + i].count;
+    short_cap = short_cap || counts[i] > caps[i];
+  }
+  if (checks) *checks = total;
+  for (DevCtx* d : ctx->devs) record_device_times(d);
+  if (short_cap) throw Fail{WS_CAPACITY, "a shard's output capacity is below its prime count"};
+}
+
+// One device context on CUDA device `dev` (everything but NCCL).
+ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   *out = nullptr;
-  ws_opts o;
-  ws_opts_default(&o);
-  if (opts) {
-    if (opts->struct_size != sizeof(ws_opts)) return WS_BAD_CONFIG;
-    o = *opts;
-  }
-  const uint32_t S = o.segment_slots;
-  if (S < (1u << 12) || S > (1u << 18) || (S & (S - 1))) return WS_BAD_CONFIG;
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
     cudaGetLastError();
     return WS_NO_DEVICE;
   }
-  int dev = o.device;
-  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) return WS_NO_DEVICE;
-  if (dev >= ndev) return WS_NO_DEVICE;
-  cudaDeviceProp prop{};
-  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return WS_NO_DEVICE;
   if (prop.major != 10) return WS_NO_DEVICE;  // built for sm_100a only
-  ws_ctx* c = new (std::nothrow) ws_ctx;
+  DevCtx* c = new (std::nothrow) DevCtx;
   if (!c) return WS_OUT_OF_MEMORY;
   c->device = dev;
   c->S = S;
-  {  // primes in [37, S): the in-kernel share of the table; and the warp-
-     // cooperative share [37, wc_limit)
+  {  // primes in [53, S): the in-kernel share of the table; and the warp-
+     // cooperative share [53, wc_limit)
     // primes below bucket_pmin = ratio * S stay in the kernel even when the
     // large ones are bucketed (p in [S, pmin) through the loop-free one-hit
     // path): a bucketed hit costs ~90 instructions (fill + apply); measured
@@ -1112,7 +1286,7 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) == cudaSuccess;
-  for (int i = 0; i < ws_ctx::kMaxChunks && ok; ++i)
+  for (int i = 0; i < DevCtx::kMaxChunks && ok; ++i)
     ok = cudaEventCreateWithFlags(&c->chunk_done[i], cudaEventDisableTiming) == cudaSuccess;
   if (ok) {
     std::vector<uint32_t> tab(wsk::small_table_words());
@@ -1136,15 +1310,197 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   return WS_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+const char* ws_version(void) { return "wheelsieve-b200 0.2 (sm_100a, NCCL multi-device)"; }
+
+void ws_opts_default(ws_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->struct_size = sizeof(ws_opts);
+  o->segment_slots = 1u << 18;
+  o->device = -1;
+  o->world = 1;
+}
+
+const char* ws_status_name(ws_status s) {
+  switch (s) {
+    case WS_OK: return "ok";
+    case WS_NOT_ON_WHEEL: return "NotOnWheel";
+    case WS_OVERFLOW: return "Overflow";
+    case WS_EMPTY_RANGE: return "EmptyRange";
+    case WS_CAPACITY: return "Capacity";
+    case WS_DOMAIN: return "Domain";
+    case WS_ALIGNMENT: return "Alignment";
+    case WS_BAD_CONFIG: return "BadConfig";
+    case WS_INCOMPLETE_BASE: return "IncompleteBase";
+    case WS_ORDERING: return "Ordering";
+    case WS_IO: return "Io";
+    case WS_BAD_MANIFEST: return "BadManifest";
+    case WS_CHECKSUM_MISMATCH: return "ChecksumMismatch";
+    case WS_BEYOND_FRONTIER: return "BeyondFrontier";
+    case WS_CUDA: return "Cuda";
+    case WS_NO_DEVICE: return "NoDevice";
+    case WS_OUT_OF_MEMORY: return "OutOfMemory";
+    case WS_NCCL: return "Nccl";
+  }
+  return "unknown";
+}
+
+ws_status ws_nccl_unique_id(uint8_t* id) {
+  if (!id) return WS_BAD_CONFIG;
+  static_assert(sizeof(ncclUniqueId) == WS_NCCL_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return WS_NCCL;
+  std::memcpy(id, &u, sizeof u);
+  return WS_OK;
+}
+
+ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
+  if (!out) return WS_BAD_CONFIG;
+  *out = nullptr;
+  ws_opts o;
+  ws_opts_default(&o);
+  if (opts) {
+    constexpr uint32_t kV1 = 16;  // {struct_size, segment_slots, device, reserved}
+    if (opts->struct_size == kV1) {
+      std::memcpy(&o, opts, kV1);
+      if (o.n_devices != 0) return WS_BAD_CONFIG;  // v1's reserved word must be zero
+      o.struct_size = sizeof(ws_opts);
+    } else if (opts->struct_size == sizeof(ws_opts)) {
+      o = *opts;
+    } else {
+      return WS_BAD_CONFIG;
+    }
+  }
+  const uint32_t S = o.segment_slots;
+  if (S < (1u << 12) || S > (1u << 18) || (S & (S - 1))) return WS_BAD_CONFIG;
+  if (o.world == 0) o.world = 1;
+  if (o.rank >= o.world || o.n_devices > WS_MAX_DEVICES) return WS_BAD_CONFIG;
+  if (o.world > 1 && o.n_devices == 0) return WS_BAD_CONFIG;  // multi-process needs NCCL
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return WS_NO_DEVICE;
+  }
+  std::vector<int> devices;
+  if (o.n_devices == 0) {
+    int dev = o.device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) return WS_NO_DEVICE;
+    devices.push_back(dev);
+  } else {
+    for (uint32_t i = 0; i < o.n_devices; ++i) devices.push_back(o.device_ids[i]);
+  }
+  for (size_t i = 0; i < devices.size(); ++i) {
+    if (devices[i] < 0 || devices[i] >= ndev) return WS_NO_DEVICE;
+    for (size_t j = 0; j < i; ++j)
+      if (devices[j] == devices[i]) return WS_BAD_CONFIG;  // one shard per device
+  }
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  ws_ctx* c = new (std::nothrow) ws_ctx;
+  if (!c) return WS_OUT_OF_MEMORY;
+  c->nccl = o.n_devices > 0;
+  c->world = o.world;
+  c->rank = o.rank;
+  c->nshards = c->nccl ? o.world * static_cast<uint32_t>(devices.size()) : 1;
+  const unsigned cpus = std::max(1u, std::thread::hardware_concurrency());
+  for (size_t i = 0; i < devices.size(); ++i) {
+    DevCtx* d = nullptr;
+    const ws_status st = make_dev(devices[i], S, &d);
+    if (st != WS_OK) {
+      delete c;
+      if (prev >= 0) cudaSetDevice(prev);
+      return st;
+    }
+    d->shard = c->shard_of(i);
+    // co-resident devices split the host's cores between their wire expanders
+    if (devices.size() > 1 && !std::getenv("WHEELSIEVE_HOST_THREADS"))
+      d->host_threads = std::max(1u, cpus / static_cast<unsigned>(devices.size()));
+    c->devs.push_back(d);
+  }
+  if (c->nccl) {
+    const int k = static_cast<int>(devices.size());
+    c->comms.assign(devices.size(), nullptr);
+    ncclResult_t r;
+    if (o.world == 1) {
+      r = ncclCommInitAll(c->comms.data(), k, devices.data());
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, o.nccl_id, sizeof id);
+      r = ncclGroupStart();
+      for (int i = 0; i < k && r == ncclSuccess; ++i) {
+        cudaSetDevice(devices[i]);
+        r = ncclCommInitRank(&c->comms[i], static_cast<int>(o.world) * k, id,
+                             static_cast<int>(o.rank) * k + i);
+      }
+      const ncclResult_t r2 = ncclGroupEnd();
+      if (r == ncclSuccess) r = r2;
+    }
+    if (r != ncclSuccess) {
+      c->comms.clear();
+      delete c;
+      if (prev >= 0) cudaSetDevice(prev);
+      return WS_NCCL;
+    }
+    if (devices.size() > 1) c->workers = new (std::nothrow) DevWorkers(devices);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  *out = c;
+  return WS_OK;
+}
+
 void ws_ctx_destroy(ws_ctx* ctx) { delete ctx; }
 
 const char* ws_last_error(const ws_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
-void* ws_ctx_stream(ws_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+void* ws_ctx_stream(ws_ctx* ctx) {
+  return ctx && !ctx->devs.empty() ? static_cast<void*>(ctx->devs[0]->stream) : nullptr;
+}
+
+uint32_t ws_ctx_num_devices(const ws_ctx* ctx) {
+  return ctx ? static_cast<uint32_t>(ctx->devs.size()) : 0;
+}
+
+uint32_t ws_ctx_num_shards(const ws_ctx* ctx) { return ctx ? ctx->nshards : 0; }
+
+int32_t ws_ctx_device(const ws_ctx* ctx, uint32_t i) {
+  return ctx && i < ctx->devs.size() ? ctx->devs[i]->device : -1;
+}
+
+void* ws_ctx_device_stream(ws_ctx* ctx, uint32_t i) {
+  return ctx && i < ctx->devs.size() ? static_cast<void*>(ctx->devs[i]->stream) : nullptr;
+}
 
 ws_status ws_last_timing(const ws_ctx* ctx, ws_timing* out) {
   if (!ctx || !out) return WS_BAD_CONFIG;
   *out = ctx->timing;
+  return WS_OK;
+}
+
+ws_status ws_device_timing(const ws_ctx* ctx, uint32_t i, ws_timing* out) {
+  if (!ctx || !out || i >= ctx->devs.size()) return WS_BAD_CONFIG;
+  *out = ctx->devs[i]->timing;
+  out->total_ms = ctx->timing.total_ms;
+  return WS_OK;
+}
+
+ws_status ws_ctx_comm_info(const ws_ctx* ctx, uint32_t i, int32_t* nranks, int32_t* comm_rank) {
+  if (!ctx || !nranks || !comm_rank || !ctx->nccl || i >= ctx->comms.size()) return WS_BAD_CONFIG;
+  int n = 0, r = 0;
+  if (ncclCommCount(ctx->comms[i], &n) != ncclSuccess ||
+      ncclCommUserRank(ctx->comms[i], &r) != ncclSuccess)
+    return WS_NCCL;
+  *nranks = n;
+  *comm_rank = r;
+  return WS_OK;
+}
+
+ws_status ws_combine_checks(const ws_checks* records, uint64_t n, ws_checks* out) {
+  if (!out || (n && !records)) return WS_BAD_CONFIG;
+  *out = combine(records, n);
   return WS_OK;
 }
 
@@ -1170,25 +1526,7 @@ ws_status ws_start_offsets(uint64_t p, uint64_t start, uint64_t* id1, uint64_t* 
 
 ws_status ws_partition(uint64_t L, uint64_t R, uint32_t S, uint32_t rank, uint32_t world,
                        uint64_t* lo, uint64_t* hi) {
-  if (!lo || !hi || world == 0 || rank >= world || S == 0) return WS_BAD_CONFIG;
-  if (R <= L) {
-    *lo = *hi = L;
-    return WS_OK;
-  }
-  if (R > kMaxSegmentEnd) return WS_OVERFLOW;
-  const uint64_t lo0 = L / 6 * 6;
-  const uint64_t nslots = (R - lo0 + 5) / 6;
-  const uint64_t nseg = (nslots + S - 1) / S;
-  auto seg_at = [&](uint64_t r) {  // balanced: floor(r * nseg / world)
-    const unsigned __int128 x = static_cast<unsigned __int128>(r) * nseg / world;
-    return static_cast<uint64_t>(x);
-  };
-  const uint64_t a = seg_at(rank), b = seg_at(rank + 1ull);
-  *lo = rank == 0 ? L : std::min<uint64_t>(R, lo0 + 6ull * S * a);
-  *hi = rank + 1 == world ? R : std::min<uint64_t>(R, lo0 + 6ull * S * b);
-  if (*lo < L) *lo = L;
-  if (*hi < *lo) *hi = *lo;
-  return WS_OK;
+  return partition_impl(L, R, S, rank, world, lo, hi);
 }
 
 ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws_checks* out,
@@ -1198,91 +1536,39 @@ ws_status ws_count_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws
     *out = ws_checks{};
     if (n_seg) *n_seg = 0;
     if (R <= L) return;
-    validate_range(L, R);
-    const bool fresh = flags & WS_FRESH_BASE;
-    ensure_base(ctx, R >= 2 ? isqrt_u64(R - 1) : 0, fresh);
-    ctx->h_jobs.assign(1, make_job(L, R, ctx->S, 0));
-    const uint64_t nseg = ctx->h_jobs[0].nseg;
-    uint32_t* dps = nullptr;
-    const bool dev_out = flags & WS_OUT_DEVICE;
-    if (per_seg) {
-      if (dev_out) {
-        if (per_seg_cap < nseg) throw Fail{WS_CAPACITY, "per_seg capacity below segment count"};
-        dps = per_seg;
-      } else {
-        ctx->per_seg.reserve(nseg, "per_seg");
-        dps = ctx->per_seg.ptr;
-      }
-    }
-    const int mode = (flags & WS_WANT_CHECKS) ? wsk::kCountChecks : wsk::kCount;
-    run_sieve(ctx, mode, dps, nullptr, 0, true);
-    if (per_seg && !dev_out)
-      ck(copy_async(ctx, per_seg, dps, std::min(nseg, per_seg_cap) * sizeof(uint32_t),
-                         cudaMemcpyDeviceToHost, ctx->stream), "per_seg");
-    const wsk::JobAcc a = *fetch_results(ctx, 1);
-    out->count = a.count;
-    out->sum = a.sum;
-    out->xor_ = a.xr;
-    out->largest = a.largest;
-    add_prelude(L, R, out);
-    if (n_seg) *n_seg = nseg;
-    ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
-    ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
+    if (ctx->nccl)
+      count_range_multi(ctx, L, R, flags, out, per_seg, per_seg_cap, n_seg);
+    else
+      count_range_single(ctx->devs[0], L, R, flags, out, per_seg, per_seg_cap, n_seg);
   });
 }
 
 ws_status ws_enumerate_range(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, uint64_t* out,
                              uint64_t cap, uint64_t* n_out, ws_checks* checks) {
-  ws_status st = guarded(ctx, [&] {
+  return guarded(ctx, [&] {
     if (!n_out) throw Fail{WS_BAD_CONFIG, "null n_out"};
     *n_out = 0;
-    ws_checks chk{};
-    if (checks) *checks = chk;
+    if (checks) *checks = ws_checks{};
     if (R <= L) return;
     if (!out && cap) throw Fail{WS_BAD_CONFIG, "null output with nonzero capacity"};
-    validate_range(L, R);
-    ensure_base(ctx, R >= 2 ? isqrt_u64(R - 1) : 0, flags & WS_FRESH_BASE);
-    uint64_t pre[2];
-    uint64_t npre = 0;
-    for (uint64_t v : {uint64_t{2}, uint64_t{3}})
-      if (v >= L && v < R) pre[npre++] = v;
-    ctx->h_jobs.assign(1, make_job(L, R, ctx->S, 0));
-    const bool dev_out = flags & WS_OUT_DEVICE;
-    if (dev_out && out && !is_device_ptr(out))
-      throw Fail{WS_BAD_CONFIG, "WS_OUT_DEVICE with a non-device pointer"};
-    unsigned long long* dst;
-    uint64_t dcap;
-    if (dev_out) {
-      dst = reinterpret_cast<unsigned long long*>(out) + std::min(npre, cap);
-      dcap = cap > npre ? cap - npre : 0;
-      if (npre && cap)
-        ck(copy_async(ctx, out, pre, std::min(npre, cap) * 8, cudaMemcpyHostToDevice,
-                      ctx->stream), "prelude");
-    } else {
-      for (uint64_t i = 0; i < npre && i < cap; ++i) out[i] = pre[i];
-      enumerate_to_host(ctx, L, R, out + std::min(npre, cap), cap > npre ? cap - npre : 0, &chk);
-      add_prelude(L, R, &chk);
-      *n_out = chk.count;
-      if (checks) *checks = chk;
-      ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
-      ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
-      if (chk.count > cap) throw Fail{WS_CAPACITY, "output capacity below the prime count"};
-      return;
-    }
-    run_sieve(ctx, wsk::kEnumerate, nullptr, dst, dcap, true);
-    const wsk::JobAcc a = *fetch_results(ctx, 1);
-    chk.count = a.count;
-    chk.sum = a.sum;
-    chk.xor_ = a.xr;
-    chk.largest = a.largest;
-    add_prelude(L, R, &chk);
-    *n_out = chk.count;
-    if (checks) *checks = chk;
-    ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
-    ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
-    if (chk.count > cap) throw Fail{WS_CAPACITY, "output capacity below the prime count"};
+    if (ctx->nccl)
+      enumerate_multi(ctx, L, R, flags, out, cap, n_out, checks);
+    else
+      enumerate_single(ctx->devs[0], L, R, flags, out, cap, n_out, checks);
   });
-  return st;
+}
+
+ws_status ws_enumerate_shards(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags,
+                              uint64_t* const* outs, const uint64_t* caps, uint64_t* counts,
+                              ws_checks* checks) {
+  return guarded(ctx, [&] {
+    if (!outs || !caps || !counts) throw Fail{WS_BAD_CONFIG, "null shard arrays"};
+    for (size_t i = 0; i < ctx->devs.size(); ++i) counts[i] = 0;
+    if (checks) *checks = ws_checks{};
+    if (!ctx->nccl) throw Fail{WS_BAD_CONFIG, "ws_enumerate_shards needs a multi-device context"};
+    if (R <= L) return;
+    enumerate_shards(ctx, L, R, flags, outs, caps, counts, checks);
+  });
 }
 
 ws_status ws_base_primes(ws_ctx* ctx, uint64_t B, uint32_t flags, uint64_t* out, uint64_t cap,
@@ -1293,18 +1579,19 @@ ws_status ws_base_primes(ws_ctx* ctx, uint64_t B, uint32_t flags, uint64_t* out,
     if (B < 2) throw Fail{WS_EMPTY_RANGE, "no primes below 2"};  // wheel.cpp:41
     if (B > 0xFFFFFFFFull) throw Fail{WS_CAPACITY, "base bound above 2^32"};
     // the store's entries are the wheel primes 5 <= p <= B (base_store.cpp:34-42):
-    // enumerate [5, B + 1) on the device
+    // enumerate [5, B + 1) on the (first) device
     if (B < 5) return;
+    if (!out && cap) throw Fail{WS_BAD_CONFIG, "null output with nonzero capacity"};
     ws_checks chk{};
-    const uint32_t f = (flags & (WS_OUT_DEVICE | WS_FRESH_BASE));
-    const ws_status st = ws_enumerate_range(ctx, 5, B + 1, f, out, cap, n, &chk);
-    if (st != WS_OK) throw Fail{st, ctx->err};
+    enumerate_single(ctx->devs[0], 5, B + 1, flags & (WS_OUT_DEVICE | WS_FRESH_BASE), out, cap, n,
+                     &chk);
   });
 }
 
 ws_status ws_sieve_segment(ws_ctx* ctx, uint64_t start, uint64_t len, uint32_t flags,
                            uint64_t* r1_words, uint64_t* r5_words) {
   return guarded(ctx, [&] {
+    DevCtx* d = ctx->devs[0];
     // SegmentBitmap checks, segment.cpp:101-110
     if (start % 6 != 0) throw Fail{WS_ALIGNMENT, "segment start is not a multiple of 6"};
     if (len == 0) throw Fail{WS_DOMAIN, "segment must span at least one wheel index"};
@@ -1312,42 +1599,42 @@ ws_status ws_sieve_segment(ws_ctx* ctx, uint64_t start, uint64_t len, uint32_t f
       throw Fail{WS_OVERFLOW, "segment end exceeds the 64-bit value range"};
     if (!r1_words || !r5_words) throw Fail{WS_BAD_CONFIG, "null output"};
     const uint64_t end = start + 6 * len;
-    ensure_base(ctx, isqrt_u64(end - 1), flags & WS_FRESH_BASE);
-    ctx->h_jobs.assign(1, make_job(start, end, ctx->S, 0));
-    const uint64_t nseg = ctx->h_jobs[0].nseg;
-    const uint64_t words32 = nseg * (ctx->S / 32);
+    ensure_base(d, isqrt_u64(end - 1), flags & WS_FRESH_BASE);
+    d->h_jobs.assign(1, make_job(start, end, d->S, 0));
+    const uint64_t nseg = d->h_jobs[0].nseg;
+    const uint64_t words32 = nseg * (d->S / 32);
     const uint64_t out64 = (len + 63) / 64;
     const bool dev_out = flags & WS_OUT_DEVICE;
     DevBuf<uint32_t> tmp;
     tmp.reserve(2 * words32 + 2, "bitmap words");
-    ctx->words_out[0] = tmp.ptr;
-    ctx->words_out[1] = tmp.ptr + words32;
+    d->words_out[0] = tmp.ptr;
+    d->words_out[1] = tmp.ptr + words32;
     try {
-      run_sieve(ctx, wsk::kCount, nullptr, nullptr, 0, true);
+      run_sieve(d, wsk::kCount, nullptr, nullptr, 0, true);
     } catch (...) {
-      ctx->words_out[0] = ctx->words_out[1] = nullptr;
+      d->words_out[0] = d->words_out[1] = nullptr;
       tmp.release();
       throw;
     }
-    ctx->words_out[0] = ctx->words_out[1] = nullptr;
+    d->words_out[0] = d->words_out[1] = nullptr;
     // uint32 LSB-first words are byte-identical to FlagArray's uint64 words
     const cudaMemcpyKind k = dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    ck(copy_async(ctx, r1_words, tmp.ptr, out64 * 8, k, ctx->stream), "r1 words");
-    ck(copy_async(ctx, r5_words, tmp.ptr + words32, out64 * 8, k, ctx->stream), "r5 words");
-    fetch_results(ctx, 1);
+    ck(copy_async(d, r1_words, tmp.ptr, out64 * 8, k, d->stream), "r1 words");
+    ck(copy_async(d, r5_words, tmp.ptr + words32, out64 * 8, k, d->stream), "r5 words");
+    fetch_results(d, 1);
     tmp.release();
     // sieve_segment leaves the value 1 set; callers clear it (engine.cpp:244)
     if (start == 0) {
       if (dev_out) {
         uint64_t w0 = 0;
-        ck(copy_sync(ctx, &w0, r1_words, 8, cudaMemcpyDeviceToHost), "w0");
+        ck(copy_sync(d, &w0, r1_words, 8, cudaMemcpyDeviceToHost), "w0");
         w0 |= 1;
-        ck(copy_sync(ctx, r1_words, &w0, 8, cudaMemcpyHostToDevice), "w0");
+        ck(copy_sync(d, r1_words, &w0, 8, cudaMemcpyHostToDevice), "w0");
       } else {
         r1_words[0] |= 1;
       }
     }
-    ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
+    d->timing.sieve_ms = event_ms(d->ev[2], d->ev[3]);
   });
 }
 
@@ -1358,54 +1645,71 @@ ws_status ws_count_intervals(ws_ctx* ctx, const uint64_t* Ls, uint64_t n, uint64
     if (!Ls || !counts) throw Fail{WS_BAD_CONFIG, "null interval arrays"};
     if (width == 0) throw Fail{WS_EMPTY_RANGE, "zero-width intervals"};
     const bool dev_out = flags & WS_OUT_DEVICE;
+    if (dev_out && ctx->nccl)
+      throw Fail{WS_BAD_CONFIG, "WS_OUT_DEVICE intervals need a single-device context"};
+    DevCtx* d0 = ctx->devs[0];
     std::vector<uint64_t> hL;
     const uint64_t* L = Ls;
     if (dev_out) {
       hL.resize(n);
-      ck(copy_sync(ctx, hL.data(), Ls, n * 8, cudaMemcpyDeviceToHost), "intervals in");
+      ck(copy_sync(d0, hL.data(), Ls, n * 8, cudaMemcpyDeviceToHost), "intervals in");
       L = hL.data();
     }
-    uint64_t maxR = 0, seg = 0;
-    ctx->h_jobs.clear();
-    ctx->h_jobs.reserve(n);
+    std::vector<std::pair<uint64_t, uint64_t>> ranges(n);
     for (uint64_t i = 0; i < n; ++i) {
       if (L[i] > kMaxSegmentEnd - width) throw Fail{WS_OVERFLOW, "interval end overflows"};
-      const uint64_t R = L[i] + width;
-      maxR = std::max(maxR, R);
-      ctx->h_jobs.push_back(make_job(L[i], R, ctx->S, seg));
-      seg += ctx->h_jobs.back().nseg;
+      ranges[i] = {L[i], L[i] + width};
     }
-    ensure_base(ctx, maxR >= 2 ? isqrt_u64(maxR - 1) : 0, flags & WS_FRESH_BASE);
-    // ensure_base may have used h_jobs for the base sieve: rebuild
-    ctx->h_jobs.clear();
-    seg = 0;
-    for (uint64_t i = 0; i < n; ++i) {
-      ctx->h_jobs.push_back(make_job(L[i], L[i] + width, ctx->S, seg));
-      seg += ctx->h_jobs.back().nseg;
-    }
-    const bool checks = sums || xors;
-    run_sieve(ctx, checks ? wsk::kCountChecks : wsk::kCount, nullptr, nullptr, 0, true);
-    const wsk::JobAcc* acc = fetch_results(ctx, n);
+    const uint64_t G = ctx->nshards;
+    std::vector<ws_checks> res;
+    // interval i -> shard i mod G, at slot i / G of that shard's records
+    count_jobs(ctx, ranges, sums || xors, flags & WS_FRESH_BASE,
+               [G](uint64_t i) { return static_cast<uint32_t>(i % G); }, (n + G - 1) / G,
+               [G](uint64_t i) { return i / G; }, res);
     std::vector<uint32_t> hc(n);
     std::vector<uint64_t> hs(n), hx(n);
     for (uint64_t i = 0; i < n; ++i) {
-      ws_checks o{acc[i].count, acc[i].sum, acc[i].xr, acc[i].largest};
-      add_prelude(L[i], L[i] + width, &o);
-      hc[i] = static_cast<uint32_t>(o.count);
-      hs[i] = o.sum;
-      hx[i] = o.xor_;
+      hc[i] = static_cast<uint32_t>(res[i].count);
+      hs[i] = res[i].sum;
+      hx[i] = res[i].xor_;
     }
     if (dev_out) {
-      ck(copy_sync(ctx, counts, hc.data(), n * 4, cudaMemcpyHostToDevice), "counts");
-      if (sums) ck(copy_sync(ctx, sums, hs.data(), n * 8, cudaMemcpyHostToDevice), "sums");
-      if (xors) ck(copy_sync(ctx, xors, hx.data(), n * 8, cudaMemcpyHostToDevice), "xors");
+      ck(copy_sync(d0, counts, hc.data(), n * 4, cudaMemcpyHostToDevice), "counts");
+      if (sums) ck(copy_sync(d0, sums, hs.data(), n * 8, cudaMemcpyHostToDevice), "sums");
+      if (xors) ck(copy_sync(d0, xors, hx.data(), n * 8, cudaMemcpyHostToDevice), "xors");
     } else {
       std::memcpy(counts, hc.data(), n * 4);
       if (sums) std::memcpy(sums, hs.data(), n * 8);
       if (xors) std::memcpy(xors, hx.data(), n * 8);
     }
-    ctx->timing.base_ms = ctx->base_built ? event_ms(ctx->ev[0], ctx->ev[1]) : 0.0;
-    ctx->timing.sieve_ms = event_ms(ctx->ev[2], ctx->ev[3]);
+  });
+}
+
+ws_status ws_count_ranges(ws_ctx* ctx, const uint64_t* Ls, const uint64_t* Rs, uint64_t n,
+                          uint32_t flags, ws_checks* out) {
+  return guarded(ctx, [&] {
+    if (n == 0) return;
+    if (!Ls || !Rs || !out) throw Fail{WS_BAD_CONFIG, "null range arrays"};
+    std::vector<std::pair<uint64_t, uint64_t>> ranges(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      if (Rs[i] > Ls[i]) validate_range(Ls[i], Rs[i]);
+      ranges[i] = {Ls[i], Rs[i]};
+    }
+    // contiguous blocks: shard g takes ranges [floor(g n / G), floor((g+1) n / G))
+    const uint64_t G = ctx->nshards;
+    auto first = [n, G](uint64_t g) {
+      return static_cast<uint64_t>(static_cast<unsigned __int128>(g) * n / G);
+    };
+    auto owner = [n, G, first](uint64_t i) {
+      uint64_t g = static_cast<uint64_t>(static_cast<unsigned __int128>(i) * G / n);
+      while (g + 1 < G && first(g + 1) <= i) ++g;
+      while (g > 0 && first(g) > i) --g;
+      return static_cast<uint32_t>(g);
+    };
+    std::vector<ws_checks> res;
+    count_jobs(ctx, ranges, flags & WS_WANT_CHECKS, flags & WS_FRESH_BASE, owner,
+               (n + G - 1) / G, [&](uint64_t i) { return i - first(owner(i)); }, res);
+    std::memcpy(out, res.data(), n * sizeof(ws_checks));
   });
 }
 

@@ -61,7 +61,7 @@ struct SieveParams {
   uint64_t s_begin;      // this launch sieves segments [s_begin, s_begin + s_count)
   uint64_t s_count;
   uint32_t S;                        // wheel slots per class per segment (power of two)
-  const uint32_t* prime_p;           // sieving primes >= 37, ascending
+  const uint32_t* prime_p;           // sieving primes >= 53 (kFirstTablePrime), ascending
   const unsigned long long* prime_m; // floor((2^64-1)/p), Barrett reciprocal (ks >= 2^53)
   const double* prime_inv;           // fl(1/p), FP64 quotient estimate (ks < 2^53)
   uint32_t nprimes;                  // host-side upper bound on the table size

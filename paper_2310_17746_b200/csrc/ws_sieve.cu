@@ -242,7 +242,7 @@ __device__ void fetch_segment(const SieveParams& P, SegInfo& si) {
   si.t_hi = isqrt64(6 * (si.ks + si.len));
 }
 
-// Phase 1: stamp primes 5..31 and the [L, R) trim into every word.  The
+// Phase 1: stamp primes 5..47 and the [L, R) trim into every word.  The
 // bitmaps hold COMPOSITE flags (bit set = crossed off or outside [L, R)):
 // the complement of the reference's FlagArray, so crossing off is a single
 // ATOMS.OR and survivors are ~word.

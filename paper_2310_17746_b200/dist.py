@@ -1,10 +1,12 @@
-"""Multi-GPU plumbing: one process per GPU, contiguous super-ranges, and the
-single end-of-run combine of {count, Σ mod 2^64, ⊕, largest}.
+"""torch.distributed mirror of the library's multi-device combine, for
+callers that shard [L, R) across their own processes instead of handing
+devices to one ws_ctx (the library's own path: Sieve(devices=..., world=...),
+which runs ONE ncclAllGather inside libwheelsieve_cuda.so).
 
-NCCL has no XOR reduction, so the combine is one all_gather of a 4-word
-record per rank (4 x int64 = 32 B), reduced on the host: count and Σ wrap
-mod 2^64, ⊕ folds, largest is a max.  Works with the nccl backend (GPU
-tensors) and gloo (CPU tensors, used by the CPU tests).
+Same contract as the library: contiguous ws_partition super-ranges, and one
+all_gather of the 32-byte record {count, sum, xor, largest} per rank folded
+by ws_combine_checks (NCCL has no XOR reduction).  Works with the nccl
+backend (GPU tensors) and gloo (CPU tensors, used by the CPU tests).
 """
 from __future__ import annotations
 
@@ -12,7 +14,7 @@ from typing import Callable, Optional
 
 import numpy as np
 
-from .wheelsieve import Checks, partition
+from .wheelsieve import Checks, combine_checks as _fold, partition
 
 MASK = (1 << 64) - 1
 
@@ -39,11 +41,7 @@ def combine_checks(local: Checks, group=None) -> Checks:
     out = [torch.empty_like(rec) for _ in range(world)]
     dist.all_gather(out, rec, group=group)
     allr = torch.stack(out).cpu().numpy().view(np.uint64)
-    count = int(allr[:, 0].sum(dtype=np.uint64))
-    s = int(allr[:, 1].sum(dtype=np.uint64))
-    x = int(np.bitwise_xor.reduce(allr[:, 2]))
-    lg = int(allr[:, 3].max())
-    return Checks(count, s, x, lg)
+    return _fold([Checks(*(int(v) for v in row)) for row in allr])
 
 
 def max_over_ranks(v: float, group=None) -> float:

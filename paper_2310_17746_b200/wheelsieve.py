@@ -26,7 +26,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import WS_FRESH_BASE, WS_OUT_DEVICE, WS_WANT_CHECKS, WsChecks, WsOpts, WsTiming
+from ._lib import (WS_FRESH_BASE, WS_MAX_DEVICES, WS_NCCL_ID_BYTES, WS_OUT_DEVICE, WS_WANT_CHECKS,
+                   WsChecks, WsOpts, WsTiming)
 
 lib = _lib.lib
 
@@ -53,6 +54,7 @@ class Errc(enum.IntEnum):
     Cuda = 99
     NoDevice = 100
     OutOfMemory = 101
+    Nccl = 102
 
 
 class Error(RuntimeError):
@@ -150,6 +152,29 @@ class Checks:
     def of(c: WsChecks) -> "Checks":
         return Checks(c.count, c.sum, c.xor_, c.largest)
 
+    def raw(self) -> WsChecks:
+        M = (1 << 64) - 1
+        return WsChecks(self.count & M, self.sum & M, self.xor & M, self.largest & M)
+
+
+def combine_checks(records: Sequence[Checks]) -> Checks:
+    """ws_combine_checks: the fold a multi-device context applies to the
+    gathered per-shard records (count and sum add mod 2^64, xor folds,
+    largest is the maximum)."""
+    arr = (WsChecks * max(1, len(records)))(*[r.raw() for r in records])
+    out = WsChecks()
+    _check(lib.ws_combine_checks(C.addressof(arr), len(records), C.byref(out)),
+           what="combine_checks")
+    return Checks.of(out)
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (WS_NCCL_ID_BYTES bytes) for a multi-process
+    context; made on rank 0 and broadcast to the other ranks' Sieve(...)."""
+    buf = (C.c_uint8 * WS_NCCL_ID_BYTES)()
+    _check(lib.ws_nccl_unique_id(C.addressof(buf)), what="nccl_unique_id")
+    return bytes(buf)
+
 
 def _ptr(a) -> int:
     """Data pointer of a numpy array or a torch tensor."""
@@ -163,19 +188,69 @@ def _is_device(a) -> bool:
 
 
 class Sieve:
-    """One GPU context (device buffers, stream, resident base-prime table).
+    """A GPU context (device buffers, streams, resident base-prime tables).
 
-    Not reentrant: use one Sieve per host thread / rank."""
+    ``Sieve(device=d)`` drives one device with no NCCL.  ``Sieve(devices=[...])``
+    drives several devices of this process, one shard each, combined by one
+    NCCL all-gather inside the library; with ``world > 1`` (one Sieve per
+    process, ``nccl_id`` from ``nccl_unique_id()`` on rank 0) the shards of
+    all processes form one job.  Not reentrant: one Sieve per
+    host thread."""
 
-    def __init__(self, device: int = -1, segment_slots: int = DEFAULT_SEGMENT_SLOTS):
+    def __init__(self, device: int = -1, segment_slots: int = DEFAULT_SEGMENT_SLOTS,
+                 devices: Optional[Sequence[int]] = None, world: int = 1, rank: int = 0,
+                 nccl_id: Optional[bytes] = None):
         o = WsOpts()
         lib.ws_opts_default(C.byref(o))
         o.segment_slots = segment_slots
         o.device = device
+        if devices is not None:
+            devices = list(devices)
+            if not 1 <= len(devices) <= WS_MAX_DEVICES:
+                raise Error(Errc.BadConfig, f"1..{WS_MAX_DEVICES} devices, got {len(devices)}")
+            o.n_devices = len(devices)
+            for i, d in enumerate(devices):
+                o.device_ids[i] = d
+            o.world = world
+            o.rank = rank
+            if world > 1:
+                if nccl_id is None or len(nccl_id) != WS_NCCL_ID_BYTES:
+                    raise Error(Errc.BadConfig, "world > 1 needs the rank-0 nccl_unique_id()")
+                for i, b in enumerate(nccl_id):
+                    o.nccl_id[i] = b
+        elif world != 1:
+            raise Error(Errc.BadConfig, "a multi-process context needs devices=[...]")
         h = C.c_void_p()
         _check(lib.ws_ctx_create(C.byref(o), C.byref(h)), what="ws_ctx_create")
         self._h = h
         self.segment_slots = segment_slots
+
+    @property
+    def num_devices(self) -> int:
+        return int(lib.ws_ctx_num_devices(self._h))
+
+    @property
+    def num_shards(self) -> int:
+        return int(lib.ws_ctx_num_shards(self._h))
+
+    @property
+    def devices(self) -> List[int]:
+        return [int(lib.ws_ctx_device(self._h, i)) for i in range(self.num_devices)]
+
+    @property
+    def streams(self) -> List[int]:
+        return [lib.ws_ctx_device_stream(self._h, i) or 0 for i in range(self.num_devices)]
+
+    def device_timing(self, i: int) -> WsTiming:
+        t = WsTiming()
+        _check(lib.ws_device_timing(self._h, i, C.byref(t)), self._h, "device_timing")
+        return t
+
+    def comm_info(self, i: int = 0):
+        """(ranks in local device i's NCCL communicator, its rank there)."""
+        n, r = C.c_int32(), C.c_int32()
+        _check(lib.ws_ctx_comm_info(self._h, i, C.byref(n), C.byref(r)), self._h, "comm_info")
+        return n.value, r.value
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -263,6 +338,36 @@ class Sieve:
                                       xors.ctypes.data if xors is not None else None),
                self._h, "count_intervals")
         return counts, sums, xors
+
+    def enumerate_shards(self, L: int, R: int, outs, fresh_base: bool = False):
+        """Multi-device: local device i enumerates its shard of [L, R) into
+        outs[i] (a CUDA tensor on that device).  Returns (counts, Checks)."""
+        n = self.num_devices
+        if len(outs) != n:
+            raise Error(Errc.BadConfig, f"{n} output tensors needed")
+        ptrs = (C.c_uint64 * n)(*[o.data_ptr() for o in outs])
+        caps = (C.c_uint64 * n)(*[o.numel() for o in outs])
+        counts = (C.c_uint64 * n)()
+        chk = WsChecks()
+        _check(lib.ws_enumerate_shards(self._h, L, R, WS_FRESH_BASE if fresh_base else 0,
+                                       C.addressof(ptrs), C.addressof(caps), C.addressof(counts),
+                                       C.byref(chk)), self._h, "enumerate_shards")
+        return [int(c) for c in counts], Checks.of(chk)
+
+    def count_ranges(self, Ls, Rs, checks: bool = False, fresh_base: bool = False):
+        """Per-range Checks of [Ls[i], Rs[i]) (each sieved independently; the
+        per-worker-tile counts of run())."""
+        Ls = np.ascontiguousarray(Ls, dtype=np.uint64)
+        Rs = np.ascontiguousarray(Rs, dtype=np.uint64)
+        if Ls.shape != Rs.shape:
+            raise Error(Errc.BadConfig, "Ls and Rs differ in length")
+        n = Ls.size
+        out = (WsChecks * max(1, n))()
+        flags = (WS_WANT_CHECKS if checks else 0) | (WS_FRESH_BASE if fresh_base else 0)
+        _check(lib.ws_count_ranges(self._h, Ls.ctypes.data, Rs.ctypes.data, n, flags,
+                                   C.addressof(out)),
+               self._h, "count_ranges")
+        return [Checks.of(out[i]) for i in range(n)]
 
     def base_primes(self, B: int, fresh_base: bool = False) -> np.ndarray:
         """BasePrimeStore::bootstrap entries: wheel primes 5 <= p <= B (device-sieved)."""
@@ -444,18 +549,51 @@ def _sieve() -> Sieve:
 
 
 _WIDTH_BYTES = {0: lambda n: (n + 7) // 8, 1: lambda n: n, 2: lambda n: 4 * n}
-_CHUNK_INTEGERS = 1 << 28  # integers sieved per device call for value sinks
+_CALL_VALUES = 1 << 28   # integers enumerated per device call for value sinks
+_CALL_COUNT = 1 << 36    # integers counted per device call for count sinks ...
+_CALL_TILES = 1 << 16    # ... and at most this many worker tiles per call
 
 
-def _account(config: SieveConfig, seg_lo: int, seg_hi: int, rep: SieveReport) -> None:
-    """Analytic flag-storage accounting of one iteration (engine.cpp:218-230)."""
+@dataclass
+class WorkerAssignment:  # engine.hpp:34-40
+    iteration: int
+    worker: int
+    lo: int
+    hi: int
+
+
+def plan_iteration(config: SieveConfig, iteration: int) -> List[WorkerAssignment]:
+    """engine.cpp:322-342: iteration i = [i S, (i+1) S) cut into `threads`
+    equal tiles in worker order."""
+    if config.threads == 0 or config.threads > config.thread_cap:
+        raise Error(Errc.BadConfig, "invalid thread count")
+    span, align = config.segment_span, 6 * config.threads
+    if span == 0 or span % align or span > K_MAX_SEGMENT_END:
+        raise Error(Errc.BadConfig, f"segment span {span} is not a positive multiple of {align}")
+    if iteration > K_MAX_SEGMENT_END // span - 1:
+        raise Error(Errc.Overflow, f"iteration {iteration} leaves the 64-bit value range")
+    sub = span // config.threads
+    return [WorkerAssignment(iteration, j, iteration * span + j * sub,
+                             iteration * span + (j + 1) * sub) for j in range(config.threads)]
+
+
+def _tiles(config: SieveConfig, seg_lo: int, seg_hi: int):
+    """The non-empty worker tiles of one iteration, clipped to seg_hi
+    (engine.cpp:233-241)."""
     sub = config.segment_span // config.threads
-    ent = byt = 0
+    out = []
     for j in range(config.threads):
         lo = seg_lo + j * sub
         if lo >= seg_hi:
             break
-        hi = min(lo + sub, seg_hi)
+        out.append((lo, seg_hi if sub > seg_hi - lo else lo + sub))
+    return out
+
+
+def _account(config: SieveConfig, tiles, rep: SieveReport) -> None:
+    """Analytic flag-storage accounting of one iteration (engine.cpp:218-230)."""
+    ent = byt = 0
+    for lo, hi in tiles:
         n = (hi - lo) // 6
         ent += 2 * n
         byt += 2 * _WIDTH_BYTES[config.flag_width](n)
@@ -464,9 +602,14 @@ def _account(config: SieveConfig, seg_lo: int, seg_hi: int, rep: SieveReport) ->
 
 
 def _run_loop(config: SieveConfig, stop, sv: Sieve) -> SieveReport:
-    """engine.cpp:149-307 on the device: the same iteration structure and
-    emission (2 and 3 first, one ascending batch per segment_span iteration),
-    with many iterations sieved per device call and batches cut on the host."""
+    """engine.cpp:149-307 on the device, with the reference's emission
+    granularity: 2 and 3 first, then for every iteration one batch per
+    non-empty worker tile in worker order -- ``emit(values)`` for value
+    sinks, ``emit_count(count, largest)`` for count sinks (engine.cpp:277-288).
+    The device sieves a block of iterations per call (every tile of the block
+    as one ws_count_ranges batch, or one ordered enumeration cut at the tile
+    borders on the host); emission and the stop check still go iteration by
+    iteration, so a sink sees exactly the reference's batches."""
     bounded = stop is None
     _validate(config, bounded)
     sink = config.sink
@@ -475,15 +618,15 @@ def _run_loop(config: SieveConfig, stop, sv: Sieve) -> SieveReport:
     limit = config.limit if bounded else 0
     limit_end = (limit // 6 + 1) * 6 if bounded else K_MAX_SEGMENT_END
     total_iters = limit_end // span + (limit_end % span != 0) if bounded else None
+    top_value = limit + 1 if bounded else K_MAX_SEGMENT_END
     rep = SieveReport()
     want_values = sink.wants_values()
-    per_call = max(1, _CHUNK_INTEGERS // span)
-    vals = np.zeros(0, np.uint64)
-    vpos = 0
-    count_total = count_largest = 0
-    if bounded and not want_values:
-        c = sv.count_range(0, limit + 1)
-        count_total, count_largest = c.count, c.largest
+    if want_values:
+        per_call = max(1, _CALL_VALUES // span)
+    else:
+        per_call = max(1, min(_CALL_COUNT // span, _CALL_TILES // config.threads))
+    block: dict = {}
+    block_end = 0
     i = 0
     seg_lo = 0
     try:
@@ -497,39 +640,51 @@ def _run_loop(config: SieveConfig, stop, sv: Sieve) -> SieveReport:
                 rep.overflowed = True
                 break
             seg_hi = limit_end if (bounded and span > limit_end - seg_lo) else seg_lo + span
-            _account(config, seg_lo, seg_hi, rep)
+            tiles = _tiles(config, seg_lo, seg_hi)
+            _account(config, tiles, rep)
+            if i >= block_end:  # sieve the next block of iterations on the device
+                n_it = min(per_call, (K_MAX_SEGMENT_END - seg_lo) // span)
+                if bounded:
+                    n_it = min(n_it, total_iters - i)
+                bhi = min(seg_lo + n_it * span, limit_end)
+                blk_tiles = [t for k in range(n_it)
+                             for t in _tiles(config, seg_lo + k * span,
+                                             min(seg_lo + (k + 1) * span, bhi))]
+                if want_values:
+                    lo_v, hi_v = max(seg_lo, 4), min(bhi, top_value)
+                    vals = sv.enumerate_range(lo_v, hi_v)[0] if lo_v < hi_v else \
+                        np.zeros(0, np.uint64)
+                    block = {"vals": vals}
+                else:
+                    Ls = [max(lo, 4) for lo, _ in blk_tiles]
+                    Rs = [max(max(lo, 4), min(hi, top_value)) for lo, hi in blk_tiles]
+                    res = sv.count_ranges(Ls, Rs)
+                    block = {(lo, hi): r for (lo, hi), r in zip(blk_tiles, res)}
+                block_end = i + n_it
             if i == 0:  # engine.cpp:268-276
                 n = 2 if (not bounded or limit >= 3) else 1
                 if want_values:
                     sink.emit(np.array([2, 3][:n], np.uint64))
                 else:
                     sink.emit_count(n, 3 if n == 2 else 2)
-            if want_values:
-                if i % per_call == 0:
-                    blo = max(seg_lo, 4)
-                    bhi = seg_lo + min(per_call, (K_MAX_SEGMENT_END - seg_lo) // span) * span
-                    if bounded:
-                        bhi = min(bhi, limit + 1)
-                    vals = sv.enumerate_range(blo, bhi)[0] if blo < bhi else np.zeros(0, np.uint64)
-                    vpos = 0
-                top = min(seg_hi, limit + 1) if bounded else seg_hi
-                end = int(np.searchsorted(vals, np.uint64(top), side="left"))
-                if end > vpos:
-                    sink.emit(vals[vpos:end])
-                vpos = end
-            elif bounded:
-                if i + 1 == total_iters and count_total > 2:
-                    sink.emit_count(count_total - 2, count_largest)
-            else:
-                c = sv.count_range(max(seg_lo, 4), seg_hi)
-                if c.count:
-                    sink.emit_count(c.count, c.largest)
+            for lo, hi in tiles:
+                if want_values:
+                    v = block["vals"]
+                    a = int(np.searchsorted(v, np.uint64(lo), side="left"))
+                    b = int(np.searchsorted(v, np.uint64(min(hi, top_value)), side="left"))
+                    if b > a:
+                        sink.emit(v[a:b])
+                else:
+                    r = block[(lo, hi)]
+                    if r.count:
+                        sink.emit_count(r.count, r.largest)
             rep.iterations = i + 1
             rep.sieved_to = seg_hi
             i += 1
             seg_lo += span
     except Error as e:
-        if isinstance(e, SinkFailure) or e.code in (Errc.Cuda, Errc.NoDevice, Errc.OutOfMemory):
+        if isinstance(e, SinkFailure) or e.code in (Errc.Cuda, Errc.NoDevice, Errc.OutOfMemory,
+                                                     Errc.Nccl):
             raise
         rep.prime_count = sink.count()
         rep.largest_prime = sink.largest()
@@ -569,7 +724,10 @@ class PrimeStream:
             raise Error(Errc.Overflow, "segment span exceeds the 64-bit value range")
         self._sv = sieve or _sieve()
         self._len = segment_wheel_len
-        self._span = 6 * segment_wheel_len * max(1, segments_per_refill)
+        # refills batch whole segments up to a value budget (a single segment
+        # may exceed it, as the reference's own buffer would)
+        per = max(1, min(segments_per_refill, _CALL_VALUES // (6 * segment_wheel_len)))
+        self._span = 6 * segment_wheel_len * per
         self._next = 0
         self._buf = np.zeros(0, np.uint64)
         self._pos = 0

@@ -61,7 +61,6 @@ def test_config2_enumeration_checksums(sieve, golden):
     v = out[:n]
     assert bool((v[1:] > v[:-1]).all())  # strictly ascending
     # the device array carries exactly the primes the checksums describe
-    assert int(v.sum().item()) % 2**64 == rec["sum"] % 2**64 or True  # int64 wraps
     assert int(v[-1].item()) == rec["largest"] and int(v[0].item()) == 2
     host = v.cpu().numpy().view(np.uint64)
     assert int(host.sum(dtype=np.uint64)) == rec["sum"]
