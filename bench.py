@@ -657,6 +657,10 @@ def run_reference(args, cfg, world, rank):
 
 
 def main():
+    # NCCL's banner and init log go to stderr (stdout carries the one JSON
+    # line); INFO makes every communicator's rank count visible there
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

@@ -204,7 +204,9 @@ ws_status ws_sieve_segment(ws_ctx* ctx, uint64_t start, uint64_t len, uint32_t f
                            uint64_t* r1_words, uint64_t* r5_words);
 
 /* Chunked prime store (ChunkedFileSink, sink.hpp:68-141):
- * enumerate [L, R) on the device and write primes_%05llu.{txt,bin} chunk
+ * enumerate [L, R) on the device -- in value windows of ~2^30 integers, so
+ * device and pinned host memory stay bounded (~0.5 GB each) at any range --
+ * and stream primes_%05llu.{txt,bin} chunk
  * files of primes_per_file values plus manifest.json (count/min/max/crc32 per
  * file, format, total_count, frontier = R), byte-identical to the reference
  * CLI's `sieve --out` for [0, limit + 1).  Binary chunks' CRC-32s are
@@ -214,6 +216,25 @@ ws_status ws_sieve_segment(ws_ctx* ctx, uint64_t start, uint64_t len, uint32_t f
 #define WS_STORE_BINARY 1u
 ws_status ws_store_range(ws_ctx* ctx, uint64_t L, uint64_t R, const char* dir, uint32_t format,
                          uint64_t primes_per_file, uint64_t* n_out);
+/* Streaming chunk writer (ChunkedFileSink, sink.hpp:68-141, sink.cpp:185-304):
+ * chunk files are opened on demand and closed at primes_per_file values; the
+ * manifest is rewritten (write-then-rename) at every rollover and on flush,
+ * so what it lists is durable.  Memory is bounded by one batch.  Values
+ * must ascend across appends (the caller's sink checks it).  The manifest
+ * frontier is one past the largest value unless set.  ws_store_range uses
+ * the same writer for device-enumerated windows of bounded size (binary
+ * CRCs computed on the device). */
+typedef struct ws_store ws_store;
+ws_status ws_store_open(const char* dir, uint32_t format, uint64_t primes_per_file,
+                        ws_store** out);
+ws_status ws_store_append(ws_store* st, const uint64_t* values, uint64_t n);
+ws_status ws_store_set_frontier(ws_store* st, uint64_t frontier);
+ws_status ws_store_flush(ws_store* st);
+uint64_t ws_store_durable_count(const ws_store* st);
+const char* ws_store_last_error(const ws_store* st);
+/* flushes (best effort: the status reports a failure) and frees */
+ws_status ws_store_close(ws_store* st);
+
 /* read_back (sink.cpp:306-321): primes in [lo, hi) of a store, every touched
  * file verified against its crc32 and count; WS_BEYOND_FRONTIER if hi exceeds
  * the recorded frontier, WS_CHECKSUM_MISMATCH / WS_BAD_MANIFEST / WS_IO. */

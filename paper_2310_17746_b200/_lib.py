@@ -23,6 +23,8 @@ EXPORTS = (
     "ws_read_back", "ws_verify_store", "ws_count_ranges", "ws_nccl_unique_id",
     "ws_ctx_num_devices", "ws_ctx_num_shards", "ws_ctx_device", "ws_ctx_device_stream",
     "ws_device_timing", "ws_ctx_comm_info", "ws_combine_checks", "ws_enumerate_shards",
+    "ws_store_open", "ws_store_append", "ws_store_set_frontier", "ws_store_flush",
+    "ws_store_durable_count", "ws_store_last_error", "ws_store_close",
 )
 
 WS_WANT_CHECKS = 0x1
@@ -55,7 +57,25 @@ class WsTiming(C.Structure):
                 ("h2d_bytes", u64), ("d2h_bytes", u64)]
 
 
+def _preload_nccl() -> None:
+    """libwheelsieve_cuda.so links libnccl.so.2.  If PyTorch's bundled NCCL
+    (nvidia-nccl wheel, newer than the system's) is installed, load it first:
+    whichever libnccl.so.2 enters the process first serves every later user
+    of that soname, and torch needs its own (newer) symbols."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        so = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(so):
+            C.CDLL(so, mode=C.RTLD_GLOBAL)
+            return
+
+
 def _load(path: str = LIB_PATH) -> C.CDLL:
+    _preload_nccl()
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build the CUDA extension first "
@@ -93,6 +113,13 @@ def _load(path: str = LIB_PATH) -> C.CDLL:
         "ws_ctx_comm_info": (C.c_int, [vp, u32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "ws_combine_checks": (C.c_int, [vp, u64, C.POINTER(WsChecks)]),
         "ws_enumerate_shards": (C.c_int, [vp, u64, u64, u32, vp, vp, vp, C.POINTER(WsChecks)]),
+        "ws_store_open": (C.c_int, [C.c_char_p, u32, u64, C.POINTER(vp)]),
+        "ws_store_append": (C.c_int, [vp, vp, u64]),
+        "ws_store_set_frontier": (C.c_int, [vp, u64]),
+        "ws_store_flush": (C.c_int, [vp]),
+        "ws_store_durable_count": (u64, [vp]),
+        "ws_store_last_error": (C.c_char_p, [vp]),
+        "ws_store_close": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

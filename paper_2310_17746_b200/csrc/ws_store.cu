@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <zlib.h>
 
+#include <new>
+
 #include <algorithm>
 #include <charconv>
 #include <cstdio>
@@ -283,123 +285,321 @@ void write_manifest(const fs::path& dir, const Manifest& m) {  // sink.cpp:242-2
 
 }  // namespace
 
-// Device half of the store, called with the values of [L, R) resident on the
-// device (dev, n values): CRC-32 of every file's bytes (binary format).
+// Device half of the store: CRC-32 of byte ranges of device-resident values.
 namespace wsk {
 cudaError_t launch_crc32_ranges(const void* data, const uint64_t* begin, const uint64_t* len,
                                 uint32_t n, uint32_t* out, cudaStream_t st);
 }
 
+// The streaming writer behind ws_store_* and ws_store_range: the
+// ChunkedFileSink life cycle (sink.cpp:185-304) -- files opened on demand,
+// closed at primes_per_file values, the manifest rewritten (write-then-
+// rename) at every rollover and on flush, so everything it lists is durable.
+struct ws_store {
+  fs::path dir;
+  int format = 0;
+  uint64_t per_file = 0;
+  std::vector<FileEntry> closed;
+  std::FILE* fp = nullptr;
+  FileEntry cur;  // the open file (count 0 until its first value)
+  uint64_t next_seq = 0;
+  uint64_t largest = 0;
+  uint64_t frontier = 0;
+  bool frontier_set = false;
+  uint64_t durable = 0;
+  std::string err;
+  std::string text;  // text-format encoding buffer
+
+  std::string durable_note() const { return " (" + std::to_string(durable) + " primes durable)"; }
+
+  void open_next() {
+    cur = FileEntry{};
+    cur.name = chunk_name(next_seq++, format);
+    fp = std::fopen((dir / cur.name).c_str(), "wb");
+    if (!fp) throw StoreFail{WS_IO, "cannot open chunk file " + cur.name + durable_note()};
+    cur.crc32 = static_cast<uint32_t>(::crc32(0, Z_NULL, 0));
+  }
+
+  void write_bytes(const void* p, size_t n) {
+    if (n && std::fwrite(p, 1, n, fp) != n)
+      throw StoreFail{WS_IO, "write to " + cur.name + " failed" + durable_note()};
+  }
+
+  // n ascending values into the open file; crc_known: the CRC-32 of their
+  // little-endian bytes, computed on the device (binary format only)
+  void put(const uint64_t* v, uint64_t n, const uint32_t* crc_known) {
+    if (format == 1) {
+      write_bytes(v, n * 8);  // little-endian host: the words are the bytes
+      if (crc_known) {
+        cur.crc32 = static_cast<uint32_t>(
+            ::crc32_combine(cur.crc32, *crc_known, static_cast<z_off_t>(n * 8)));
+      } else {
+        uLong c = cur.crc32;
+        const auto* b = reinterpret_cast<const Bytef*>(v);
+        for (uint64_t off = 0; off < n * 8; off += (1u << 30))
+          c = ::crc32(c, b + off, static_cast<uInt>(std::min<uint64_t>(1u << 30, n * 8 - off)));
+        cur.crc32 = static_cast<uint32_t>(c);
+      }
+    } else {
+      text.clear();
+      encode_text(text, v, n);
+      write_bytes(text.data(), text.size());
+      uLong c = cur.crc32;
+      for (size_t off = 0; off < text.size(); off += (1u << 30))
+        c = ::crc32(c, reinterpret_cast<const Bytef*>(text.data() + off),
+                    static_cast<uInt>(std::min<size_t>(1u << 30, text.size() - off)));
+      cur.crc32 = static_cast<uint32_t>(c);
+    }
+    if (cur.count == 0) cur.min = v[0];
+    cur.max = v[n - 1];
+    cur.count += n;
+    largest = v[n - 1];
+  }
+
+  void close_file() {
+    if (!fp) return;
+    const bool ok = std::fclose(fp) == 0;
+    fp = nullptr;
+    if (!ok) throw StoreFail{WS_IO, "closing " + cur.name + " failed" + durable_note()};
+    closed.push_back(cur);
+    manifest();
+  }
+
+  void manifest() {
+    Manifest m;
+    m.format = format;
+    m.primes_per_file = per_file;
+    m.files = closed;
+    for (const FileEntry& f : closed) m.total_count += f.count;
+    m.frontier = frontier_set ? frontier : (largest == 0 ? 0 : largest + 1);
+    write_manifest(dir, m);
+    durable = m.total_count;
+  }
+
+  // values split at file boundaries; crcs (nullable): one per piece the split
+  // produces, in order (the caller computed them with the same split)
+  void append(const uint64_t* v, uint64_t n, const uint32_t* crcs) {
+    while (n) {
+      if (!fp) open_next();
+      const uint64_t take = std::min(n, per_file - cur.count);
+      put(v, take, crcs);
+      if (crcs) ++crcs;
+      v += take;
+      n -= take;
+      if (cur.count == per_file) close_file();
+    }
+  }
+
+  void flush() {
+    if (fp)
+      close_file();
+    else
+      manifest();
+  }
+};
+
+namespace {
+
+template <class F>
+ws_status store_guard(ws_store* st, F&& f) {
+  if (!st) return WS_BAD_CONFIG;
+  st->err.clear();
+  try {
+    f();
+  } catch (const StoreFail& e) {
+    st->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    st->err = e.what();
+    return WS_IO;
+  }
+  return WS_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
+ws_status ws_store_open(const char* dir, uint32_t format, uint64_t primes_per_file,
+                        ws_store** out) {
+  if (!dir || !out) return WS_BAD_CONFIG;
+  *out = nullptr;
+  if (primes_per_file == 0) return WS_DOMAIN;  // sink.cpp:187-188
+  if (format > 1) return WS_BAD_CONFIG;
+  std::error_code ec;
+  fs::create_directories(dir, ec);
+  if (ec) return WS_IO;
+  ws_store* st = new (std::nothrow) ws_store;
+  if (!st) return WS_OUT_OF_MEMORY;
+  st->dir = dir;
+  st->format = static_cast<int>(format);
+  st->per_file = primes_per_file;
+  *out = st;
+  return WS_OK;
+}
+
+ws_status ws_store_append(ws_store* st, const uint64_t* values, uint64_t n) {
+  return store_guard(st, [&] {
+    if (n && !values) throw StoreFail{WS_BAD_CONFIG, "null values"};
+    st->append(values, n, nullptr);
+  });
+}
+
+ws_status ws_store_set_frontier(ws_store* st, uint64_t frontier) {
+  return store_guard(st, [&] {
+    if (frontier <= st->largest && st->largest != 0)  // sink.cpp:296-302
+      throw StoreFail{WS_DOMAIN, "frontier " + std::to_string(frontier) +
+                                     " does not cover the emitted prime " +
+                                     std::to_string(st->largest)};
+    st->frontier = frontier;
+    st->frontier_set = true;
+  });
+}
+
+ws_status ws_store_flush(ws_store* st) { return store_guard(st, [&] { st->flush(); }); }
+
+uint64_t ws_store_durable_count(const ws_store* st) { return st ? st->durable : 0; }
+
+const char* ws_store_last_error(const ws_store* st) { return st ? st->err.c_str() : "null store"; }
+
+ws_status ws_store_close(ws_store* st) {
+  if (!st) return WS_OK;
+  const ws_status s = store_guard(st, [&] { st->flush(); });
+  if (st->fp) std::fclose(st->fp);
+  delete st;
+  return s;
+}
+
+// [L, R) enumerated on the device in value windows of bounded size; each
+// window's values are CRC'd on the device piece by piece (binary format),
+// copied to a pinned staging buffer and appended to the streaming writer.
 ws_status ws_store_range(ws_ctx* ctx, uint64_t L, uint64_t R, const char* dir, uint32_t format,
                          uint64_t primes_per_file, uint64_t* n_out) {
   if (!ctx || !dir || !n_out) return WS_BAD_CONFIG;
   *n_out = 0;
-  if (primes_per_file == 0) return WS_DOMAIN;  // sink.cpp:189-190
+  if (primes_per_file == 0) return WS_DOMAIN;  // sink.cpp:187-188
   if (format > 1) return WS_BAD_CONFIG;
-  const uint64_t cap = std::max<uint64_t>(1, ws_prime_count_bound(L, R));
-  uint64_t* dev = nullptr;
-  uint64_t* host = nullptr;
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  const int dev0 = ws_ctx_device(ctx, 0);
+  ws_store* st = nullptr;
+  uint64_t* dbuf = nullptr;
+  uint64_t* hbuf = nullptr;
   uint64_t* d_rng = nullptr;
   uint32_t* d_crc = nullptr;
   auto cleanup = [&] {
-    if (dev) cudaFree(dev);
-    if (host) cudaFreeHost(host);
+    if (dbuf) cudaFree(dbuf);
+    if (hbuf) cudaFreeHost(hbuf);
     if (d_rng) cudaFree(d_rng);
     if (d_crc) cudaFree(d_crc);
+    if (st) {
+      if (st->fp) std::fclose(st->fp);
+      delete st;
+    }
+    if (prev >= 0) cudaSetDevice(prev);
   };
+  ws_status code = WS_OK;
   try {
-    std::error_code ec;
-    fs::create_directories(dir, ec);
-    if (ec) throw StoreFail{WS_IO, std::string("cannot create output directory ") + dir};
-    if (cudaMalloc(&dev, cap * 8) != cudaSuccess)
-      throw StoreFail{WS_OUT_OF_MEMORY, "store buffer"};
-    uint64_t n = 0;
-    ws_checks chk{};
-    const ws_status st = ws_enumerate_range(ctx, L, R, WS_OUT_DEVICE, dev, cap, &n, &chk);
-    if (st != WS_OK) throw StoreFail{st, ws_last_error(ctx)};
-    cudaStream_t s = static_cast<cudaStream_t>(ws_ctx_stream(ctx));
-    const uint64_t nfiles = (n + primes_per_file - 1) / primes_per_file;
-    std::vector<uint32_t> file_crc(nfiles, 0);
-    if (format == 1 && n) {
-      // ranges of <= 64 KiB inside each file, CRC'd on the device
-      constexpr uint64_t kPiece = 8192;  // values per range
-      std::vector<uint64_t> begin, len;
-      std::vector<uint64_t> first(nfiles + 1, 0);
-      for (uint64_t f = 0; f < nfiles; ++f) {
-        first[f] = begin.size();
-        const uint64_t a = f * primes_per_file, b = std::min(n, a + primes_per_file);
-        for (uint64_t x = a; x < b; x += kPiece) {
-          begin.push_back(8 * x);
-          len.push_back(8 * (std::min(b, x + kPiece) - x));
+    if (cudaSetDevice(dev0) != cudaSuccess) throw StoreFail{WS_NO_DEVICE, "cudaSetDevice"};
+    ws_status s = ws_store_open(dir, format, primes_per_file, &st);
+    if (s != WS_OK) throw StoreFail{s, std::string("cannot create output directory ") + dir};
+    // value windows of whole segments, at most ~2^30 integers: the densest
+    // window (the first) bounds the buffers, 8 B per prime on each side
+    const uint64_t span = 6ull * (1u << 18) * 682;
+    const uint64_t lo0 = L / 6 * 6;
+    uint64_t cap = 1;
+    for (uint64_t a = L; a < R;) {
+      const uint64_t b = (R - lo0 > (a - lo0) + span) ? lo0 + ((a - lo0) / span + 1) * span : R;
+      cap = std::max(cap, ws_prime_count_bound(a, b));
+      break;  // the first window is the densest
+    }
+    constexpr uint64_t kPiece = 8192;  // values per device CRC range
+    const uint64_t max_ranges = cap / kPiece + 2 * (cap / primes_per_file + 2) + 4;
+    if (cudaMalloc(&dbuf, cap * 8) != cudaSuccess ||
+        cudaMalloc(&d_rng, 2 * max_ranges * 8) != cudaSuccess ||
+        cudaMalloc(&d_crc, max_ranges * 4) != cudaSuccess)
+      throw StoreFail{WS_OUT_OF_MEMORY, "store window buffers"};
+    if (cudaMallocHost(&hbuf, cap * 8) != cudaSuccess)
+      throw StoreFail{WS_OUT_OF_MEMORY, "store host staging"};
+    cudaStream_t strm = static_cast<cudaStream_t>(ws_ctx_stream(ctx));
+    std::vector<uint64_t> begin, len, cuts;
+    std::vector<uint32_t> crc, piece_crc;
+    uint64_t total = 0;
+    for (uint64_t a = L; a < R;) {
+      const uint64_t b = (R - lo0 > (a - lo0) + span) ? lo0 + ((a - lo0) / span + 1) * span : R;
+      uint64_t n = 0;
+      ws_checks chk{};
+      s = ws_enumerate_range(ctx, a, b, WS_OUT_DEVICE, dbuf, cap, &n, &chk);
+      if (s != WS_OK) throw StoreFail{s, ws_last_error(ctx)};
+      if (cudaSetDevice(dev0) != cudaSuccess) throw StoreFail{WS_NO_DEVICE, "cudaSetDevice"};
+      if (n) {
+        // the pieces append() will cut this window into: file boundaries
+        cuts.assign(1, 0);
+        uint64_t room = st->fp ? primes_per_file - st->cur.count : primes_per_file;
+        for (uint64_t x = 0; x < n;) {
+          const uint64_t t = std::min(n - x, room);
+          x += t;
+          cuts.push_back(x);
+          room = primes_per_file;
+        }
+        const uint64_t np = cuts.size() - 1;
+        piece_crc.assign(np, 0);
+        if (format == 1) {  // device CRC of every <= 64 KiB range inside each piece
+          begin.clear();
+          len.clear();
+          std::vector<uint64_t> first(np + 1, 0);
+          for (uint64_t p = 0; p < np; ++p) {
+            first[p] = begin.size();
+            for (uint64_t x = cuts[p]; x < cuts[p + 1]; x += kPiece) {
+              begin.push_back(8 * x);
+              len.push_back(8 * (std::min(cuts[p + 1], x + kPiece) - x));
+            }
+          }
+          first[np] = begin.size();
+          const uint64_t nr = begin.size();
+          if (nr > max_ranges) throw StoreFail{WS_CUDA, "store range table overflow"};
+          crc.resize(nr);
+          if (cudaMemcpyAsync(d_rng, begin.data(), nr * 8, cudaMemcpyHostToDevice, strm) !=
+                  cudaSuccess ||
+              cudaMemcpyAsync(d_rng + nr, len.data(), nr * 8, cudaMemcpyHostToDevice, strm) !=
+                  cudaSuccess ||
+              wsk::launch_crc32_ranges(dbuf, d_rng, d_rng + nr, static_cast<uint32_t>(nr), d_crc,
+                                       strm) != cudaSuccess ||
+              cudaMemcpyAsync(crc.data(), d_crc, nr * 4, cudaMemcpyDeviceToHost, strm) !=
+                  cudaSuccess)
+            throw StoreFail{WS_CUDA, "device crc"};
+          if (cudaMemcpyAsync(hbuf, dbuf, n * 8, cudaMemcpyDeviceToHost, strm) != cudaSuccess ||
+              cudaStreamSynchronize(strm) != cudaSuccess)
+            throw StoreFail{WS_CUDA, "values readback"};
+          for (uint64_t p = 0; p < np; ++p) {
+            uLong c = ::crc32(0, Z_NULL, 0);
+            for (uint64_t r = first[p]; r < first[p + 1]; ++r)
+              c = ::crc32_combine(c, crc[r], static_cast<z_off_t>(len[r]));
+            piece_crc[p] = static_cast<uint32_t>(c);
+          }
+          st->append(hbuf, n, piece_crc.data());
+        } else {
+          if (cudaMemcpyAsync(hbuf, dbuf, n * 8, cudaMemcpyDeviceToHost, strm) != cudaSuccess ||
+              cudaStreamSynchronize(strm) != cudaSuccess)
+            throw StoreFail{WS_CUDA, "values readback"};
+          st->append(hbuf, n, nullptr);
         }
       }
-      first[nfiles] = begin.size();
-      const uint64_t nr = begin.size();
-      if (cudaMalloc(&d_rng, 2 * nr * 8) != cudaSuccess || cudaMalloc(&d_crc, nr * 4) != cudaSuccess)
-        throw StoreFail{WS_OUT_OF_MEMORY, "crc ranges"};
-      if (cudaMemcpyAsync(d_rng, begin.data(), nr * 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-          cudaMemcpyAsync(d_rng + nr, len.data(), nr * 8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-          wsk::launch_crc32_ranges(dev, d_rng, d_rng + nr, static_cast<uint32_t>(nr), d_crc, s) !=
-              cudaSuccess)
-        throw StoreFail{WS_CUDA, "crc kernel"};
-      std::vector<uint32_t> crc(nr);
-      if (cudaMemcpyAsync(crc.data(), d_crc, nr * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-          cudaStreamSynchronize(s) != cudaSuccess)
-        throw StoreFail{WS_CUDA, "crc readback"};
-      for (uint64_t f = 0; f < nfiles; ++f) {
-        uLong c = ::crc32(0, Z_NULL, 0);
-        for (uint64_t r = first[f]; r < first[f + 1]; ++r)
-          c = ::crc32_combine(c, crc[r], static_cast<z_off_t>(len[r]));
-        file_crc[f] = static_cast<uint32_t>(c);
-      }
+      total += n;
+      a = b;
     }
-    if (cudaMallocHost(&host, std::max<uint64_t>(n, 1) * 8) != cudaSuccess)
-      throw StoreFail{WS_OUT_OF_MEMORY, "host staging"};
-    if (n && (cudaMemcpyAsync(host, dev, n * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-              cudaStreamSynchronize(s) != cudaSuccess))
-      throw StoreFail{WS_CUDA, "values readback"};
-    Manifest m;
-    m.format = static_cast<int>(format);
-    m.primes_per_file = primes_per_file;
-    m.frontier = R;  // the CLI sets the sieved-through bound (wheelsieve.cpp:167)
-    const fs::path d(dir);
-    std::string text;
-    for (uint64_t f = 0; f < nfiles; ++f) {
-      const uint64_t a = f * primes_per_file, b = std::min(n, a + primes_per_file);
-      FileEntry fe;
-      fe.name = chunk_name(f, m.format);
-      fe.count = b - a;
-      fe.min = host[a];
-      fe.max = host[b - 1];
-      if (format == 1) {
-        write_file(d / fe.name, host + a, (b - a) * 8);
-        fe.crc32 = file_crc[f];
-      } else {
-        text.clear();
-        encode_text(text, host + a, b - a);
-        write_file(d / fe.name, text.data(), text.size());
-        uLong c = ::crc32(0, Z_NULL, 0);
-        for (size_t off = 0; off < text.size(); off += (1u << 30))
-          c = ::crc32(c, reinterpret_cast<const Bytef*>(text.data() + off),
-                      static_cast<uInt>(std::min<size_t>(1u << 30, text.size() - off)));
-        fe.crc32 = static_cast<uint32_t>(c);
-      }
-      m.total_count += fe.count;
-      m.files.push_back(std::move(fe));
-    }
-    write_manifest(d, m);
-    *n_out = n;
+    // the CLI records the sieved-through bound (wheelsieve.cpp:167)
+    st->frontier = R;
+    st->frontier_set = true;
+    st->flush();
+    *n_out = total;
   } catch (const StoreFail& e) {
-    cleanup();
-    return e.code;
+    code = e.code;
   } catch (...) {
-    cleanup();
-    return WS_IO;
+    code = WS_IO;
   }
   cleanup();
-  return WS_OK;
+  return code;
 }
 
 ws_status ws_read_back(const char* dir, uint64_t lo, uint64_t hi, uint64_t* out, uint64_t cap,

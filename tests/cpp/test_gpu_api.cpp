@@ -1,6 +1,6 @@
-// C++ parity tests of wheelsieve::gpu (include/wheelsieve/gpu.hpp) that read
-// like the reference's own suite: each case cites the reference test it
-// mirrors.  Expected values come from a textbook sieve local to this file
+// C++ parity tests of the drop-in C++ API (include/wheelsieve/*.hpp,
+// libwheelsieve.so over the GPU C ABI) that read like the reference's own
+// suite: each case cites the reference test it mirrors.  Expected values come from a textbook sieve local to this file
 // (an independent checker, like the reference's naive_sieve oracle,
 // wheel.cpp:40-54) and from known answers in the reference tests.
 // Prints "[PASS]"/"[FAIL]" lines; exit code = number of failures.
@@ -10,9 +10,17 @@
 #include <string>
 #include <vector>
 
+#include "wheelsieve/base_store.hpp"
+#include "wheelsieve/engine.hpp"
 #include "wheelsieve/gpu.hpp"
+#include "wheelsieve/segment.hpp"
+#include "wheelsieve/sink.hpp"
+#include "wheelsieve/stream.hpp"
+#include "wheelsieve/wheel.hpp"
 
-using namespace wheelsieve::gpu;
+using namespace wheelsieve;
+using gpu::Checks;
+using gpu::Context;
 
 namespace {
 
@@ -52,11 +60,18 @@ std::vector<uint64_t> textbook(uint64_t n) {  // all primes <= n
   return out;
 }
 
-std::vector<uint64_t> run_collect(Device& dev, uint64_t limit, unsigned threads, uint64_t span) {
+std::vector<uint64_t> run_collect(Context& dev, uint64_t limit, unsigned threads, uint64_t span) {
   MemorySink sink;
   SieveConfig config{limit, threads, round_segment_span(span, threads), FlagWidth::Bit, &sink};
-  run(config, dev);
+  gpu::run(config, dev);
   return sink.primes();
+}
+
+// sieve_segment on a fresh SegmentBitmap with a bootstrapped base store
+SegmentBitmap sieved(uint64_t start, uint64_t len) {
+  SegmentBitmap seg(start, len);
+  sieve_segment(seg, BasePrimeStore::bootstrap(std::max<uint64_t>(25, start + 6 * len)));
+  return seg;
 }
 
 class StopRequestingSink : public MemorySink {  // test_engine.cpp:22-34
@@ -84,7 +99,7 @@ class FailingSink : public MemorySink {  // test_engine.cpp:38-45
 }  // namespace
 
 int main() {
-  Device dev;
+  Context dev;
 
   // test_engine.cpp:48-71
   CHECK(round_segment_span(6000, 1) == 6000);
@@ -123,12 +138,12 @@ int main() {
   {  // test_engine.cpp:123-133
     MemorySink sink;
     for (uint64_t limit : {uint64_t{0}, uint64_t{1}})
-      EXPECT_ERROR(Errc::EmptyRange, run({limit, 1, 6000, FlagWidth::Bit, &sink}, dev));
+      EXPECT_ERROR(Errc::EmptyRange, gpu::run({limit, 1, 6000, FlagWidth::Bit, &sink}, dev));
   }
 
   {  // test_engine.cpp:135-148
     MemorySink sink;
-    const SieveReport r = run({1'000'000, 2, 600000, FlagWidth::Bit, &sink}, dev);
+    const SieveReport r = gpu::run({1'000'000, 2, 600000, FlagWidth::Bit, &sink}, dev);
     CHECK(r.prime_count == 78498);
     CHECK(r.largest_prime == 999983);
     CHECK(r.iterations == 2);
@@ -140,7 +155,7 @@ int main() {
   {  // test_engine.cpp:150-161
     auto rep = [&](FlagWidth w, unsigned t) {
       CountSink sink;
-      return run({10'000, t, 6000, w, &sink}, dev);
+      return gpu::run({10'000, t, 6000, w, &sink}, dev);
     };
     CHECK(rep(FlagWidth::Bit, 1).peak_flag_entries == 2000);
     CHECK(rep(FlagWidth::Bit, 1).peak_flag_bytes == 250);
@@ -159,7 +174,7 @@ int main() {
   {  // test_engine.cpp:175-183
     CountSink counter;
     const SieveReport r =
-        run({123'456, 3, round_segment_span(6000, 3), FlagWidth::Bit, &counter}, dev);
+        gpu::run({123'456, 3, round_segment_span(6000, 3), FlagWidth::Bit, &counter}, dev);
     CHECK(r.prime_count == 11601);
     CHECK(r.largest_prime == 123'449);
     CHECK(counter.count() == 11601 && counter.largest() == 123'449);
@@ -167,19 +182,19 @@ int main() {
 
   {  // test_engine.cpp:185-225
     MemorySink sink;
-    EXPECT_ERROR(Errc::BadConfig, run({1000, 1, 6000, FlagWidth::Bit, nullptr}, dev));
-    EXPECT_ERROR(Errc::BadConfig, run({1000, 0, 6000, FlagWidth::Bit, &sink}, dev));
-    EXPECT_ERROR(Errc::BadConfig, run({1000, 3, 6000, FlagWidth::Bit, &sink}, dev));
-    EXPECT_ERROR(Errc::BadConfig, run({1000, 2000, 6'000'000, FlagWidth::Bit, &sink}, dev));
-    EXPECT_ERROR(Errc::BadConfig, run({std::nullopt, 1, 6000, FlagWidth::Bit, &sink}, dev));
+    EXPECT_ERROR(Errc::BadConfig, gpu::run({1000, 1, 6000, FlagWidth::Bit, nullptr}, dev));
+    EXPECT_ERROR(Errc::BadConfig, gpu::run({1000, 0, 6000, FlagWidth::Bit, &sink}, dev));
+    EXPECT_ERROR(Errc::BadConfig, gpu::run({1000, 3, 6000, FlagWidth::Bit, &sink}, dev));
+    EXPECT_ERROR(Errc::BadConfig, gpu::run({1000, 2000, 6'000'000, FlagWidth::Bit, &sink}, dev));
+    EXPECT_ERROR(Errc::BadConfig, gpu::run({std::nullopt, 1, 6000, FlagWidth::Bit, &sink}, dev));
     std::atomic<bool> stop{false};
-    EXPECT_ERROR(Errc::BadConfig, run_unbounded({1000, 1, 6000, FlagWidth::Bit, &sink}, stop, dev));
+    EXPECT_ERROR(Errc::BadConfig, gpu::run_unbounded({1000, 1, 6000, FlagWidth::Bit, &sink}, stop, dev));
   }
 
   {  // test_engine.cpp:227-238
     FailingSink sink;
     try {
-      run({10'000, 1, 96, FlagWidth::Bit, &sink}, dev);
+      gpu::run({10'000, 1, 96, FlagWidth::Bit, &sink}, dev);
       CHECK(false);
     } catch (const SinkFailure& e) {
       CHECK(e.code() == Errc::Io);
@@ -193,14 +208,14 @@ int main() {
     CountSink counter;
     std::atomic<bool> stop{true};
     const SieveReport r =
-        run_unbounded({std::nullopt, 1, 6000, FlagWidth::Bit, &counter}, stop, dev);
+        gpu::run_unbounded({std::nullopt, 1, 6000, FlagWidth::Bit, &counter}, stop, dev);
     CHECK(r.stopped && !r.overflowed && r.prime_count == 0 && r.iterations == 0);
   }
 
   {  // test_engine.cpp:252-262
     std::atomic<bool> stop{false};
     StopRequestingSink sink(stop);
-    const SieveReport r = run_unbounded({std::nullopt, 1, 6000, FlagWidth::Bit, &sink}, stop, dev);
+    const SieveReport r = gpu::run_unbounded({std::nullopt, 1, 6000, FlagWidth::Bit, &sink}, stop, dev);
     CHECK(r.stopped && r.iterations == 1);
     CHECK(r.prime_count == 783 && r.largest_prime == 5987 && r.sieved_to == 6000);
     CHECK(sink.primes() == textbook(5999));
@@ -209,8 +224,8 @@ int main() {
   {  // test_engine.cpp:264-272
     std::atomic<bool> s1{false}, s4{false};
     StopRequestingSink k1(s1), k4(s4);
-    run_unbounded({std::nullopt, 1, 6000, FlagWidth::Bit, &k1}, s1, dev);
-    run_unbounded({std::nullopt, 4, 6000, FlagWidth::Bit, &k4}, s4, dev);
+    gpu::run_unbounded({std::nullopt, 1, 6000, FlagWidth::Bit, &k1}, s1, dev);
+    gpu::run_unbounded({std::nullopt, 4, 6000, FlagWidth::Bit, &k4}, s4, dev);
     CHECK(k1.primes() == k4.primes());
   }
 
@@ -245,23 +260,33 @@ int main() {
     CHECK(counts[0] == 628'905 && sums[0] == 238'210'012'871'732'589ull);
   }
 
-  {  // test_segment.cpp:135-184 against the SegmentBitmap mirror
-    const SegmentFlags seg = dev.sieve_segment(12000, 1000);
+  {  // test_segment.cpp:135-184 through SegmentBitmap + sieve_segment
+    const SegmentBitmap seg = sieved(12000, 1000);
     CHECK(!seg.flag_for(14443) && !seg.flag_for(14417) && seg.flag_for(12007));
     const auto all = textbook(18000);
     std::vector<uint64_t> sl;
     for (uint64_t p : all)
       if (p >= 12000) sl.push_back(p);
     CHECK(seg.surviving() == sl);
-    const SegmentFlags first = dev.sieve_segment(0, 1000);
+    const SegmentBitmap first = sieved(0, 1000);
     CHECK(first.flag_for(1));  // not a multiple of anything; callers clear it
-    const SegmentFlags one = dev.sieve_segment(10200, 1);
+    const SegmentBitmap one = sieved(10200, 1);
     CHECK(!one.flag_for(10201) && !one.flag_for(10205));
-    const SegmentFlags sq = dev.sieve_segment(168, 1);
+    const SegmentBitmap sq = sieved(168, 1);
     CHECK(!sq.flag_for(169) && sq.flag_for(173));
-    EXPECT_ERROR(Errc::Alignment, dev.sieve_segment(10, 5));
-    EXPECT_ERROR(Errc::Domain, dev.sieve_segment(12, 0));
-    EXPECT_ERROR(Errc::Overflow, dev.sieve_segment(kMaxSegmentEnd, 1));
+    EXPECT_ERROR(Errc::Alignment, SegmentBitmap(10, 5));
+    EXPECT_ERROR(Errc::Domain, SegmentBitmap(12, 0));
+    EXPECT_ERROR(Errc::Overflow, SegmentBitmap(kMaxSegmentEnd, 1));
+    EXPECT_ERROR(Errc::NotOnWheel, (void)seg.flag_for(12002));
+    EXPECT_ERROR(Errc::Domain, (void)seg.flag_for(18001));
+    SegmentBitmap tiny(12000, 1000);  // an incomplete base store (segment.cpp:166-169)
+    EXPECT_ERROR(Errc::IncompleteBase, sieve_segment(tiny, BasePrimeStore::bootstrap(25)));
+    SegmentBitmap trim = sieved(594000, 1000);  // widths agree (test_segment.cpp:186-193)
+    SegmentBitmap wide(594000, 1000, FlagWidth::Byte);
+    sieve_segment(wide, BasePrimeStore::bootstrap(600000));
+    CHECK(trim.surviving() == wide.surviving() && trim.count_surviving() == wide.count_surviving());
+    trim.clear_values_above(597000);
+    CHECK(*trim.last_surviving() < 597000 && trim.flag_entries() == 2000);
   }
 
   {  // test_base_store.cpp:29-38 and test_wheel.cpp:30-74
@@ -274,33 +299,84 @@ int main() {
   }
 
   {  // test_stream.cpp:12-51, acceptance.cpp:363-400
-    PrimeStream st(1000, dev);
+    PrimeStream st(1000);
     std::vector<uint64_t> first;
     for (int i = 0; i < 10; ++i) first.push_back(*st.next());
     CHECK((first == std::vector<uint64_t>{2, 3, 5, 7, 11, 13, 17, 19, 23, 29}));
-    PrimeStream s2(7, dev);
+    PrimeStream s2(7);
     const auto ref = textbook(1'000'000);
     bool same = true;
     for (uint64_t p : ref) same = same && (*s2.next() == p);
     CHECK(same);
-    PrimeStream s3(1 << 12, dev);
+    PrimeStream s3(1 << 12);
     uint64_t v = 0;
     for (int i = 0; i < 100'000; ++i) v = *s3.next();
     CHECK(v == 1'299'709);
-    EXPECT_ERROR(Errc::Domain, PrimeStream(0, dev));
+    EXPECT_ERROR(Errc::Domain, PrimeStream(0));
+    CHECK(s3.base().covers(1'299'710));
     CHECK(PrimeStream::segment_would_overflow(kMaxSegmentEnd, 1));
     CHECK(!PrimeStream::segment_would_overflow(0, 1));
   }
 
-  {  // chunked store round trip through the C++ mirror (sink.hpp:68-141)
-    const std::string d = "/tmp/wheelsieve_gpu_cpp_store";
+  {  // chunked store round trip (sink.hpp:68-141): the device store, and
+     // run() into a ChunkedFileSink -- byte-identical files
+    const std::string d = "/tmp/wheelsieve_gpu_cpp_store", e = "/tmp/wheelsieve_gpu_cpp_sink";
     std::filesystem::remove_all(d);
+    std::filesystem::remove_all(e);
     const uint64_t n = dev.store_range(0, 1'000'001, d, true, 10'000);
     CHECK(n == 78'498);
     verify_store(d);
     CHECK(read_back(d, 0, 1'000'001) == textbook(1'000'000));
     EXPECT_ERROR(Errc::BeyondFrontier, read_back(d, 0, 1'000'002));
+    {
+      ChunkedFileSink sink({e, 10'000, FileFormat::Binary});
+      const SieveReport r = gpu::run({1'000'000, 2, 600'000, FlagWidth::Bit, &sink}, dev);
+      CHECK(sink.durable_count() == 70'000);  // 7 closed files before the final flush
+      sink.set_frontier(r.sieved_to);
+      sink.flush();
+      CHECK(sink.durable_count() == 78'498);
+      EXPECT_ERROR(Errc::Domain, sink.set_frontier(999'983));
+    }
+    verify_store(e);
+    auto slurp = [](const std::string& p) {
+      std::FILE* f = std::fopen(p.c_str(), "rb");
+      std::string s;
+      char buf[1 << 16];
+      size_t k;
+      while (f && (k = std::fread(buf, 1, sizeof buf, f)) > 0) s.append(buf, k);
+      if (f) std::fclose(f);
+      return s;
+    };
+    for (const char* f : {"/manifest.json", "/primes_00000.bin", "/primes_00007.bin"})
+      CHECK(slurp(d + f) == slurp(e + f) && !slurp(d + f).empty());
+    EXPECT_ERROR(Errc::Domain, ChunkedFileSink({e, 0, FileFormat::Text}));
     std::filesystem::remove_all(d);
+    std::filesystem::remove_all(e);
+  }
+
+  {  // count sinks get one emit_count per non-empty worker tile
+     // (engine.cpp:277-288): a limit inside the first tile of iteration 1
+    CountSink c;
+    const SieveReport r = gpu::run({6'100, 2, 6'000, FlagWidth::Bit, &c}, dev);
+    CHECK(r.iterations == 2 && r.prime_count == 795 && r.largest_prime == 6'091);
+    MemorySink m;
+    EXPECT_ERROR(Errc::Domain, m.emit_count(1, 7));  // value sinks take no counts
+  }
+
+  {  // a multi-device context (NCCL, one communicator per device): the same answers
+    gpu::ContextOptions o;
+    o.devices = {0};
+    Context multi(o);
+    CHECK(multi.num_devices() == 1 && multi.num_shards() == 1);
+    std::vector<uint32_t> per;
+    const Checks c = multi.count_range(0, 1'000'000'001, false, &per);
+    CHECK(c.count == 50'847'534 && per.size() == 636 && per[0] == 119'266);
+    MemorySink sink;
+    gpu::run({1'000'000, 3, round_segment_span(600'000, 3), FlagWidth::Bit, &sink}, multi);
+    CHECK(sink.primes() == textbook(1'000'000));
+    const auto tiles = multi.count_ranges(std::vector<uint64_t>{0, 100, 10'000},
+                                          std::vector<uint64_t>{100, 10'000, 10}, true);
+    CHECK(tiles[0].count == 25 && tiles[1].count == 1229 - 25 && tiles[2].count == 0);
   }
 
   std::printf(g_fail ? "[FAIL] %d failures\n" : "[PASS] all checks\n", g_fail);

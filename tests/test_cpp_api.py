@@ -1,5 +1,6 @@
-"""The C++ host API (include/wheelsieve/gpu.hpp) compiles against the C ABI
-on CPU, and its reference-mirroring test program passes on the GPU."""
+"""The drop-in C++ API (include/wheelsieve/*.hpp, libwheelsieve.so over the
+C ABI) compiles on CPU, and its reference-mirroring test program passes on the
+GPU."""
 import os
 import subprocess
 
@@ -13,7 +14,7 @@ LIBDIR = os.path.join(ROOT, "paper_2310_17746_b200")
 def _build(tmp_path):
     exe = str(tmp_path / "test_gpu_api")
     subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
-                    SRC, "-o", exe, f"-L{LIBDIR}", "-lwheelsieve_cuda",
+                    SRC, "-o", exe, f"-L{LIBDIR}", "-lwheelsieve", "-lwheelsieve_cuda",
                     f"-Wl,-rpath,{LIBDIR}"], check=True)
     return exe
 

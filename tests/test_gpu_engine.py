@@ -170,3 +170,80 @@ def test_prime_stream(port):  # test_stream.cpp:12-69, acceptance.cpp:363-400
         PrimeStream(0)
     assert e.value.code == Errc.Domain
     assert PrimeStream.segment_would_overflow(ws.wheelsieve.K_MAX_SEGMENT_END, 1)
+
+
+class _RecordingCounts(CountSink):
+    def __init__(self):
+        super().__init__()
+        self.batches = []
+
+    def emit_count(self, n, largest):
+        super().emit_count(n, largest)
+        if n:
+            self.batches.append((n, largest))
+
+
+class _RecordingValues(MemorySink):
+    def __init__(self):
+        super().__init__()
+        self.batches = []
+
+    def accept(self, batch):
+        super().accept(batch)
+        self.batches.append((int(batch.size), int(batch[-1])))
+
+
+def _expected_tiles(port, limit, threads, span):
+    """engine.cpp:233-288: per iteration, one batch per non-empty worker tile
+    (after 2, 3), computed here from the oracle over each tile's values."""
+    out = [(2, 3)]
+    limit_end = (limit // 6 + 1) * 6
+    seg_lo = 0
+    sub = span // threads
+    while seg_lo < limit_end:
+        seg_hi = min(seg_lo + span, limit_end)
+        for j in range(threads):
+            lo = seg_lo + j * sub
+            if lo >= seg_hi:
+                break
+            hi = min(lo + sub, seg_hi)
+            a, b = max(lo, 4), min(hi, limit + 1)
+            if a < b:
+                r = port.range(a, b)
+                if r["count"]:
+                    out.append((r["count"], r["largest"]))
+        seg_lo += span
+    return out
+
+
+@pytest.mark.parametrize("limit,threads,span", [(100_000, 3, 6012), (1_000_000, 8, 600_000),
+                                                (6_100, 2, 6_000), (10**7 + 7, 5, 600_000)])
+def test_emission_granularity_per_tile(port, limit, threads, span):
+    """Count sinks get emit_count(count, largest) for every non-empty worker
+    tile of every iteration, value sinks emit(values) per tile -- the
+    reference's batches exactly (engine.cpp:277-288)."""
+    want = _expected_tiles(port, limit, threads, span)
+    c = _RecordingCounts()
+    run(SieveConfig(limit, threads, span, 0, c))
+    assert c.batches == want
+    v = _RecordingValues()
+    run(SieveConfig(limit, threads, span, 0, v))
+    assert v.batches == want
+
+
+def test_count_sink_failure_partials(port):
+    """SinkFailure carries the totals of the batches emitted before the
+    failing one (engine.cpp:290-295) -- per tile, also for count sinks."""
+    class Refuse(CountSink):
+        def emit_count(self, n, largest):
+            if largest > 50_000:
+                raise Error(Errc.Io, "disk full")
+            super().emit_count(n, largest)
+
+    s = Refuse()
+    with pytest.raises(SinkFailure) as e:
+        run(SieveConfig(200_000, 4, 24_000, 0, s))
+    want = port.range(0, 48_001)  # tiles of 6000: the last accepted one ends at 48000
+    assert e.value.partial.prime_count == want["count"]
+    assert e.value.partial.largest_prime == want["largest"]
+    assert e.value.partial.iterations == 2
