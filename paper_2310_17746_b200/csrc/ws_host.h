@@ -186,6 +186,9 @@ struct DevCtx {
   uint32_t bucket_min_ratio = 8;       // buckets iff largest base prime >= ratio * S
   uint32_t bucket_ctas_per_sm = 0;     // tuning knob (WHEELSIEVE_BUCKET_CTAS)
   uint32_t ctas_per_sm = 0;            // tuning knob, all launches (WHEELSIEVE_CTAS_PER_SM)
+  // predicated single-hit atomics (WHEELSIEVE_SINGLE_PRED=1): 17% fewer shared
+  // wavefronts at C3 but no faster (204.4 ms either way; C4 +0.2 ms), so off
+  uint32_t single_pred = 0;
 
   // scratch
   DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)

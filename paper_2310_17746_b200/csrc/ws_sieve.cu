@@ -501,8 +501,15 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       if (__shfl_sync(kFull, p, 0) > t_hi) break;
       uint32_t rel1 = len, rel5 = len;
       prime_offsets_t<decltype(fast)::value>(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
-      mark_or(a1, rel1, len, P.S / 32 - 1);
-      mark_or(a5, rel5, len, P.S / 32 - 1);
+      if (P.single_pred) {
+        // predicated: lanes without a hit issue no shared-memory access, so
+        // the warp's conflict degree is that of its hitting lanes only
+        mark_if(a1, rel1, len);
+        mark_if(a5, rel5, len);
+      } else {
+        mark_or(a1, rel1, len, P.S / 32 - 1);
+        mark_or(a5, rel5, len, P.S / 32 - 1);
+      }
     }
   };
   if (mc.fast)
