@@ -334,6 +334,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
         g = std::max<uint32_t>(1, std::min<uint32_t>(g, ((1u << 31) - 1) / (piece * c->S)));
         fh.group_runs = g;
         fh.huge_step = c->huge_step;
+        fh.huge_loop = c->huge_loop;
         fh.max_run_segs = static_cast<uint32_t>(piece) * c->huge_step;
         ck(wsk::launch_bucket_fill_huge(fh, c->fstream), "bucket fill (huge primes)");
         c->timing.launches += 1;
@@ -1265,6 +1266,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_CTAS_PER_SM")) c->ctas_per_sm = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_HOST_WIRE")) c->host_wire = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_SINGLE_PRED")) c->single_pred = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_HUGE_LOOP")) c->huge_loop = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_BASE_EXTEND")) c->base_extend = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
     c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));

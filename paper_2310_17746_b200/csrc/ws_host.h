@@ -180,6 +180,7 @@ struct DevCtx {
   uint32_t piece_override = 0;         // tuning knob (WHEELSIEVE_FILL_PIECE)
   bool fill_huge = true;               // carried-offset fill for p >= run length (WHEELSIEVE_FILL_HUGE)
   uint32_t huge_step = 1;              // runs per histogram step there (WHEELSIEVE_HUGE_STEP)
+  uint32_t huge_loop = 0;              // WHEELSIEVE_HUGE_LOOP=1: the hit-loop kernel at step 1
   uint32_t huge_from = 0;              // its lower bound in units of S (0: the run length)
   uint64_t huge_thr = 0;               // the run length in slots the count below is for
   uint32_t n_below_huge = 0;           // table primes (>= 53) below huge_thr

@@ -114,6 +114,7 @@ struct FillParams {
   uint32_t max_run_segs;    // histogram size (dynamic shared memory)
   uint32_t group_runs;      // bucket_fill_huge_kernel: consecutive runs per block row
   uint32_t huge_step;       // ... and runs per histogram step (max_run_segs covers them)
+  uint32_t huge_loop;       // 1: the hit-loop kernel even for one run per step (A/B knob)
 };
 constexpr int kFillThreads = 256;
 constexpr int kFillPrimesPerThread = 16;

@@ -1122,6 +1122,75 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_huge_kernel(const Fi
   }
 }
 
+// bucket_fill_huge_kernel for one run per step (the default): a prime of at
+// least the run length hits a run at most once per class, so each (prime,
+// class) is one predicated check per run -- no hit loop, so no warp runs to
+// the busiest lane's trip count -- and the next hits stay in registers
+// (16 primes x 2 classes per thread) instead of shared memory.
+__global__ void __launch_bounds__(kFillThreads) bucket_fill_huge1_kernel(const FillParams F) {
+  extern __shared__ uint32_t fill_smem[];
+  uint32_t* hist = fill_smem;  // max_run_segs counters, then the run's list cursors
+  const uint32_t r_begin = blockIdx.y * F.group_runs;
+  const uint32_t r_end = min(F.nruns, r_begin + F.group_runs);
+  const uint64_t g_lo = F.runs[r_begin].k_lo, g_hi = F.runs[r_end - 1].k_hi;
+  const uint32_t S = 1u << F.log2S;
+  const uint32_t t_lo = isqrt64(6 * g_lo), t_hi = isqrt64(6 * g_hi);
+  const ModCtx mc = mod_ctx(g_lo);
+  const uint32_t gspan = static_cast<uint32_t>(g_hi - g_lo);  // < 2^31 (host bound)
+  const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
+  const uint32_t p_end = F.nprimes_dev ? min(F.p_end, *F.nprimes_dev) : F.p_end;
+  uint32_t pp[kFillPrimesPerThread], n1[kFillPrimesPerThread], n5[kFillPrimesPerThread];
+#pragma unroll
+  for (int j = 0; j < kFillPrimesPerThread; ++j) {
+    const uint32_t i = first + j * kFillThreads + threadIdx.x;
+    pp[j] = 0;
+    n1[j] = n5[j] = 0xFFFFFFFFu;
+    if (i < p_end) {
+      pp[j] = __ldg(F.prime_p + i);
+      uint32_t q1, q5;
+      if (prime_offsets(pp[j], __ldg(F.prime_inv + i), i, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
+        if (q1 < gspan) n1[j] = q1;
+        if (q5 < gspan) n5[j] = q5;
+      }
+    }
+  }
+#pragma unroll 1
+  for (uint32_t r = r_begin; r < r_end; ++r) {
+    const Run run = F.runs[r];
+    const uint32_t lo = static_cast<uint32_t>(run.k_lo - g_lo);
+    const uint32_t hi = static_cast<uint32_t>(run.k_hi - g_lo);
+    for (uint32_t k = threadIdx.x; k < run.nseg; k += kFillThreads) hist[k] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kFillPrimesPerThread; ++j) {
+      if (n1[j] < hi) atomicAdd(hist + ((n1[j] - lo) >> F.log2S), 1u);
+      if (n5[j] < hi) atomicAdd(hist + ((n5[j] - lo) >> F.log2S), 1u);
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < run.nseg; k += kFillThreads) {
+      const uint32_t c = hist[k];
+      hist[k] = (run.seg0 + k) * F.bcap + (c ? atomicAdd(F.bcount + run.seg0 + k, c) : 0u);
+    }
+    __syncthreads();
+    auto put = [&](uint32_t& h, uint32_t p, uint32_t cls_bit) {
+      if (h < hi) {
+        const uint32_t rel = h - lo;
+        const uint32_t seg = rel >> F.log2S;
+        const uint32_t idx = atomicAdd(hist + seg, 1u);
+        if (idx < (run.seg0 + seg + 1) * F.bcap) F.bucket[idx] = (rel & (S - 1)) | cls_bit;
+        const uint32_t n = h + p;  // the next hit is past this run (p >= its span)
+        h = n >= h && n < gspan ? n : 0xFFFFFFFFu;
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < kFillPrimesPerThread; ++j) {
+      put(n1[j], pp[j], 0u);
+      put(n5[j], pp[j], S);
+    }
+    __syncthreads();  // every cursor is used before the next run clears hist
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Small base tables: a dense sieve of [0, n] (n <= kTinyMax = 2^18) writing
 // the primes >= 53 in ascending order with their Barrett constants
@@ -1302,6 +1371,10 @@ cudaError_t launch_bucket_fill_huge(const FillParams& f, cudaStream_t st) {
   const uint32_t nb = f.p_end > f.p_begin ? (f.p_end - f.p_begin + per_block - 1) / per_block : 0;
   if (nb == 0 || f.nruns == 0 || f.group_runs == 0) return cudaSuccess;
   dim3 grid(nb, (f.nruns + f.group_runs - 1) / f.group_runs);
+  if (f.huge_step == 1 && !f.huge_loop) {
+    bucket_fill_huge1_kernel<<<grid, kFillThreads, f.max_run_segs * sizeof(uint32_t), st>>>(f);
+    return cudaGetLastError();
+  }
   const size_t smem = (f.max_run_segs + 2 * kFillPrimesPerBlock) * sizeof(uint32_t);
   bucket_fill_huge_kernel<<<grid, kFillThreads, smem, st>>>(f);
   return cudaGetLastError();
