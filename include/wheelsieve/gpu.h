@@ -105,7 +105,9 @@ typedef struct ws_opts {
   int32_t device_ids[WS_MAX_DEVICES];
   uint32_t world;         /* processes sharing each job (0 or 1: this one alone) */
   uint32_t rank;          /* this process's rank in [0, world) */
-  uint8_t nccl_id[WS_NCCL_ID_BYTES]; /* world > 1: the id ws_nccl_unique_id made on rank 0 */
+  uint8_t nccl_id[WS_NCCL_ID_BYTES]; /* world > 1: the id ws_nccl_unique_id made on rank 0
+                                        (ncclCommInitRank); all zero with world 1:
+                                        ncclCommInitAll over device_ids */
 } ws_opts;
 
 typedef struct ws_checks {

@@ -319,6 +319,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
       f.bcount = c->bcount[b].ptr;
       f.bcap = cap;
       f.max_run_segs = static_cast<uint32_t>(piece);
+      f.w_unroll = c->w_unroll;
       if (huge_begin < c->nprimes) {
         // p >= run length: at most one hit per class per run; offsets are
         // carried across runs (bucket_fill_huge_kernel)
@@ -1267,6 +1268,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_HOST_WIRE")) c->host_wire = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_SINGLE_PRED")) c->single_pred = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_HUGE_LOOP")) c->huge_loop = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_FILL_UNROLL")) c->w_unroll = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_BASE_EXTEND")) c->base_extend = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
     c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));
@@ -1429,9 +1431,11 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
     const int k = static_cast<int>(devices.size());
     c->comms.assign(devices.size(), nullptr);
     ncclResult_t r;
-    if (o.world == 1) {
+    bool have_id = false;
+    for (uint8_t b : o.nccl_id) have_id = have_id || b != 0;
+    if (o.world == 1 && !have_id) {
       r = ncclCommInitAll(c->comms.data(), k, devices.data());
-    } else {
+    } else {  // a job shared with other processes (or a caller-made id)
       ncclUniqueId id;
       std::memcpy(&id, o.nccl_id, sizeof id);
       r = ncclGroupStart();

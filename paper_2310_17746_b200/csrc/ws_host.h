@@ -181,6 +181,10 @@ struct DevCtx {
   bool fill_huge = true;               // carried-offset fill for p >= run length (WHEELSIEVE_FILL_HUGE)
   uint32_t huge_step = 1;              // runs per histogram step there (WHEELSIEVE_HUGE_STEP)
   uint32_t huge_loop = 0;              // WHEELSIEVE_HUGE_LOOP=1: the hit-loop kernel at step 1
+  // WHEELSIEVE_FILL_UNROLL=1: fill pass 2 runs both classes, two hits each, per
+  // step (independent cursor atomics); measured slower (C5 23.6 vs 23.3 ms,
+  // C4 51.7 vs 50.9 ms): the predicated lanes cost more than the overlap wins
+  uint32_t w_unroll = 0;
   uint32_t huge_from = 0;              // its lower bound in units of S (0: the run length)
   uint64_t huge_thr = 0;               // the run length in slots the count below is for
   uint32_t n_below_huge = 0;           // table primes (>= 53) below huge_thr

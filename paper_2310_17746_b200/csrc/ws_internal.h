@@ -115,6 +115,7 @@ struct FillParams {
   uint32_t group_runs;      // bucket_fill_huge_kernel: consecutive runs per block row
   uint32_t huge_step;       // ... and runs per histogram step (max_run_segs covers them)
   uint32_t huge_loop;       // 1: the hit-loop kernel even for one run per step (A/B knob)
+  uint32_t w_unroll;        // bucket_fill_kernel pass 2: both classes, 2 hits each per step
 };
 constexpr int kFillThreads = 256;
 constexpr int kFillPrimesPerThread = 16;

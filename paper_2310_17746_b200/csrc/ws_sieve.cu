@@ -1005,25 +1005,55 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_kernel(const FillPar
     hist[i] = (run.seg0 + i) * F.bcap + (c ? atomicAdd(F.bcount + run.seg0 + i, c) : 0u);
   }
   __syncthreads();
-  // pass 2: write the entries
+  // pass 2: write the entries; p is loaded one prime ahead (a plain load at
+  // the point of use stalled every prime's first hit on global latency)
+  uint32_t pw = first + threadIdx.x < p_end ? __ldg(F.prime_p + first + threadIdx.x) : 0u;
 #pragma unroll 1
   for (int j = 0; j < kFillPrimesPerThread; ++j) {
     const uint32_t li = j * kFillThreads + threadIdx.x;
     const uint32_t i = first + li;
     if (i >= p_end) break;
-    const uint32_t r1 = first1[li], r5 = first5[li];
-    if (r1 == 0xFFFFFFFFu && r5 == 0xFFFFFFFFu) continue;
-    const uint32_t p = F.prime_p[i];
+    const uint32_t p = pw;
+    if (i + kFillThreads < p_end && j + 1 < kFillPrimesPerThread)
+      pw = __ldg(F.prime_p + i + kFillThreads);
+    uint32_t h1 = first1[li], h5 = first5[li];
+    if (h1 == 0xFFFFFFFFu && h5 == 0xFFFFFFFFu) continue;
     // an entry is written while its segment's list has room: index below
     // the end of the segment's list (overflow is detected by the sieve)
     auto put = [&](uint32_t seg, uint32_t entry) {
       const uint32_t idx = atomicAdd(hist + seg, 1u);
       if (idx < (run.seg0 + seg + 1) * F.bcap) F.bucket[idx] = entry;
     };
-    if (p <= 0xFFFFFFFFu - span) {
-      for (uint32_t h = r1; h < span; h += p) put(h >> F.log2S, h & (S - 1));
-      for (uint32_t h = r5; h < span; h += p) put(h >> F.log2S, (h & (S - 1)) | S);
+    if (p <= 0xFFFFFFFFu - span && !F.w_unroll) {
+      for (uint32_t h = h1; h < span; h += p) put(h >> F.log2S, h & (S - 1));
+      for (uint32_t h = h5; h < span; h += p) put(h >> F.log2S, (h & (S - 1)) | S);
+    } else if (p <= 0xFFFFFFFFu - span) {
+      // both classes and two hits of each per step: p >= 2S puts consecutive
+      // hits in different segments, so the four cursor atomics are
+      // independent and their round trips overlap (one at a time, every
+      // store waited for its own atomic)
+      while (h1 < span || h5 < span) {
+        const bool a = h1 < span, b = h5 < span;
+        const uint32_t g1 = h1 + p, g5 = h5 + p;  // no wrap: h < span <= 2^32 - 1 - p
+        const bool a2 = a && g1 < span, b2 = b && g5 < span;
+        uint32_t i1 = 0, j1 = 0, i5 = 0, j5 = 0;
+        if (a) i1 = atomicAdd(hist + (h1 >> F.log2S), 1u);
+        if (a2) j1 = atomicAdd(hist + (g1 >> F.log2S), 1u);
+        if (b) i5 = atomicAdd(hist + (h5 >> F.log2S), 1u);
+        if (b2) j5 = atomicAdd(hist + (g5 >> F.log2S), 1u);
+        auto store = [&](bool ok, uint32_t idx, uint32_t h, uint32_t cls) {
+          if (ok && idx < (run.seg0 + (h >> F.log2S) + 1) * F.bcap)
+            F.bucket[idx] = (h & (S - 1)) | cls;
+        };
+        store(a, i1, h1, 0u);
+        store(a2, j1, g1, 0u);
+        store(b, i5, h5, S);
+        store(b2, j5, g5, S);
+        h1 = a2 ? g1 + p : 0xFFFFFFFFu;  // g1 < span: g1 + p cannot wrap either
+        h5 = b2 ? g5 + p : 0xFFFFFFFFu;
+      }
     } else {
+      const uint32_t r1 = h1, r5 = h5;
       for (uint64_t h = r1; h < span; h += p)
         put(static_cast<uint32_t>(h >> F.log2S), static_cast<uint32_t>(h) & (S - 1));
       for (uint64_t h = r5; h < span; h += p)
@@ -1351,6 +1381,14 @@ cudaError_t sieve_configure(int* blocks_per_sm) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fns[m], kThreads, smem);
     if (e != cudaSuccess) return e;
     blocks_per_sm[m] = b < 1 ? 1 : b;
+  }
+  // the fill kernels' histograms + per-prime state can pass the 48 KB default
+  // (runs up to 4096 segments with WHEELSIEVE_FILL_PIECE)
+  for (const void* f : {reinterpret_cast<const void*>(bucket_fill_kernel),
+                        reinterpret_cast<const void*>(bucket_fill_huge_kernel),
+                        reinterpret_cast<const void*>(bucket_fill_huge1_kernel)}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

@@ -213,9 +213,11 @@ class Sieve:
                 o.device_ids[i] = d
             o.world = world
             o.rank = rank
-            if world > 1:
-                if nccl_id is None or len(nccl_id) != WS_NCCL_ID_BYTES:
-                    raise Error(Errc.BadConfig, "world > 1 needs the rank-0 nccl_unique_id()")
+            if world > 1 and nccl_id is None:
+                raise Error(Errc.BadConfig, "world > 1 needs the rank-0 nccl_unique_id()")
+            if nccl_id is not None:  # communicators by ncclCommInitRank with this id
+                if len(nccl_id) != WS_NCCL_ID_BYTES:
+                    raise Error(Errc.BadConfig, f"an NCCL id has {WS_NCCL_ID_BYTES} bytes")
                 for i, b in enumerate(nccl_id):
                     o.nccl_id[i] = b
         elif world != 1:

@@ -179,3 +179,27 @@ def test_duplicate_devices_rejected():
     with pytest.raises(ws.Error) as e:
         ws.Sieve(devices=[d, d])
     assert e.value.code == ws.Errc.BadConfig
+
+
+def test_multiprocess_init_path_one_rank():
+    """The communicator path of a multi-process job (an id from
+    ws_nccl_unique_id, ncclCommInitRank inside an NCCL group), as one rank."""
+    import torch
+    nid = ws.nccl_unique_id()
+    assert len(nid) == 128 and any(nid)
+    with ws.Sieve(devices=[torch.cuda.current_device()], world=1, rank=0, nccl_id=nid) as s:
+        assert s.comm_info(0) == (1, 0) and s.num_shards == 1
+        c = s.count_range(0, 10**9 + 1, checks=True)
+        assert (c.count, c.largest) == (50_847_534, 999_999_937)
+        counts, sums, _ = s.count_intervals(np.array([2**40, 2**41], np.uint64), 10**6)
+        assert counts.tolist() == [s.count_range(2**40, 2**40 + 10**6).count,
+                                   s.count_range(2**41, 2**41 + 10**6).count]
+
+
+def test_bad_multi_configs():
+    with pytest.raises(ws.Error) as e:
+        ws.Sieve(devices=[0], world=2, rank=0)  # no NCCL id
+    assert e.value.code == ws.Errc.BadConfig
+    with pytest.raises(ws.Error) as e:
+        ws.Sieve(devices=[0], world=2, rank=2, nccl_id=bytes(128))  # rank >= world
+    assert e.value.code == ws.Errc.BadConfig
