@@ -672,10 +672,20 @@ def main():
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_env()
     cfg = CONFIGS[args.config]
-    if args.impl == "reference":
-        line = run_reference(args, cfg, world, rank)
-    else:
-        line = run_ours(args, cfg, world, rank, local)
+    # stdout carries exactly one JSON line: while the run goes on, fd 1 (which
+    # native code such as NCCL's version banner writes to) points at stderr
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        if args.impl == "reference":
+            line = run_reference(args, cfg, world, rank)
+        else:
+            line = run_ours(args, cfg, world, rank, local)
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
     if line is not None and rank == 0:
         print(json.dumps(line), flush=True)
 
