@@ -21,6 +21,7 @@
 #include <filesystem>
 #include <fstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "wheelsieve/gpu.h"
@@ -229,6 +230,14 @@ void encode_text(std::string& out, const uint64_t* v, uint64_t n) {  // sink.cpp
   }
 }
 
+uint32_t crc_extend(uint32_t crc, const std::string& bytes) {
+  uLong c = crc;
+  for (size_t off = 0; off < bytes.size(); off += (1u << 30))
+    c = ::crc32(c, reinterpret_cast<const Bytef*>(bytes.data() + off),
+                static_cast<uInt>(std::min<size_t>(1u << 30, bytes.size() - off)));
+  return static_cast<uint32_t>(c);
+}
+
 std::vector<uint64_t> load_and_verify(const fs::path& dir, const FileEntry& f, int format) {
   std::ifstream in(dir / f.name, std::ios::binary);  // sink.cpp:161-183
   if (!in) throw StoreFail{WS_BAD_MANIFEST, "manifest lists missing chunk file " + f.name};
@@ -340,15 +349,32 @@ struct ws_store {
           c = ::crc32(c, b + off, static_cast<uInt>(std::min<uint64_t>(1u << 30, n * 8 - off)));
         cur.crc32 = static_cast<uint32_t>(c);
       }
-    } else {
+    } else if (n < (1u << 20)) {
       text.clear();
       encode_text(text, v, n);
       write_bytes(text.data(), text.size());
-      uLong c = cur.crc32;
-      for (size_t off = 0; off < text.size(); off += (1u << 30))
-        c = ::crc32(c, reinterpret_cast<const Bytef*>(text.data() + off),
-                    static_cast<uInt>(std::min<size_t>(1u << 30, text.size() - off)));
-      cur.crc32 = static_cast<uint32_t>(c);
+      cur.crc32 = crc_extend(cur.crc32, text);
+    } else {
+      // large batches: decimal encoding and CRC in parallel pieces (the
+      // encoding, not the disk, bounds a text store), written in order and
+      // the pieces' CRCs chained with crc32_combine
+      const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+      std::vector<std::string> piece(T);
+      std::vector<uint32_t> pcrc(T, 0);
+      std::vector<std::thread> th;
+      for (unsigned t = 0; t < T; ++t)
+        th.emplace_back([&, t] {
+          const uint64_t a = n * t / T, b = n * (t + 1) / T;
+          piece[t].reserve((b - a) * 17);
+          encode_text(piece[t], v + a, b - a);
+          pcrc[t] = crc_extend(static_cast<uint32_t>(::crc32(0, Z_NULL, 0)), piece[t]);
+        });
+      for (auto& x : th) x.join();
+      for (unsigned t = 0; t < T; ++t) {
+        write_bytes(piece[t].data(), piece[t].size());
+        cur.crc32 = static_cast<uint32_t>(
+            ::crc32_combine(cur.crc32, pcrc[t], static_cast<z_off_t>(piece[t].size())));
+      }
     }
     if (cur.count == 0) cur.min = v[0];
     cur.max = v[n - 1];
