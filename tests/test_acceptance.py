@@ -48,3 +48,31 @@ def test_reference_acceptance_criteria():
     for crit in (1, 2, 3, 4, 5, 7, 8, 9):
         assert status.get(crit) == "PASS", (crit, r.stdout, r.stderr)
     assert status.get(6) in ("PASS", "FAIL", "SKIP")
+
+
+UNIT = os.path.join(ROOT, "tests", "cpp", "_ref", "unit_gpu")
+CLI_T = os.path.join(ROOT, "tests", "cpp", "_ref", "cli_gpu")
+
+
+def test_unit_suite_builds_against_dropin_headers():
+    """The reference's doctest unit suite (test_wheel, test_segment,
+    test_base_store, test_stream, test_sink, test_engine) and test_cli.cpp,
+    unchanged, on tests/cpp/shim/doctest.h."""
+    if not os.path.exists(REF_SRC):
+        pytest.skip("reference sources absent (GPU box): the binaries were built in the container")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "unit"], check=True)
+    assert os.path.exists(UNIT) and os.path.exists(CLI_T)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exe,min_cases", [(UNIT, 79), (CLI_T, 14)])
+def test_reference_unit_suites(exe, min_cases):
+    if not os.path.exists(exe):
+        pytest.skip(f"{os.path.basename(exe)} not built (build() compiles it where /root/reference exists)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1800,
+                       cwd=os.path.join(ROOT, "tests", "cpp"))
+    m = re.search(r"(\d+) test cases, (\d+) failed", r.stdout)
+    assert m, r.stdout[-2000:] + r.stderr[-2000:]
+    assert int(m.group(1)) >= min_cases and int(m.group(2)) == 0, \
+        "\n".join(ln for ln in r.stdout.splitlines() if not ln.startswith("[PASS]"))
+    assert r.returncode == 0
