@@ -197,6 +197,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.out = out;
   p.out_cap = out_cap;
   p.single_pred = c->single_pred;
+  p.mid_bitaddr = c->mid_bitaddr;
   p.words1 = c->words_out[0];
   p.words5 = c->words_out[1];
   if (wire) {
@@ -1267,6 +1268,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_CTAS_PER_SM")) c->ctas_per_sm = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_HOST_WIRE")) c->host_wire = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_SINGLE_PRED")) c->single_pred = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_MID_BITADDR")) c->mid_bitaddr = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_HUGE_LOOP")) c->huge_loop = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_FILL_UNROLL")) c->w_unroll = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_BASE_EXTEND")) c->base_extend = std::atoi(e) != 0;

@@ -194,6 +194,7 @@ struct DevCtx {
   // predicated single-hit atomics (WHEELSIEVE_SINGLE_PRED=1): 17% fewer shared
   // wavefronts at C3 but no faster (204.4 ms either way; C4 +0.2 ms), so off
   uint32_t single_pred = 0;
+  uint32_t mid_bitaddr = 1;            // WHEELSIEVE_MID_BITADDR
 
   // scratch
   DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)

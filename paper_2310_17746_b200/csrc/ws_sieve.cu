@@ -373,6 +373,11 @@ __device__ __forceinline__ void mark_or(uint32_t a0, uint32_t h, uint32_t len, u
   atom_or_shared(a0 + (((h >> 5) & wmask) << 2), h < len ? 1u << (h & 31u) : 0u);
 }
 
+// cross off the bit at shared-memory bit address hb
+__device__ __forceinline__ void mark_bitaddr(uint32_t hb) {
+  atom_or_shared((hb >> 3) & ~3u, 1u << (hb & 31u));
+}
+
 // cross off bit h of the bitmap at shared address a0
 __device__ __forceinline__ void mark(uint32_t a0, uint32_t h) {
   atom_or_shared(a0 + ((h >> 5) << 2), 1u << (h & 31u));
@@ -465,6 +470,10 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   // p < S: one thread per prime, static warp-sized chunks (round robin);
   // both classes advance together (their hits are the same stride p apart)
   {
+    // bit addresses fit 32 bits while the bitmaps sit below 2^28 in the
+    // shared window (always, for unclustered launches)
+    const bool bitaddr = P.mid_bitaddr && a1 < (1u << 28) && a5 < (1u << 28);
+    const uint32_t b1 = a1 << 3;
     uint32_t base = n_wc + 32 * warp;
     uint32_t pn;
     double ipn;
@@ -479,9 +488,23 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       const int32_t d = static_cast<int32_t>(rel5 - rel1);
       const uint32_t dpos = d > 0 ? static_cast<uint32_t>(d) : 0u;
       uint32_t h = rel1;
-      for (; h + dpos < len; h += p) {
-        mark(a1, h);
-        mark(a5, h + d);
+      if (bitaddr) {
+        // the hits as shared-memory BIT addresses: word address (hb >> 3) & ~3
+        // and bit hb & 31 with no base add, and the loop bound precomputed
+        // (12 instructions per pair of marks instead of 14)
+        const uint32_t dd = (a5 << 3) - b1 + static_cast<uint32_t>(d);
+        const uint32_t lim = len > dpos ? b1 + (len - dpos) : 0u;
+        uint32_t hb = b1 + h;
+        for (; hb < lim; hb += p) {
+          mark_bitaddr(hb);
+          mark_bitaddr(hb + dd);
+        }
+        h = hb - b1;
+      } else {
+        for (; h + dpos < len; h += p) {
+          mark(a1, h);
+          mark(a5, h + d);
+        }
       }
       mark_if(a1, h, len);
       mark_if(a5, h + d, d < 0 ? len : 0u);
