@@ -899,7 +899,7 @@ struct Shard {
 
 Shard shard_of(const ws_ctx* ctx, uint32_t g, uint64_t L, uint64_t R) {
   Shard s;
-  const uint32_t S = ctx->devs[0]->S;
+  const uint32_t S = ctx->S;
   if (partition_impl(L, R, S, g, ctx->nshards, &s.lo, &s.hi) != WS_OK)
     throw Fail{WS_OVERFLOW, "range end exceeds the sievable 64-bit range"};
   if (s.hi > s.lo) {
@@ -964,7 +964,7 @@ void count_range_single(DevCtx* d, uint64_t L, uint64_t R, uint32_t flags, ws_ch
 void count_range_multi(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws_checks* out,
                        uint32_t* per_seg, uint64_t per_seg_cap, uint64_t* n_seg) {
   validate_range(L, R);
-  const uint64_t nseg = make_job(L, R, ctx->devs[0]->S, 0).nseg;
+  const uint64_t nseg = make_job(L, R, ctx->S, 0).nseg;
   const bool dev_out = flags & WS_OUT_DEVICE;
   if (per_seg && dev_out && per_seg_cap < nseg)
     throw Fail{WS_CAPACITY, "per_seg capacity below segment count"};
@@ -1411,6 +1411,7 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   ws_ctx* c = new (std::nothrow) ws_ctx;
   if (!c) return WS_OUT_OF_MEMORY;
   c->nccl = o.n_devices > 0;
+  c->S = S;
   c->world = o.world;
   c->rank = o.rank;
   c->nshards = c->nccl ? o.world * static_cast<uint32_t>(devices.size()) : 1;

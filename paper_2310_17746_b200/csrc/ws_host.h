@@ -360,6 +360,8 @@ struct ws_ctx {
   bool nccl = false;
   uint32_t world = 1, rank = 0;  // processes sharing a job, and this one's rank
   uint32_t nshards = 1;          // world * devs.size()
+  uint32_t S = 1u << 18;         // segment slots (DevCtx::S is swapped during base builds,
+                                 // so other threads read this immutable copy)
   std::vector<ncclComm_t> comms;
   wsh::DevWorkers* workers = nullptr;
   std::string err;
