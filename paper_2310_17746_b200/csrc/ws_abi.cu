@@ -626,6 +626,20 @@ void nccl_ck(ncclResult_t r, const char* what) {
 std::vector<wsk::JobAcc> allgather_records(ws_ctx* ctx, const std::vector<const wsk::JobAcc*>& send,
                                            uint64_t n_per) {
   const uint64_t total = n_per * ctx->nshards;
+  if (ctx->virt) {  // test mode: the same records, gathered through the host
+    std::vector<wsk::JobAcc> all(total);
+    for (size_t i = 0; i < ctx->devs.size(); ++i) {
+      DevCtx* d = ctx->devs[i];
+      ck(cudaSetDevice(d->device), "cudaSetDevice");
+      auto* h = static_cast<wsk::JobAcc*>(d->pin_gather.reserve(n_per * sizeof(wsk::JobAcc), "pinned gather"));
+      ck(copy_async(d, h, send[i], n_per * sizeof(wsk::JobAcc), cudaMemcpyDeviceToHost, d->stream),
+         "gather readback");
+      ck(cudaStreamSynchronize(d->stream), "gather sync");
+      ck(cudaGetLastError(), "kernel");
+      std::copy(h, h + n_per, all.begin() + ctx->shard_of(i) * n_per);
+    }
+    return all;
+  }
   for (DevCtx* d : ctx->devs) {
     ck(cudaSetDevice(d->device), "cudaSetDevice");
     d->gather.reserve(total, "gather buffer");
@@ -1401,9 +1415,11 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   } else {
     for (uint32_t i = 0; i < o.n_devices; ++i) devices.push_back(o.device_ids[i]);
   }
+  const char* virt_env = std::getenv("WHEELSIEVE_VIRTUAL_SHARDS");
+  const bool virt = o.n_devices > 0 && o.world == 1 && virt_env && std::atoi(virt_env) != 0;
   for (size_t i = 0; i < devices.size(); ++i) {
     if (devices[i] < 0 || devices[i] >= ndev) return WS_NO_DEVICE;
-    for (size_t j = 0; j < i; ++j)
+    for (size_t j = 0; j < i && !virt; ++j)
       if (devices[j] == devices[i]) return WS_BAD_CONFIG;  // one shard per device
   }
   int prev = -1;
@@ -1430,7 +1446,9 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
       d->host_threads = std::max(1u, cpus / static_cast<unsigned>(devices.size()));
     c->devs.push_back(d);
   }
-  if (c->nccl) {
+  c->virt = virt;
+  if (c->nccl && virt && devices.size() > 1) c->workers = new (std::nothrow) DevWorkers(devices);
+  if (c->nccl && !virt) {
     const int k = static_cast<int>(devices.size());
     c->comms.assign(devices.size(), nullptr);
     ncclResult_t r;
@@ -1499,6 +1517,11 @@ ws_status ws_device_timing(const ws_ctx* ctx, uint32_t i, ws_timing* out) {
 }
 
 ws_status ws_ctx_comm_info(const ws_ctx* ctx, uint32_t i, int32_t* nranks, int32_t* comm_rank) {
+  if (ctx && ctx->virt && nranks && comm_rank && i < ctx->devs.size()) {  // test mode: no NCCL
+    *nranks = static_cast<int32_t>(ctx->nshards);
+    *comm_rank = static_cast<int32_t>(ctx->shard_of(i));
+    return WS_OK;
+  }
   if (!ctx || !nranks || !comm_rank || !ctx->nccl || i >= ctx->comms.size()) return WS_BAD_CONFIG;
   int n = 0, r = 0;
   if (ncclCommCount(ctx->comms[i], &n) != ncclSuccess ||

@@ -358,6 +358,10 @@ class DevWorkers {
 struct ws_ctx {
   std::vector<wsh::DevCtx*> devs;
   bool nccl = false;
+  // test mode (WHEELSIEVE_VIRTUAL_SHARDS=1): several shards on one GPU, the
+  // shard records gathered on the host instead of by NCCL (which refuses two
+  // ranks on one device); everything else is the multi-device path
+  bool virt = false;
   uint32_t world = 1, rank = 0;  // processes sharing a job, and this one's rank
   uint32_t nshards = 1;          // world * devs.size()
   uint32_t S = 1u << 18;         // segment slots (DevCtx::S is swapped during base builds,
