@@ -467,7 +467,7 @@ def run_ours(args, cfg, world, rank, local):
     line = {
         "metric": cfg["metric"], "value": value, "unit": cfg["unit"], "n_gpus": nshards,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong" if kind != "intervals" else "strong",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (deterministic ranges; c5 seeded splitmix64)",
         "config": {"workload": cfg["workload"], "L": L, "R": R, "segment_slots": SEG,

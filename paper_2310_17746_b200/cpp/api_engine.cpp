@@ -83,62 +83,19 @@ SieveReport run_loop(const SieveConfig& config, const std::atomic<bool>* stop,
     rep.wall_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   };
-  // the current block: iterations [blk_first, blk_end)
+  // the block of iterations sieved by the last device call ends at blk_end
   uint64_t blk_end = 0;
   std::vector<uint64_t> vals;       // value sinks: the block's primes
   std::vector<Tile> blk_tiles;      // count sinks: the block's tiles ...
   std::vector<gpu::Checks> counts;  // ... and their results
   size_t tile_cursor = 0;
   std::vector<Tile> tiles;
-  {
-    for (uint64_t i = 0, seg_lo = 0;; ++i, seg_lo += span) {
-      if (bounded && i >= total) break;
-      if (stop && stop->load(std::memory_order_acquire)) {
-        rep.stopped = true;
-        break;
-      }
-      if (!bounded && seg_lo > kMaxSegmentEnd - span) {
-        rep.overflowed = true;
-        break;
-      }
-      const uint64_t seg_hi = (bounded && span > limit_end - seg_lo) ? limit_end : seg_lo + span;
-      tiles.clear();
-      tiles_of(config, seg_lo, seg_hi, tiles);
-      {  // analytic flag accounting of this iteration (engine.cpp:218-230)
-        uint64_t entries = 0, bytes = 0;
-        for (const Tile& t : tiles) {
-          const uint64_t len = (t.hi - t.lo) / 6;
-          entries += 2 * len;
-          bytes += 2 * flag_payload_bytes(len, config.flag_width);
-        }
-        rep.peak_flag_entries = std::max(rep.peak_flag_entries, entries);
-        rep.peak_flag_bytes = std::max(rep.peak_flag_bytes, bytes);
-      }
-      if (i >= blk_end) {  // the next block of iterations on the device
-        uint64_t n = std::min(per_call, (kMaxSegmentEnd - seg_lo) / span);
-        if (bounded) n = std::min(n, total - i);
-        const uint64_t bhi = std::min(seg_lo + n * span, limit_end);
-        if (values) {
-          const uint64_t a = std::max<uint64_t>(seg_lo, 4), b = std::min(bhi, top);
-          vals = a < b ? ctx.enumerate_range(a, b) : std::vector<uint64_t>{};
-        } else {
-          blk_tiles.clear();
-          for (uint64_t k = 0; k < n; ++k)
-            tiles_of(config, seg_lo + k * span, std::min(seg_lo + (k + 1) * span, bhi), blk_tiles);
-          std::vector<uint64_t> Ls(blk_tiles.size()), Rs(blk_tiles.size());
-          for (size_t t = 0; t < blk_tiles.size(); ++t) {
-            Ls[t] = std::max<uint64_t>(blk_tiles[t].lo, 4);
-            Rs[t] = std::max(Ls[t], std::min(blk_tiles[t].hi, top));
-          }
-          counts = ctx.count_ranges(Ls, Rs);
-          tile_cursor = 0;
-        }
-        blk_end = i + n;
-      }
-      // emission in worker order; a sink error becomes SinkFailure with the
-      // totals emitted before it (engine.cpp:264-296)
-      try {
-      if (i == 0) {  // 2 and 3 lead the stream (engine.cpp:268-276)
+  // one iteration's batches in worker order: 2 and 3 first (engine.cpp:268-276),
+  // then one per non-empty tile; a sink error becomes SinkFailure with the
+  // totals emitted before it (engine.cpp:264-296)
+  auto emit_iteration = [&](uint64_t i) {
+    try {
+      if (i == 0) {
         static constexpr uint64_t kFirst[2] = {2, 3};
         const size_t n = (!bounded || limit >= 3) ? 2 : 1;
         if (values)
@@ -156,15 +113,60 @@ SieveReport run_loop(const SieveConfig& config, const std::atomic<bool>* stop,
           if (r.count) sink.emit_count(r.count, r.largest);
         }
       }
-      } catch (const Error& e) {
-        rep.prime_count = sink.count();
-        rep.largest_prime = sink.largest();
-        stamp();
-        throw SinkFailure(e.code(), e.what(), rep);
-      }
-      rep.iterations = i + 1;
-      rep.sieved_to = seg_hi;
+    } catch (const Error& e) {
+      rep.prime_count = sink.count();
+      rep.largest_prime = sink.largest();
+      stamp();
+      throw SinkFailure(e.code(), e.what(), rep);
     }
+  };
+  for (uint64_t i = 0, seg_lo = 0;; ++i, seg_lo += span) {
+    if (bounded && i >= total) break;
+    if (stop && stop->load(std::memory_order_acquire)) {
+      rep.stopped = true;
+      break;
+    }
+    if (!bounded && seg_lo > kMaxSegmentEnd - span) {
+      rep.overflowed = true;
+      break;
+    }
+    const uint64_t seg_hi = (bounded && span > limit_end - seg_lo) ? limit_end : seg_lo + span;
+    tiles.clear();
+    tiles_of(config, seg_lo, seg_hi, tiles);
+    {  // analytic flag accounting of this iteration (engine.cpp:218-230)
+      uint64_t entries = 0, bytes = 0;
+      for (const Tile& t : tiles) {
+        const uint64_t len = (t.hi - t.lo) / 6;
+        entries += 2 * len;
+        bytes += 2 * flag_payload_bytes(len, config.flag_width);
+      }
+      rep.peak_flag_entries = std::max(rep.peak_flag_entries, entries);
+      rep.peak_flag_bytes = std::max(rep.peak_flag_bytes, bytes);
+    }
+    if (i >= blk_end) {  // the next block of iterations on the device
+      uint64_t n = std::min(per_call, (kMaxSegmentEnd - seg_lo) / span);
+      if (bounded) n = std::min(n, total - i);
+      const uint64_t bhi = std::min(seg_lo + n * span, limit_end);
+      if (values) {
+        const uint64_t a = std::max<uint64_t>(seg_lo, 4), b = std::min(bhi, top);
+        vals = a < b ? ctx.enumerate_range(a, b) : std::vector<uint64_t>{};
+      } else {
+        blk_tiles.clear();
+        for (uint64_t k = 0; k < n; ++k)
+          tiles_of(config, seg_lo + k * span, std::min(seg_lo + (k + 1) * span, bhi), blk_tiles);
+        std::vector<uint64_t> Ls(blk_tiles.size()), Rs(blk_tiles.size());
+        for (size_t t = 0; t < blk_tiles.size(); ++t) {
+          Ls[t] = std::max<uint64_t>(blk_tiles[t].lo, 4);
+          Rs[t] = std::max(Ls[t], std::min(blk_tiles[t].hi, top));
+        }
+        counts = ctx.count_ranges(Ls, Rs);
+        tile_cursor = 0;
+      }
+      blk_end = i + n;
+    }
+    emit_iteration(i);
+    rep.iterations = i + 1;
+    rep.sieved_to = seg_hi;
   }
   if (bounded) rep.sieved_to = limit + 1;
   rep.prime_count = sink.count();
