@@ -66,3 +66,21 @@ def test_writer_durability_and_errors(tmp_path):
     assert lib.ws_store_close(st) == 0
     assert sorted(os.listdir(tmp_path / "s")) == ["manifest.json", "primes_00000.bin",
                                                    "primes_00001.bin"]
+
+
+@pytest.mark.parametrize("binary", [True, False])
+def test_large_batches_write_in_parallel_pieces(tmp_path, binary):
+    """Batches above 64 MB go out as parallel pwrite()s (and, in text, parallel
+    encoding): the files equal those of many small sequential batches, and
+    their recorded CRC-32s verify."""
+    rng = np.random.default_rng(3)
+    values = np.cumsum(rng.integers(1, 40, 9_000_000, dtype=np.uint64)).astype(np.uint64)
+    big, small = tmp_path / "big", tmp_path / "small"
+    _write(big, values, binary, 5_000_000, 1, int(values[-1]) + 1)
+    _write(small, values, binary, 5_000_000, 97, int(values[-1]) + 1)
+    a, b = _files(big), _files(small)
+    assert sorted(a) == sorted(b) == ["manifest.json", f"primes_00000.{'bin' if binary else 'txt'}",
+                                       f"primes_00001.{'bin' if binary else 'txt'}"]
+    for name in a:
+        assert a[name] == b[name], name
+    assert lib.ws_verify_store(str(big).encode()) == 0
