@@ -14,6 +14,7 @@
 //      the enumerated values.
 // No exception crosses the ABI; errors become ws_status + ws_last_error.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -30,6 +31,36 @@
 #include "ws_host.h"
 #include "ws_internal.h"
 #include "ws_wire.h"
+
+namespace wsh {
+
+const NcclApi* nccl_api() {
+  static const NcclApi* api = [] () -> const NcclApi* {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return nullptr;
+    static NcclApi a;
+    bool ok = true;
+    auto get = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      ok = ok && fn != nullptr;
+    };
+    get(a.GetUniqueId, "ncclGetUniqueId");
+    get(a.CommInitAll, "ncclCommInitAll");
+    get(a.CommInitRank, "ncclCommInitRank");
+    get(a.CommDestroy, "ncclCommDestroy");
+    get(a.GroupStart, "ncclGroupStart");
+    get(a.GroupEnd, "ncclGroupEnd");
+    get(a.AllGather, "ncclAllGather");
+    get(a.CommCount, "ncclCommCount");
+    get(a.CommUserRank, "ncclCommUserRank");
+    get(a.GetErrorString, "ncclGetErrorString");
+    return ok ? &a : nullptr;
+  }();
+  return api;
+}
+
+}  // namespace wsh
 
 using namespace wsh;
 
@@ -614,7 +645,8 @@ void on_devices(ws_ctx* ctx, const std::function<void(DevCtx*, size_t)>& fn) {
 }
 
 void nccl_ck(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) throw Fail{WS_NCCL, std::string(what) + ": " + ncclGetErrorString(r)};
+  if (r != ncclSuccess)
+    throw Fail{WS_NCCL, std::string(what) + ": " + nccl_api()->GetErrorString(r)};
 }
 
 // The context's one collective: every shard contributes n_per 32-byte
@@ -644,18 +676,18 @@ std::vector<wsk::JobAcc> allgather_records(ws_ctx* ctx, const std::vector<const 
     ck(cudaSetDevice(d->device), "cudaSetDevice");
     d->gather.reserve(total, "gather buffer");
   }
-  nccl_ck(ncclGroupStart(), "ncclGroupStart");
+  nccl_ck(nccl_api()->GroupStart(), "ncclGroupStart");
   for (size_t i = 0; i < ctx->devs.size(); ++i) {
     DevCtx* d = ctx->devs[i];
     ck(cudaSetDevice(d->device), "cudaSetDevice");
-    const ncclResult_t r = ncclAllGather(send[i], d->gather.ptr, 4 * n_per, ncclUint64,
-                                         ctx->comms[i], d->stream);
+    const ncclResult_t r = nccl_api()->AllGather(send[i], d->gather.ptr, 4 * n_per, ncclUint64,
+                                                 ctx->comms[i], d->stream);
     if (r != ncclSuccess) {
-      ncclGroupEnd();
+      nccl_api()->GroupEnd();
       nccl_ck(r, "ncclAllGather");
     }
   }
-  nccl_ck(ncclGroupEnd(), "ncclGroupEnd");
+  nccl_ck(nccl_api()->GroupEnd(), "ncclGroupEnd");
   DevCtx* d0 = ctx->devs[0];
   ck(cudaSetDevice(d0->device), "cudaSetDevice");
   auto* h = static_cast<wsk::JobAcc*>(d0->pin_gather.reserve(total * sizeof(wsk::JobAcc), "pinned gather"));
@@ -1375,7 +1407,7 @@ ws_status ws_nccl_unique_id(uint8_t* id) {
   if (!id) return WS_BAD_CONFIG;
   static_assert(sizeof(ncclUniqueId) == WS_NCCL_ID_BYTES, "ncclUniqueId size");
   ncclUniqueId u;
-  if (ncclGetUniqueId(&u) != ncclSuccess) return WS_NCCL;
+  if (!nccl_api() || nccl_api()->GetUniqueId(&u) != ncclSuccess) return WS_NCCL;
   std::memcpy(id, &u, sizeof u);
   return WS_OK;
 }
@@ -1448,24 +1480,30 @@ ws_status ws_ctx_create(const ws_opts* opts, ws_ctx** out) {
   }
   c->virt = virt;
   if (c->nccl && virt && devices.size() > 1) c->workers = new (std::nothrow) DevWorkers(devices);
+  if (c->nccl && !virt && !nccl_api()) {
+    delete c;
+    if (prev >= 0) cudaSetDevice(prev);
+    return WS_NCCL;
+  }
   if (c->nccl && !virt) {
+    const NcclApi* N = nccl_api();
     const int k = static_cast<int>(devices.size());
     c->comms.assign(devices.size(), nullptr);
     ncclResult_t r;
     bool have_id = false;
     for (uint8_t b : o.nccl_id) have_id = have_id || b != 0;
     if (o.world == 1 && !have_id) {
-      r = ncclCommInitAll(c->comms.data(), k, devices.data());
+      r = N->CommInitAll(c->comms.data(), k, devices.data());
     } else {  // a job shared with other processes (or a caller-made id)
       ncclUniqueId id;
       std::memcpy(&id, o.nccl_id, sizeof id);
-      r = ncclGroupStart();
+      r = N->GroupStart();
       for (int i = 0; i < k && r == ncclSuccess; ++i) {
         cudaSetDevice(devices[i]);
-        r = ncclCommInitRank(&c->comms[i], static_cast<int>(o.world) * k, id,
-                             static_cast<int>(o.rank) * k + i);
+        r = N->CommInitRank(&c->comms[i], static_cast<int>(o.world) * k, id,
+                            static_cast<int>(o.rank) * k + i);
       }
-      const ncclResult_t r2 = ncclGroupEnd();
+      const ncclResult_t r2 = N->GroupEnd();
       if (r == ncclSuccess) r = r2;
     }
     if (r != ncclSuccess) {
@@ -1524,8 +1562,8 @@ ws_status ws_ctx_comm_info(const ws_ctx* ctx, uint32_t i, int32_t* nranks, int32
   }
   if (!ctx || !nranks || !comm_rank || !ctx->nccl || i >= ctx->comms.size()) return WS_BAD_CONFIG;
   int n = 0, r = 0;
-  if (ncclCommCount(ctx->comms[i], &n) != ncclSuccess ||
-      ncclCommUserRank(ctx->comms[i], &r) != ncclSuccess)
+  if (nccl_api()->CommCount(ctx->comms[i], &n) != ncclSuccess ||
+      nccl_api()->CommUserRank(ctx->comms[i], &r) != ncclSuccess)
     return WS_NCCL;
   *nranks = n;
   *comm_rank = r;

@@ -289,6 +289,24 @@ struct DevCtx {
 
 namespace wsh {
 
+// NCCL, loaded on first use (dlopen of libnccl.so.2 -- or the copy already in
+// the process, e.g. PyTorch's): single-device users never pay for mapping the
+// ~400 MB library, and a multi-device context fails with WS_NCCL, not the
+// whole library with a load error, where NCCL is missing.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*CommCount)(const ncclComm_t, int*);
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+const NcclApi* nccl_api();  // nullptr when libnccl.so.2 cannot be loaded
+
 // One host thread per local device of a multi-device context.  run(fn)
 // executes fn(i) on worker i for every device concurrently and returns when
 // all have finished; each worker keeps its device current.
@@ -373,7 +391,7 @@ struct ws_ctx {
   ~ws_ctx() {
     delete workers;
     for (ncclComm_t c : comms)
-      if (c) ncclCommDestroy(c);
+      if (c && wsh::nccl_api()) wsh::nccl_api()->CommDestroy(c);
     for (wsh::DevCtx* d : devs) delete d;
   }
   uint32_t shard_of(size_t i) const { return rank * static_cast<uint32_t>(devs.size()) + static_cast<uint32_t>(i); }

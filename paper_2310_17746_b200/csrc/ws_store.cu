@@ -333,51 +333,16 @@ struct ws_store {
     cur.crc32 = static_cast<uint32_t>(::crc32(0, Z_NULL, 0));
   }
 
-  // Large writes go out as parallel pwrite()s of pieces at their file
-  // offsets: one thread copying into the page cache caps a binary store near
-  // 3.5 GB/s.
-  static constexpr size_t kParallelWrite = size_t{64} << 20;
-
   void write_at(const std::vector<std::pair<const char*, size_t>>& parts) {
-    size_t total = 0;
-    for (const auto& pr : parts) total += pr.second;
-    if (total < kParallelWrite) {
-      for (const auto& pr : parts)
-        if (pr.second && std::fwrite(pr.first, 1, pr.second, fp) != pr.second)
-          throw StoreFail{WS_IO, "write to " + cur.name + " failed" + durable_note()};
-      return;
-    }
-    if (std::fflush(fp) != 0) throw StoreFail{WS_IO, "write to " + cur.name + " failed" + durable_note()};
-    const off_t base = ftello(fp);
-    const int fd = fileno(fp);
-    std::vector<std::thread> th;
-    std::atomic<bool> ok{true};
-    off_t at = base;
-    for (const auto& pr : parts) {
-      th.emplace_back([&, pr, at] {
-        for (size_t done = 0; done < pr.second;) {
-          const ssize_t w = ::pwrite(fd, pr.first + done, pr.second - done, at + done);
-          if (w <= 0) {
-            ok = false;
-            return;
-          }
-          done += static_cast<size_t>(w);
-        }
-      });
-      at += static_cast<off_t>(pr.second);
-    }
-    for (auto& t : th) t.join();
-    if (!ok || fseeko(fp, at, SEEK_SET) != 0)
-      throw StoreFail{WS_IO, "write to " + cur.name + " failed" + durable_note()};
+    // sequential: writes to one file serialise on its inode anyway (parallel
+    // pwrite()s measured no faster, C4e store 2.7 vs 3.2 GB/s)
+    for (const auto& pr : parts)
+      if (pr.second && std::fwrite(pr.first, 1, pr.second, fp) != pr.second)
+        throw StoreFail{WS_IO, "write to " + cur.name + " failed" + durable_note()};
   }
 
-  void write_bytes(const void* p, size_t n) {
-    const char* c = static_cast<const char*>(p);
-    std::vector<std::pair<const char*, size_t>> parts;
-    const size_t T = n < kParallelWrite ? 1 : std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency()));
-    for (size_t t = 0; t < T; ++t) parts.emplace_back(c + n * t / T, n * (t + 1) / T - n * t / T);
-    write_at(parts);
-  }
+  void write_bytes(const void* p, size_t n) { write_at({{static_cast<const char*>(p), n}}); }
+
 
   // n ascending values into the open file; crc_known: the CRC-32 of their
   // little-endian bytes, computed on the device (binary format only)
