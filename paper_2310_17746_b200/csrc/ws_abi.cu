@@ -275,13 +275,19 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   std::vector<wsk::Run> runs;
   std::vector<uint32_t> run_off(nwin + 1, 0);
   uint64_t piece = W;
+  bool staged = false;
   if (buckets) {
     // optional cap on sieve CTAs per SM to leave room for fill CTAs (measured: no gain)
     if (c->bucket_ctas_per_sm)
       max_grid = std::min<uint64_t>(max_grid, static_cast<uint64_t>(c->sms) * c->bucket_ctas_per_sm);
     // runs are cut into 32-segment pieces: short per-thread hit loops and a
     // fill grid that covers the GPU (measured best for c4 and c5)
-    piece = c->piece_override ? c->piece_override : 32;
+    // (64 with the staged fills of a single-job window: their queues flush
+    // whole chunks, so longer pieces keep write locality -- C4 51.3 -> 50.4 ms;
+    // multi-job windows such as C5's keep the two-pass fills, where staging
+    // measured slower: 22.5 vs 24.2 ms)
+    staged = nj == 1 && c->stage_cap > 0;
+    piece = c->piece_override ? c->piece_override : (staged ? 64 : 32);
     piece = std::min<uint64_t>(piece, W);
     // a run's span in slots is indexed in 32 bits by the fill kernels
     piece = std::max<uint64_t>(1, std::min<uint64_t>(piece, (0xFFFFFFFFull / c->S) - 1));
@@ -352,6 +358,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
       f.bcap = cap;
       f.max_run_segs = static_cast<uint32_t>(piece);
       f.w_unroll = c->w_unroll;
+      f.stage_cap = staged ? c->stage_cap : 0;
       if (huge_begin < c->nprimes) {
         // p >= run length: at most one hit per class per run; offsets are
         // carried across runs (bucket_fill_huge_kernel)
@@ -1317,6 +1324,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_MID_BITADDR")) c->mid_bitaddr = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_HUGE_LOOP")) c->huge_loop = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_FILL_UNROLL")) c->w_unroll = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_STAGE_CAP")) c->stage_cap = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BASE_EXTEND")) c->base_extend = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
     c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));

@@ -185,6 +185,7 @@ struct DevCtx {
   // step (independent cursor atomics); measured slower (C5 23.6 vs 23.3 ms,
   // C4 51.7 vs 50.9 ms): the predicated lanes cost more than the overlap wins
   uint32_t w_unroll = 0;
+  uint32_t stage_cap = 256;            // WHEELSIEVE_STAGE_CAP: staged fill queue entries (0: two-pass fills)
   uint32_t huge_from = 0;              // its lower bound in units of S (0: the run length)
   uint64_t huge_thr = 0;               // the run length in slots the count below is for
   uint32_t n_below_huge = 0;           // table primes (>= 53) below huge_thr

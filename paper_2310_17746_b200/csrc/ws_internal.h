@@ -117,6 +117,8 @@ struct FillParams {
   uint32_t huge_step;       // ... and runs per histogram step (max_run_segs covers them)
   uint32_t huge_loop;       // 1: the hit-loop kernel even for one run per step (A/B knob)
   uint32_t w_unroll;        // bucket_fill_kernel pass 2: both classes, 2 hits each per step
+  uint32_t stage_cap;       // > 0: staged fills, per-segment shared-memory queues of this
+                            // many entries flushed as contiguous chunks (0: two-pass fills)
 };
 constexpr int kFillThreads = 256;
 constexpr int kFillPrimesPerThread = 16;

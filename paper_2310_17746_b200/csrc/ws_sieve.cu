@@ -1245,6 +1245,193 @@ __global__ void __launch_bounds__(kFillThreads) bucket_fill_huge1_kernel(const F
 }
 
 // ---------------------------------------------------------------------------
+// Staged fills.  The two-pass fills above store every hit straight to its
+// segment's list: the 32 lanes of a store hit 32 different lists, so each
+// warp store is 32 separate L1 wavefronts and 32 partial L2 sectors -- about
+// one data-pipe wavefront per 4-byte entry.  The staged fills queue a batch's
+// hits per segment in shared memory (one returning shared atomic + one
+// shared store each) and then flush every queue as one contiguous chunk: one
+// global reservation (atomicAdd on the segment's count) per (batch, segment)
+// and coalesced stores, ~1/32 wavefront per entry.  No histogram pass: the
+// reservation happens at flush time.  A queue that fills up sends its extra
+// hits down the direct path (one global atomic each), so any cap is correct.
+// bcount[s] still counts every hit of segment s, written or not, so an
+// overflowed list is detected by the sieve exactly as before.
+
+// queue entry `entry` for window segment gseg (run-local seg)
+__device__ __forceinline__ void stage_put(const FillParams& F, uint32_t* scnt, uint32_t* stage,
+                                          uint32_t cap, uint32_t seg, uint32_t gseg,
+                                          uint32_t entry) {
+  const uint32_t idx = atomicAdd(scnt + seg, 1u);
+  if (idx < cap) {
+    stage[seg * cap + idx] = entry;
+  } else {
+    const uint32_t g = atomicAdd(F.bcount + gseg, 1u);
+    if (g < F.bcap) F.bucket[gseg * F.bcap + g] = entry;
+  }
+}
+
+// every queue of the run's nseg segments to its list, queues left empty.
+// Called by the whole block right after a __syncthreads that ends the puts.
+// Reservations first, all in flight together (one global atomic per
+// non-empty queue, one thread each: a single round trip), then every warp
+// copies whole queues with coalesced stores.  sbase: nseg words of scratch.
+// Ends with a __syncthreads (the queues are empty for the next puts).
+__device__ __forceinline__ void stage_flush(const FillParams& F, uint32_t* scnt, uint32_t* sbase,
+                                            const uint32_t* stage, uint32_t cap, uint32_t seg0,
+                                            uint32_t nseg) {
+  for (uint32_t s = threadIdx.x; s < nseg; s += kFillThreads) {
+    const uint32_t c = scnt[s];
+    const uint32_t n = c < cap ? c : cap;
+    scnt[s] = n;
+    sbase[s] = n ? atomicAdd(F.bcount + seg0 + s, n) : 0u;
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (uint32_t s = warp; s < nseg; s += kFillThreads / 32) {
+    const uint32_t n = scnt[s], base = sbase[s];
+    if (base >= F.bcap) continue;
+    const uint32_t lim = F.bcap - base < n ? F.bcap - base : n;
+    uint32_t* dst = F.bucket + (seg0 + s) * F.bcap + base;
+    const uint32_t* src = stage + s * cap;
+    for (uint32_t i = lane; i < lim; i += 32) dst[i] = src[i];
+  }
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < nseg; s += kFillThreads) scnt[s] = 0;
+  __syncthreads();  // the queues are empty again
+}
+
+// bucket_fill_kernel, staged: a batch is one prime per thread (256 primes);
+// each batch's hits over the run are queued, then flushed.
+__global__ void __launch_bounds__(kFillThreads) bucket_fill_staged_kernel(const FillParams F) {
+  extern __shared__ uint32_t fill_smem[];
+  uint32_t* scnt = fill_smem;                        // max_run_segs queue lengths
+  uint32_t* sbase = fill_smem + F.max_run_segs;      // ... and their list reservations
+  uint32_t* stage = fill_smem + 2 * F.max_run_segs;  // max_run_segs queues of stage_cap entries
+  const uint32_t cap = F.stage_cap;
+  const Run run = F.runs[blockIdx.y];
+  const uint32_t S = 1u << F.log2S;
+  const uint32_t span = static_cast<uint32_t>(run.k_hi - run.k_lo);  // < 2^32 (host bound)
+  const uint32_t t_lo = isqrt64(6 * run.k_lo), t_hi = isqrt64(6 * run.k_hi);
+  const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
+  const uint32_t p_end = F.nprimes_dev ? min(F.p_end, *F.nprimes_dev) : F.p_end;
+  if (first >= p_end || __ldg(F.prime_p + first) > t_hi) return;  // see bucket_fill_kernel
+  const ModCtx mc = mod_ctx(run.k_lo);
+  for (uint32_t i = threadIdx.x; i < run.nseg; i += kFillThreads) scnt[i] = 0;
+  uint32_t pn = 0;
+  double ipn = 0.0;
+  if (first + threadIdx.x < p_end) {
+    pn = __ldg(F.prime_p + first + threadIdx.x);
+    ipn = __ldg(F.prime_inv + first + threadIdx.x);
+  }
+  // primes per thread per batch: a batch of kb * 256 primes from p0 up puts
+  // at most kb * 256 * 2S / p0 hits in a segment's queue on average; keep that
+  // near 3/4 of the capacity
+  const uint32_t p0 = __ldg(F.prime_p + first);
+  const uint32_t kb = max(1u, min(static_cast<uint32_t>(kFillPrimesPerThread),
+                                  static_cast<uint32_t>((3ull * cap * p0) / (2048ull * S))));
+  __syncthreads();  // the queues are empty
+#pragma unroll 1
+  for (int j = 0; j < kFillPrimesPerThread; ++j) {
+    const uint32_t b0 = first + j * kFillThreads;  // this step's first prime (block-uniform)
+    const uint32_t i = b0 + threadIdx.x;
+    const uint32_t p = pn;
+    const double ip = ipn;
+    // primes ascend: once a step's first prime is inactive in the run, so is the rest
+    if (b0 >= p_end || __ldg(F.prime_p + b0) > t_hi) break;
+    if (i + kFillThreads < p_end && j + 1 < kFillPrimesPerThread) {
+      pn = __ldg(F.prime_p + i + kFillThreads);
+      ipn = __ldg(F.prime_inv + i + kFillThreads);
+    }
+    uint32_t q1, q5;
+    if (i < p_end && prime_offsets(p, ip, i, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
+      if (p <= 0xFFFFFFFFu - span) {  // 32-bit stepping cannot wrap
+        for (uint32_t h = q1; h < span; h += p)
+          stage_put(F, scnt, stage, cap, h >> F.log2S, run.seg0 + (h >> F.log2S), h & (S - 1));
+        for (uint32_t h = q5; h < span; h += p)
+          stage_put(F, scnt, stage, cap, h >> F.log2S, run.seg0 + (h >> F.log2S),
+                    (h & (S - 1)) | S);
+      } else {  // p within `span` of 2^32 (top of the 64-bit value range)
+        for (uint64_t h = q1; h < span; h += p) {
+          const uint32_t seg = static_cast<uint32_t>(h >> F.log2S);
+          stage_put(F, scnt, stage, cap, seg, run.seg0 + seg, static_cast<uint32_t>(h) & (S - 1));
+        }
+        for (uint64_t h = q5; h < span; h += p) {
+          const uint32_t seg = static_cast<uint32_t>(h >> F.log2S);
+          stage_put(F, scnt, stage, cap, seg, run.seg0 + seg,
+                    (static_cast<uint32_t>(h) & (S - 1)) | S);
+        }
+      }
+    }
+    // flush after every kb-th prime, and after the block's last active one
+    const bool last = j + 1 == kFillPrimesPerThread || b0 + kFillThreads >= p_end ||
+                      __ldg(F.prime_p + b0 + kFillThreads) > t_hi;
+    if ((j + 1) % kb == 0 || last) {
+      __syncthreads();
+      stage_flush(F, scnt, sbase, stage, cap, run.seg0, run.nseg);
+    }
+  }
+}
+
+// bucket_fill_huge1_kernel, staged: per run, the block's <= 2 hits per prime
+// are queued, then flushed (no histogram pass, no reservation pass).
+__global__ void __launch_bounds__(kFillThreads) bucket_fill_huge1_staged_kernel(const FillParams F) {
+  extern __shared__ uint32_t fill_smem[];
+  uint32_t* scnt = fill_smem;
+  uint32_t* sbase = fill_smem + F.max_run_segs;
+  uint32_t* stage = fill_smem + 2 * F.max_run_segs;
+  const uint32_t cap = F.stage_cap;
+  const uint32_t r_begin = blockIdx.y * F.group_runs;
+  const uint32_t r_end = min(F.nruns, r_begin + F.group_runs);
+  const uint64_t g_lo = F.runs[r_begin].k_lo, g_hi = F.runs[r_end - 1].k_hi;
+  const uint32_t S = 1u << F.log2S;
+  const uint32_t t_lo = isqrt64(6 * g_lo), t_hi = isqrt64(6 * g_hi);
+  const ModCtx mc = mod_ctx(g_lo);
+  const uint32_t gspan = static_cast<uint32_t>(g_hi - g_lo);  // < 2^31 (host bound)
+  const uint32_t first = F.p_begin + blockIdx.x * kFillPrimesPerBlock;
+  const uint32_t p_end = F.nprimes_dev ? min(F.p_end, *F.nprimes_dev) : F.p_end;
+  uint32_t pp[kFillPrimesPerThread], n1[kFillPrimesPerThread], n5[kFillPrimesPerThread];
+#pragma unroll
+  for (int j = 0; j < kFillPrimesPerThread; ++j) {
+    const uint32_t i = first + j * kFillThreads + threadIdx.x;
+    pp[j] = 0;
+    n1[j] = n5[j] = 0xFFFFFFFFu;
+    if (i < p_end) {
+      pp[j] = __ldg(F.prime_p + i);
+      uint32_t q1, q5;
+      if (prime_offsets(pp[j], __ldg(F.prime_inv + i), i, F.prime_m, mc, t_lo, t_hi, q1, q5)) {
+        if (q1 < gspan) n1[j] = q1;
+        if (q5 < gspan) n5[j] = q5;
+      }
+    }
+  }
+  for (uint32_t k = threadIdx.x; k < F.max_run_segs; k += kFillThreads) scnt[k] = 0;
+  __syncthreads();
+#pragma unroll 1
+  for (uint32_t r = r_begin; r < r_end; ++r) {
+    const Run run = F.runs[r];
+    const uint32_t lo = static_cast<uint32_t>(run.k_lo - g_lo);
+    const uint32_t hi = static_cast<uint32_t>(run.k_hi - g_lo);
+    auto put = [&](uint32_t& h, uint32_t p, uint32_t cls_bit) {
+      if (h < hi) {
+        const uint32_t rel = h - lo;
+        const uint32_t seg = rel >> F.log2S;
+        stage_put(F, scnt, stage, cap, seg, run.seg0 + seg, (rel & (S - 1)) | cls_bit);
+        const uint32_t n = h + p;  // the next hit is past this run (p >= its span)
+        h = n >= h && n < gspan ? n : 0xFFFFFFFFu;
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < kFillPrimesPerThread; ++j) {
+      put(n1[j], pp[j], 0u);
+      put(n5[j], pp[j], S);
+    }
+    __syncthreads();
+    stage_flush(F, scnt, sbase, stage, cap, run.seg0, run.nseg);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Small base tables: a dense sieve of [0, n] (n <= kTinyMax = 2^18) writing
 // the primes >= 53 in ascending order with their Barrett constants
 // (naive_sieve, wheel.cpp:40-54).  Used as level 0 of the two-level base build
@@ -1409,7 +1596,9 @@ cudaError_t sieve_configure(int* blocks_per_sm) {
   // (runs up to 4096 segments with WHEELSIEVE_FILL_PIECE)
   for (const void* f : {reinterpret_cast<const void*>(bucket_fill_kernel),
                         reinterpret_cast<const void*>(bucket_fill_huge_kernel),
-                        reinterpret_cast<const void*>(bucket_fill_huge1_kernel)}) {
+                        reinterpret_cast<const void*>(bucket_fill_huge1_kernel),
+                        reinterpret_cast<const void*>(bucket_fill_staged_kernel),
+                        reinterpret_cast<const void*>(bucket_fill_huge1_staged_kernel)}) {
     e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     if (e != cudaSuccess) return e;
   }
@@ -1427,12 +1616,33 @@ cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t 
   return cudaGetLastError();
 }
 
+// staged fills: the queue capacity that fits the dynamic shared-memory limit
+// (kFillSmemMax) with the run's queue lengths, 0 = use the two-pass kernels
+constexpr size_t kFillSmemMax = 96 * 1024;
+uint32_t stage_cap_for(const FillParams& f) {
+  if (f.stage_cap == 0 || f.max_run_segs == 0) return 0;
+  const size_t words = kFillSmemMax / sizeof(uint32_t);
+  if (words <= 2 * f.max_run_segs) return 0;
+  const size_t fit = (words - 2 * f.max_run_segs) / f.max_run_segs;
+  const uint32_t cap = static_cast<uint32_t>(fit < f.stage_cap ? fit : f.stage_cap);
+  return cap >= 32 ? cap : 0;
+}
+size_t stage_smem(const FillParams& f) {
+  return static_cast<size_t>(f.max_run_segs) * (2 + f.stage_cap) * sizeof(uint32_t);
+}
+
 cudaError_t launch_bucket_fill_huge(const FillParams& f, cudaStream_t st) {
   const uint32_t per_block = kFillThreads * kFillPrimesPerThread;
   const uint32_t nb = f.p_end > f.p_begin ? (f.p_end - f.p_begin + per_block - 1) / per_block : 0;
   if (nb == 0 || f.nruns == 0 || f.group_runs == 0) return cudaSuccess;
   dim3 grid(nb, (f.nruns + f.group_runs - 1) / f.group_runs);
   if (f.huge_step == 1 && !f.huge_loop) {
+    if (const uint32_t cap = stage_cap_for(f)) {
+      FillParams g = f;
+      g.stage_cap = cap;
+      bucket_fill_huge1_staged_kernel<<<grid, kFillThreads, stage_smem(g), st>>>(g);
+      return cudaGetLastError();
+    }
     bucket_fill_huge1_kernel<<<grid, kFillThreads, f.max_run_segs * sizeof(uint32_t), st>>>(f);
     return cudaGetLastError();
   }
@@ -1446,6 +1656,12 @@ cudaError_t launch_bucket_fill(const FillParams& f, cudaStream_t st) {
   const uint32_t nb = (f.p_end - f.p_begin + per_block - 1) / per_block;
   if (nb == 0 || f.nruns == 0) return cudaSuccess;
   dim3 grid(nb, f.nruns);
+  if (const uint32_t cap = stage_cap_for(f)) {
+    FillParams g = f;
+    g.stage_cap = cap;
+    bucket_fill_staged_kernel<<<grid, kFillThreads, stage_smem(g), st>>>(g);
+    return cudaGetLastError();
+  }
   const size_t smem = (f.max_run_segs + 2 * kFillPrimesPerBlock) * sizeof(uint32_t);
   bucket_fill_kernel<<<grid, kFillThreads, smem, st>>>(f);
   return cudaGetLastError();
