@@ -173,6 +173,15 @@ struct WireArgs {  // kEnumWire outputs
   uint8_t* blk8;
 };
 
+// A call's timing events (ev[2] start, ev[3] end of the sieve): while the
+// stream is being captured into a graph they become event-record nodes, so a
+// replayed call still times its sieve.
+void record_timing_event(DevCtx* c, cudaEvent_t e) {
+  ck(c->capturing ? cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal)
+                  : cudaEventRecord(e, c->stream),
+     "event");
+}
+
 void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* out,
                unsigned long long out_cap, bool timed, uint32_t acc_base = 0,
                bool record_start = true, const WireArgs* wire = nullptr) {
@@ -320,7 +329,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   }
   // ev[2] (call start) / ev[4] order the fill stream after everything queued so far
   join_base(c);
-  if (record_start) ck(cudaEventRecord(c->ev[2], c->stream), "event");
+  if (record_start) record_timing_event(c, c->ev[2]);
   if (buckets) {
     ck(cudaEventRecord(c->ev_order, c->stream), "event");
     ck(cudaStreamWaitEvent(c->fstream, c->ev_order, 0), "fill wait");
@@ -396,7 +405,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     c->timing.launches += 1;
   }
   (void)timed;
-  ck(cudaEventRecord(c->ev[3], c->stream), "event");
+  record_timing_event(c, c->ev[3]);
   c->timing.segments += nseg;
 }
 
@@ -962,6 +971,103 @@ Shard shard_of(const ws_ctx* ctx, uint32_t g, uint64_t L, uint64_t R) {
   return s;
 }
 
+// ---- CUDA-graph replay of repeated small count calls ----------------------
+// A count call's device work (a fresh base build, the accumulator reset, the
+// sieve launch, the per-segment copy) is about ten API calls, a tenth of a
+// small call such as C1 (0.2 ms).  When the same call repeats, the second one
+// is captured into a graph and every later one replays it with a single
+// cudaGraphLaunch.  Small single-pass count calls qualify, with a fresh base
+// or a resident one that already covers them: their work is then fully
+// determined by the CallKey (inputs, buffers, the resident table, and the
+// allocation generation: any reallocation invalidates the graph).  The replay restores the host-side state the captured call left
+// (resident-table bounds, counters).  Anything that fails during capture
+// falls back to running the work directly.
+constexpr uint64_t kGraphMaxSegs = 8192;
+
+bool graph_eligible(const DevCtx* d, uint64_t lo, uint64_t hi, bool fresh) {
+  if (!d->graphs || hi <= lo) return false;
+  const uint64_t B = hi >= 2 ? isqrt_u64(hi - 1) : 0;
+  // a cached base must already cover B (else the call extends or rebuilds it)
+  if (!fresh && !(d->base_valid && d->base_B >= B)) return false;
+  // no bucket windows (their fill pipeline spans streams and windows)
+  if (B >= static_cast<uint64_t>(d->bucket_min_ratio) * d->S) return false;
+  return make_job(lo, hi, d->S, 0).nseg <= kGraphMaxSegs;
+}
+
+template <class F>
+void graph_or_run(DevCtx* d, CallKey key, bool fresh, F&& enqueue) {
+  key.fresh = fresh;
+  if (!fresh) {  // the resident table the captured launches read
+    key.base_B = d->base_B;
+    key.nprimes = d->nprimes;
+    key.nprimes_dev = d->nprimes_dev;
+  }
+  key.gen = g_alloc_gen.load();
+  CallGraph& g = d->cg;
+  if (g.valid && g.key == key) {
+    ck(cudaGraphLaunch(g.exec, d->stream), "graph launch");
+    d->timing.launches += g.timing.launches;
+    d->timing.segments += g.timing.segments;
+    d->timing.h2d_bytes += g.timing.h2d_bytes;
+    d->timing.d2h_bytes += g.timing.d2h_bytes;
+    d->base_valid = g.base_valid;
+    d->base_built = g.base_built;
+    d->base_B = g.base_B;
+    d->nprimes = g.nprimes;
+    d->nprimes_dev = g.nprimes_dev;
+    d->base_pending = false;
+    return;
+  }
+  if (!(g.seen && g.key == key)) {  // first sighting: run it, remember it
+    g.seen = true;
+    g.valid = false;
+    g.key = key;
+    enqueue();
+    return;
+  }
+  const ws_timing before = d->timing;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    d->capturing = true;
+    bool ok = true;
+    try {
+      enqueue();
+    } catch (...) {
+      ok = false;
+    }
+    d->capturing = false;
+    e = cudaStreamEndCapture(d->stream, &graph);
+    if (ok && e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+    if (!ok && e == cudaSuccess) e = cudaErrorStreamCaptureInvalidated;
+    if (graph) cudaGraphDestroy(graph);
+  }
+  if (e != cudaSuccess || key.gen != g_alloc_gen.load()) {
+    // not capturable (or it allocated): run directly from now on
+    cudaGetLastError();
+    if (exec) cudaGraphExecDestroy(exec);
+    g.seen = false;
+    d->timing = before;
+    enqueue();
+    return;
+  }
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g.exec = exec;
+  g.valid = true;
+  g.timing = ws_timing{};
+  g.timing.launches = d->timing.launches - before.launches;
+  g.timing.segments = d->timing.segments - before.segments;
+  g.timing.h2d_bytes = d->timing.h2d_bytes - before.h2d_bytes;
+  g.timing.d2h_bytes = d->timing.d2h_bytes - before.d2h_bytes;
+  g.base_valid = d->base_valid;
+  g.base_built = d->base_built;
+  g.base_B = d->base_B;
+  g.nprimes = d->nprimes;
+  g.nprimes_dev = d->nprimes_dev;
+  ck(cudaGraphLaunch(exec, d->stream), "graph launch");
+}
+
 // Queues the count of [lo, hi) on one device (its accumulator d->acc[0]; the
 // per-segment counts into the device array dps when non-null).  An empty
 // range leaves a zero accumulator.
@@ -988,9 +1094,7 @@ void count_range_single(DevCtx* d, uint64_t L, uint64_t R, uint32_t flags, ws_ch
                         uint32_t* per_seg, uint64_t per_seg_cap, uint64_t* n_seg) {
   validate_range(L, R);
   const bool fresh = flags & WS_FRESH_BASE;
-  ensure_base(d, R >= 2 ? isqrt_u64(R - 1) : 0, fresh);
-  d->h_jobs.assign(1, make_job(L, R, d->S, 0));
-  const uint64_t nseg = d->h_jobs[0].nseg;
+  const uint64_t nseg = make_job(L, R, d->S, 0).nseg;
   uint32_t* dps = nullptr;
   const bool dev_out = flags & WS_OUT_DEVICE;
   if (per_seg) {
@@ -1003,10 +1107,29 @@ void count_range_single(DevCtx* d, uint64_t L, uint64_t R, uint32_t flags, ws_ch
     }
   }
   const int mode = (flags & WS_WANT_CHECKS) ? wsk::kCountChecks : wsk::kCount;
-  run_sieve(d, mode, dps, nullptr, 0, true);
-  if (per_seg && !dev_out)
-    ck(copy_async(d, per_seg, dps, std::min(nseg, per_seg_cap) * sizeof(uint32_t),
-                  cudaMemcpyDeviceToHost, d->stream), "per_seg");
+  auto enqueue = [&] {
+    ensure_base(d, R >= 2 ? isqrt_u64(R - 1) : 0, fresh);
+    d->h_jobs.assign(1, make_job(L, R, d->S, 0));
+    run_sieve(d, mode, dps, nullptr, 0, true);
+    if (per_seg && !dev_out)
+      ck(copy_async(d, per_seg, dps, std::min(nseg, per_seg_cap) * sizeof(uint32_t),
+                    cudaMemcpyDeviceToHost, d->stream), "per_seg");
+  };
+  // (a copy into pageable host memory inside a graph is slower than a direct
+  // one: host per-segment outputs take the direct path)
+  if (graph_eligible(d, L, R, fresh) && (!per_seg || dev_out)) {
+    CallKey k;
+    k.lo = L;
+    k.hi = R;
+    k.mode = mode;
+    k.dps = dps;
+    k.dst = (per_seg && !dev_out) ? per_seg : nullptr;
+    k.kind = static_cast<int>(per_seg ? std::min(nseg, per_seg_cap) : 0) * 2 + (dev_out ? 1 : 0);
+    k.S = d->S;
+    graph_or_run(d, k, fresh, enqueue);
+  } else {
+    enqueue();
+  }
   *out = to_checks(*fetch_results(d, 1));
   add_prelude(L, R, out);
   if (n_seg) *n_seg = nseg;
@@ -1029,11 +1152,30 @@ void count_range_multi(ws_ctx* ctx, uint64_t L, uint64_t R, uint32_t flags, ws_c
       d->per_seg.reserve(sh.nseg, "per_seg");
       dps = d->per_seg.ptr;
     }
-    queue_count(d, sh.lo, sh.hi, mode, flags & WS_FRESH_BASE, dps);
-    if (dps && per_seg_cap > sh.seg0) {
-      const uint64_t n = std::min(sh.nseg, per_seg_cap - sh.seg0);
-      ck(copy_async(d, per_seg + sh.seg0, dps, n * sizeof(uint32_t),
-                    dev_out ? cudaMemcpyDefault : cudaMemcpyDeviceToHost, d->stream), "per_seg");
+    auto enqueue = [&] {
+      queue_count(d, sh.lo, sh.hi, mode, flags & WS_FRESH_BASE, dps);
+      if (dps && per_seg_cap > sh.seg0) {
+        const uint64_t n = std::min(sh.nseg, per_seg_cap - sh.seg0);
+        ck(copy_async(d, per_seg + sh.seg0, dps, n * sizeof(uint32_t),
+                      dev_out ? cudaMemcpyDefault : cudaMemcpyDeviceToHost, d->stream),
+           "per_seg");
+      }
+    };
+    if (ctx->devs.size() == 1 && graph_eligible(d, sh.lo, sh.hi, flags & WS_FRESH_BASE) &&
+        (!per_seg || dev_out)) {
+      CallKey k;
+      k.lo = sh.lo;
+      k.hi = sh.hi;
+      k.mode = mode;
+      k.dps = dps;
+      k.dst = (dps && per_seg_cap > sh.seg0) ? per_seg + sh.seg0 : nullptr;
+      k.kind = static_cast<int>(dps && per_seg_cap > sh.seg0
+                                    ? std::min(sh.nseg, per_seg_cap - sh.seg0) : 0) * 2 +
+               (dev_out ? 1 : 0);
+      k.S = d->S;
+      graph_or_run(d, k, flags & WS_FRESH_BASE, enqueue);
+    } else {
+      enqueue();
     }
   });
   std::vector<const wsk::JobAcc*> send;
@@ -1325,6 +1467,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_HUGE_LOOP")) c->huge_loop = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_FILL_UNROLL")) c->w_unroll = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_STAGE_CAP")) c->stage_cap = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_GRAPHS")) c->graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_BASE_EXTEND")) c->base_extend = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
     c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));

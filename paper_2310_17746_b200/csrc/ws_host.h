@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <condition_variable>
 #include <cstdint>
@@ -45,6 +46,11 @@ inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Fail{WS_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
 }
 
+// Bumped by every (re)allocation or release of a device / pinned buffer: a
+// captured CUDA graph (CallGraph) holds raw pointers and is valid only while
+// this is unchanged.
+inline std::atomic<uint64_t> g_alloc_gen{0};
+
 template <class T>
 struct DevBuf {
   T* ptr = nullptr;
@@ -52,17 +58,22 @@ struct DevBuf {
   void reserve(size_t n, const char* what) {
     if (n <= cap) return;
     release();
+    ++g_alloc_gen;
     ck(cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T)), what);
     cap = n;
   }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) {
+      cudaFree(ptr);
+      ++g_alloc_gen;
+    }
     ptr = nullptr;
     cap = 0;
   }
   // grow to n elements keeping the first `keep` (stream-ordered copy)
   void grow(size_t n, size_t keep, cudaStream_t st, const char* what) {
     if (n <= cap) return;
+    ++g_alloc_gen;
     T* q = nullptr;
     ck(cudaMalloc(&q, n * sizeof(T)), what);
     if (keep && ptr) {
@@ -87,12 +98,16 @@ struct PinnedBuf {
   void* reserve(size_t n, const char* what) {
     if (n <= bytes) return ptr;
     release();
+    ++g_alloc_gen;
     ck(cudaMallocHost(&ptr, std::max<size_t>(n, 64)), what);
     bytes = n;
     return ptr;
   }
   void release() {
-    if (ptr) cudaFreeHost(ptr);
+    if (ptr) {
+      cudaFreeHost(ptr);
+      ++g_alloc_gen;
+    }
     ptr = nullptr;
     bytes = 0;
   }
@@ -137,6 +152,39 @@ inline uint64_t small_primes_upto(uint64_t B) {  // |{5,7,...,47} ∩ [5, B]| (t
   for (uint32_t q : sp) c += q <= B;
   return c;
 }
+
+// Everything a small count call's captured device work depends on.
+struct CallKey {
+  uint64_t lo = 0, hi = 0;
+  int mode = -1;
+  const void* dps = nullptr;  // device per-segment counts (nullable)
+  const void* dst = nullptr;  // their copy destination (nullable)
+  int kind = 0;               // its cudaMemcpyKind
+  uint32_t S = 0;
+  bool fresh = false;         // the call rebuilds the base table
+  uint64_t base_B = 0;        // else: the resident table it reads
+  uint32_t nprimes = 0;
+  const void* nprimes_dev = nullptr;
+  uint64_t gen = 0;           // g_alloc_gen at capture
+  bool operator==(const CallKey& o) const {
+    return lo == o.lo && hi == o.hi && mode == o.mode && dps == o.dps && dst == o.dst &&
+           kind == o.kind && S == o.S && fresh == o.fresh && base_B == o.base_B &&
+           nprimes == o.nprimes && nprimes_dev == o.nprimes_dev && gen == o.gen;
+  }
+};
+
+// CUDA-graph replay of a repeated small count call (ws_abi.cu, graph_or_run):
+// the second identical call is captured, later ones are one cudaGraphLaunch.
+struct CallGraph {
+  bool seen = false, valid = false;
+  CallKey key;
+  cudaGraphExec_t exec = nullptr;
+  ws_timing timing{};  // the captured call's counters (launches, segments, bytes)
+  bool base_valid = false, base_built = false;
+  uint64_t base_B = 0;
+  uint32_t nprimes = 0;
+  const uint32_t* nprimes_dev = nullptr;
+};
 
 struct DevCtx {
   int device = 0;
@@ -196,6 +244,9 @@ struct DevCtx {
   // wavefronts at C3 but no faster (204.4 ms either way; C4 +0.2 ms), so off
   uint32_t single_pred = 0;
   uint32_t mid_bitaddr = 1;            // WHEELSIEVE_MID_BITADDR
+  bool graphs = true;                  // WHEELSIEVE_GRAPHS=0: no graph replay of small calls
+  bool capturing = false;              // the stream is being captured (timing events external)
+  CallGraph cg;
 
   // scratch
   DevBuf<uint32_t> bucket[2];  // double-buffered window lists (fill w+1 || sieve w)
@@ -245,6 +296,7 @@ struct DevCtx {
 
   ~DevCtx() {
     cudaSetDevice(device);
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
     if (pool) wswire::pool_destroy(pool);
     wire.release();
     wblk.release();
