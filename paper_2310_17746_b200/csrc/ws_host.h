@@ -244,6 +244,7 @@ struct DevCtx {
   // wavefronts at C3 but no faster (204.4 ms either way; C4 +0.2 ms), so off
   uint32_t single_pred = 0;
   uint32_t mid_bitaddr = 1;            // WHEELSIEVE_MID_BITADDR
+  uint32_t miss_lane = 1;              // WHEELSIEVE_MISS_LANE
   bool graphs = true;                  // WHEELSIEVE_GRAPHS=0: no graph replay of small calls
   bool capturing = false;              // the stream is being captured (timing events external)
   CallGraph cg;

@@ -84,6 +84,7 @@ struct SieveParams {
   uint8_t* blk8;                     // kEnumWire: survivors per block, segment s at s * S / 128
   uint32_t single_pred;              // single-hit primes: predicated atomics (else OR 0 on a miss)
   uint32_t mid_bitaddr;              // mid-prime loop on shared bit addresses
+  uint32_t miss_lane;                // single-hit misses OR 0 into word `lane` (else a word from h)
   uint32_t* words1;                  // nullable (count modes): survivor flag words of
   uint32_t* words5;                  // each class, segment s at word s * S / 32
 };

@@ -373,6 +373,14 @@ __device__ __forceinline__ void mark_or(uint32_t a0, uint32_t h, uint32_t len, u
   atom_or_shared(a0 + (((h >> 5) & wmask) << 2), h < len ? 1u << (h & 31u) : 0u);
 }
 
+// ... the miss going to word `lane` (bank `lane`) instead: a miss then adds at
+// most one access to a bank a hit uses, rather than one at a random bank
+// (modelled: 3.09 vs 3.53 wavefronts per warp op at a 50% hit rate)
+__device__ __forceinline__ void mark_or_lane(uint32_t a0, uint32_t h, uint32_t len, uint32_t lane) {
+  const bool hit = h < len;
+  atom_or_shared(a0 + ((hit ? h >> 5 : lane) << 2), hit ? 1u << (h & 31u) : 0u);
+}
+
 // cross off the bit at shared-memory bit address hb
 __device__ __forceinline__ void mark_bitaddr(uint32_t hb) {
   atom_or_shared((hb >> 3) & ~3u, 1u << (hb & 31u));
@@ -529,6 +537,9 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
         // the warp's conflict degree is that of its hitting lanes only
         mark_if(a1, rel1, len);
         mark_if(a5, rel5, len);
+      } else if (P.miss_lane) {
+        mark_or_lane(a1, rel1, len, lane);
+        mark_or_lane(a5, rel5, len, lane);
       } else {
         mark_or(a1, rel1, len, P.S / 32 - 1);
         mark_or(a5, rel5, len, P.S / 32 - 1);
