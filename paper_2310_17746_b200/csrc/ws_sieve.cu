@@ -386,6 +386,34 @@ __device__ __forceinline__ void mark_bitaddr(uint32_t hb) {
   atom_or_shared((hb >> 3) & ~3u, 1u << (hb & 31u));
 }
 
+// Mid-prime hits with the multiples of 5 skipped.  Hit j of prime p in class
+// c sits at wheel index K_j = K_0 + j p and has value 6 K_j + c = p m_j; it is
+// a multiple of 5 -- a slot the stamped prime 5 has already crossed off --
+// exactly when K_j == -c (mod 5), i.e. for every fifth j from j0 on (p is
+// coprime to 5).  From hb (shared bit address of hit 0) below lim: hits
+// 0 .. j0-1, then groups of four with the fifth skipped.
+__device__ __forceinline__ void mark_skip5(uint32_t hb, uint32_t lim, uint32_t p, uint32_t j0) {
+  for (; j0 > 0 && hb < lim; --j0, hb += p) mark_bitaddr(hb);
+  hb += p;  // hit j0: a multiple of 5
+  const uint32_t p2 = 2 * p, p3 = 3 * p, p5 = 5 * p;
+  for (; hb + p3 < lim; hb += p5) {
+    mark_bitaddr(hb);
+    mark_bitaddr(hb + p);
+    mark_bitaddr(hb + p2);
+    mark_bitaddr(hb + p3);
+  }
+  for (uint32_t k = 0; k < 3 && hb < lim; ++k, hb += p) mark_bitaddr(hb);
+}
+
+// j0 of class c (cmod = (-c) mod 5: 4 for 6k+1, 0 for 6k+5) for a first hit at
+// wheel index K0 (K0 mod 5 = k05) of a prime with 1/p mod 5 = inv5
+__device__ __forceinline__ uint32_t skip5_phase(uint32_t k05, uint32_t cmod, uint32_t inv5) {
+  const uint32_t d = cmod + 5u - k05;  // 1..9: (cmod - K0) mod 5 after one reduction
+  const uint32_t dm = d >= 5u ? d - 5u : d;
+  const uint32_t x = dm * inv5;  // <= 16
+  return x - 5u * ((x * 13u) >> 6);  // x mod 5 for x <= 16
+}
+
 // cross off bit h of the bitmap at shared address a0
 __device__ __forceinline__ void mark(uint32_t a0, uint32_t h) {
   atom_or_shared(a0 + ((h >> 5) << 2), 1u << (h & 31u));
@@ -420,6 +448,32 @@ __device__ __forceinline__ void mark_strided(uint32_t a0, uint32_t h0, uint32_t 
   for (; a < alim; a += step) atom_or_shared(a, bit);
 }
 
+// mark_strided with the multiples of 5 skipped (see mark_skip5): hit
+// j = lane + 32 i is on a multiple of 5 iff j == j0 (mod 5), i.e. for the
+// lane's iterations i == phi (mod 5), phi = 3 (j0 - lane) mod 5.  The lane
+// marks iterations 0 .. phi-1, skips phi, then runs groups of four with the
+// fifth skipped; the groups keep the strided loop's one-bit, one-add shape.
+__device__ __forceinline__ void mark_strided_skip5(uint32_t a0, uint32_t h0, uint32_t p,
+                                                   uint32_t len, uint32_t lane, uint32_t j0) {
+  const uint32_t h = h0 + lane * p;
+  if (h >= len) return;
+  const uint32_t bit = 1u << (h & 31u);
+  const uint32_t alim = a0 + (((len - (h & 31u) + 31u) >> 5) << 2);
+  const uint32_t step = 4 * p;
+  uint32_t a = a0 + ((h >> 5) << 2);
+  const uint32_t x = 3u * j0 + 2u * lane;  // 3 (j0 - lane) mod 5, as 3 j0 + 2 lane < 80
+  uint32_t phi = x - 5u * ((x * 205u) >> 10);
+  for (; phi > 0 && a < alim; --phi, a += step) atom_or_shared(a, bit);
+  a += step;  // the iteration on a multiple of 5
+  for (; a + 3 * step < alim; a += 5 * step) {
+    atom_or_shared(a, bit);
+    atom_or_shared(a + step, bit);
+    atom_or_shared(a + 2 * step, bit);
+    atom_or_shared(a + 3 * step, bit);
+  }
+  for (uint32_t k = 0; k < 3 && a < alim; ++k, a += step) atom_or_shared(a, bit);
+}
+
 // Phase 2: medium and large primes.
 __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo& si,
                                              uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr,
@@ -430,6 +484,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   const uint32_t a1 = smem_addr(bm1), a5 = smem_addr(bm5);
   const uint32_t t_lo = si.t_lo, t_hi = si.t_hi;
   const ModCtx mc = mod_ctx(ks);
+  const uint32_t ks5 = static_cast<uint32_t>(ks % 5u);  // for the multiple-of-5 skips
   const uint32_t n_wc = min(P.n_wc, nprimes), n_mid = min(P.n_mid, nprimes);
   const uint32_t n_S = min(P.n_S, n_mid);
   // warp-cooperative primes, handed out dynamically (largest work first); the
@@ -453,8 +508,14 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     claim(wi, wp, wip);
     uint32_t rel1, rel5;
     if (!prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
-    mark_strided(a1, rel1, p, len, lane);
-    mark_strided(a5, rel5, p, len, lane);
+    if (p < P.coop_skip5_max) {  // warp-uniform
+      const uint32_t inv5 = (0x42310u >> (4u * (p % 5u))) & 7u;
+      mark_strided_skip5(a1, rel1, p, len, lane, skip5_phase((ks5 + rel1) % 5u, 4u, inv5));
+      mark_strided_skip5(a5, rel5, p, len, lane, skip5_phase((ks5 + rel5) % 5u, 0u, inv5));
+    } else {
+      mark_strided(a1, rel1, p, len, lane);
+      mark_strided(a5, rel5, p, len, lane);
+    }
   }
   // large primes come from the window's bucket list unless it overflowed
   const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;
@@ -481,7 +542,9 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     // bit addresses fit 32 bits while the bitmaps sit below 2^28 in the
     // shared window (always, for unclustered launches)
     const bool bitaddr = P.mid_bitaddr && a1 < (1u << 28) && a5 < (1u << 28);
-    const uint32_t b1 = a1 << 3;
+    const uint32_t b1 = a1 << 3, b5 = a5 << 3;
+    // primes below skip5_max: class loops that skip the multiples of 5
+    const uint32_t skip_max = bitaddr ? P.skip5_max : 0u;
     uint32_t base = n_wc + 32 * warp;
     uint32_t pn;
     double ipn;
@@ -493,6 +556,12 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       if (__shfl_sync(kFull, p, 0) > t_hi) break;  // primes ascend: the rest is inactive
       uint32_t rel1, rel5;
       if (!prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) continue;
+      if (p < skip_max) {
+        const uint32_t inv5 = (0x42310u >> (4u * (p % 5u))) & 7u;  // 1/p mod 5
+        mark_skip5(b1 + rel1, b1 + len, p, skip5_phase((ks5 + rel1) % 5u, 4u, inv5));
+        mark_skip5(b5 + rel5, b5 + len, p, skip5_phase((ks5 + rel5) % 5u, 0u, inv5));
+        continue;
+      }
       const int32_t d = static_cast<int32_t>(rel5 - rel1);
       const uint32_t dpos = d > 0 ? static_cast<uint32_t>(d) : 0u;
       uint32_t h = rel1;
