@@ -240,7 +240,6 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.mid_bitaddr = c->mid_bitaddr;
   p.miss_lane = c->miss_lane;
   p.skip5_max = c->skip5_max;
-  p.coop_skip5_max = c->coop_skip5_max;
   p.words1 = c->words_out[0];
   p.words5 = c->words_out[1];
   if (wire) {
@@ -1473,7 +1472,6 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_GRAPHS")) c->graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_MISS_LANE")) c->miss_lane = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_SKIP5")) c->skip5_max = std::strtoul(e, nullptr, 10);
-  if (const char* e = std::getenv("WHEELSIEVE_COOP_SKIP5")) c->coop_skip5_max = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BASE_EXTEND")) c->base_extend = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
     c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));

@@ -246,7 +246,6 @@ struct DevCtx {
   uint32_t mid_bitaddr = 1;            // WHEELSIEVE_MID_BITADDR
   uint32_t miss_lane = 1;              // WHEELSIEVE_MISS_LANE
   uint32_t skip5_max = 16384;          // WHEELSIEVE_SKIP5: mid primes below it skip multiples of 5
-  uint32_t coop_skip5_max = 512;       // WHEELSIEVE_COOP_SKIP5: warp-cooperative primes below it too
   bool graphs = true;                  // WHEELSIEVE_GRAPHS=0: no graph replay of small calls
   bool capturing = false;              // the stream is being captured (timing events external)
   CallGraph cg;

@@ -448,32 +448,6 @@ __device__ __forceinline__ void mark_strided(uint32_t a0, uint32_t h0, uint32_t 
   for (; a < alim; a += step) atom_or_shared(a, bit);
 }
 
-// mark_strided with the multiples of 5 skipped (see mark_skip5): hit
-// j = lane + 32 i is on a multiple of 5 iff j == j0 (mod 5), i.e. for the
-// lane's iterations i == phi (mod 5), phi = 3 (j0 - lane) mod 5.  The lane
-// marks iterations 0 .. phi-1, skips phi, then runs groups of four with the
-// fifth skipped; the groups keep the strided loop's one-bit, one-add shape.
-__device__ __forceinline__ void mark_strided_skip5(uint32_t a0, uint32_t h0, uint32_t p,
-                                                   uint32_t len, uint32_t lane, uint32_t j0) {
-  const uint32_t h = h0 + lane * p;
-  if (h >= len) return;
-  const uint32_t bit = 1u << (h & 31u);
-  const uint32_t alim = a0 + (((len - (h & 31u) + 31u) >> 5) << 2);
-  const uint32_t step = 4 * p;
-  uint32_t a = a0 + ((h >> 5) << 2);
-  const uint32_t x = 3u * j0 + 2u * lane;  // 3 (j0 - lane) mod 5, as 3 j0 + 2 lane < 80
-  uint32_t phi = x - 5u * ((x * 205u) >> 10);
-  for (; phi > 0 && a < alim; --phi, a += step) atom_or_shared(a, bit);
-  a += step;  // the iteration on a multiple of 5
-  for (; a + 3 * step < alim; a += 5 * step) {
-    atom_or_shared(a, bit);
-    atom_or_shared(a + step, bit);
-    atom_or_shared(a + 2 * step, bit);
-    atom_or_shared(a + 3 * step, bit);
-  }
-  for (uint32_t k = 0; k < 3 && a < alim; ++k, a += step) atom_or_shared(a, bit);
-}
-
 // Phase 2: medium and large primes.
 __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo& si,
                                              uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr,
@@ -508,14 +482,8 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     claim(wi, wp, wip);
     uint32_t rel1, rel5;
     if (!prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
-    if (p < P.coop_skip5_max) {  // warp-uniform
-      const uint32_t inv5 = (0x42310u >> (4u * (p % 5u))) & 7u;
-      mark_strided_skip5(a1, rel1, p, len, lane, skip5_phase((ks5 + rel1) % 5u, 4u, inv5));
-      mark_strided_skip5(a5, rel5, p, len, lane, skip5_phase((ks5 + rel5) % 5u, 0u, inv5));
-    } else {
-      mark_strided(a1, rel1, p, len, lane);
-      mark_strided(a5, rel5, p, len, lane);
-    }
+    mark_strided(a1, rel1, p, len, lane);
+    mark_strided(a5, rel5, p, len, lane);
   }
   // large primes come from the window's bucket list unless it overflowed
   const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;

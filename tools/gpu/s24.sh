@@ -1,0 +1,6 @@
+for i in 1 2 3; do
+for c in c3s c2; do
+echo "== $c current"; python tools/prof_run.py $c 3 | tail -1
+echo "== $c nocoop-code"; (cd scratch/nocoop && python tools/prof_run.py $c 3 | tail -1)
+echo "== $c current SKIP5=0"; WHEELSIEVE_SKIP5=0 python tools/prof_run.py $c 3 | tail -1
+done; done
