@@ -254,6 +254,20 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   // offset check in the kernel is cheaper than fill + apply + windowing.
   const bool buckets = c->nprimes > p.n_mid && c->base_B > c->bucket_pmin &&
                        c->base_B >= static_cast<uint64_t>(c->bucket_min_ratio) * c->S;
+  // wide units (sieve_wide_kernel): single-job count launches without bucket
+  // lists, long enough to keep every SM's lone CTA busy for many units
+  if (c->wide > 1 && mode <= wsk::kCountChecks && nj == 1 && !buckets &&
+      c->S == (1u << 18) && c->words_out[0] == nullptr &&
+      nseg >= static_cast<uint64_t>(c->wide_min_units) * c->wide * c->sms) {
+    p.wide = std::min<uint32_t>(c->wide, wsk::kWideMax);
+    p.n_S = std::min<uint32_t>(
+        std::max(table_primes_below(c, static_cast<uint64_t>(p.wide) * c->S), p.n_wc), c->nprimes);
+    p.n_mid = c->nprimes;
+    p.miss_lane = 1;
+    p.wc_trans = c->wc_trans;
+    if (c->wide_n_wc) p.n_wc = std::min<uint32_t>(c->wide_n_wc, p.n_S);
+    max_grid = c->sms;
+  }
   uint64_t W = nseg;
   uint32_t cap = 0;
   if (buckets) {
@@ -401,7 +415,8 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     p.s_begin = ws;
     p.s_count = we - ws;
     p.ticket = c->ticket.ptr + 2 * w;
-    const int grid = static_cast<int>(std::min<uint64_t>(we - ws, max_grid));
+    const uint64_t units = p.wide > 1 ? (we - ws + p.wide - 1) / p.wide : we - ws;
+    const int grid = static_cast<int>(std::min<uint64_t>(units, max_grid));
     ck(wsk::launch_sieve(mode, p, grid, c->stream), "sieve launch");
     if (buckets) ck(cudaEventRecord(c->sieve_done[b], c->stream), "event");
     c->timing.launches += 1;
@@ -1472,6 +1487,12 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_GRAPHS")) c->graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_MISS_LANE")) c->miss_lane = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_SKIP5")) c->skip5_max = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_WIDE")) c->wide = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_WC_TRANS")) c->wc_trans = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_WIDE_WC_LIMIT"))
+    c->wide_n_wc = table_primes_below(c, std::strtoul(e, nullptr, 10));
+  if (const char* e = std::getenv("WHEELSIEVE_WIDE_MIN_UNITS"))
+    c->wide_min_units = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_BASE_EXTEND")) c->base_extend = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_WIRE_PIECE"))
     c->wire_piece = std::max<uint64_t>(1024, std::strtoull(e, nullptr, 10));

@@ -36,6 +36,7 @@ struct JobAcc {
 // (ws_wire.cpp).
 enum Mode : int { kCount = 0, kCountChecks = 1, kEnumerate = 2, kEnumWire = 3 };
 constexpr int kNumModes = 4;
+constexpr uint32_t kWideMax = 3;  // segments per unit of the wide count kernel (192 KiB)
 constexpr uint32_t kWireBlockSlots = 128;
 
 // Large-prime buckets: per window of segments, the hits of every prime
@@ -86,6 +87,8 @@ struct SieveParams {
   uint32_t mid_bitaddr;              // mid-prime loop on shared bit addresses
   uint32_t miss_lane;                // single-hit misses OR 0 into word `lane` (else a word from h)
   uint32_t skip5_max;                // mid primes below it skip their hits on multiples of 5
+  uint32_t wide;                     // > 1: sieve_wide_kernel, this many segments per unit
+  uint32_t wc_trans;                 // wide: transposed (conflict-free) warp-cooperative marking
   uint32_t* words1;                  // nullable (count modes): survivor flag words of
   uint32_t* words5;                  // each class, segment s at word s * S / 32
 };

@@ -460,7 +460,43 @@ __device__ __forceinline__ void mark_strided(uint32_t a0, uint32_t h0, uint32_t 
   for (; a < alim; a += step) atom_or_shared(a, bit);
 }
 
-// Phase 2: medium and large primes.
+// Transposed warp-cooperative marking of one class: hits are taken in
+// superblocks of 1024, lane l owning hits 32 l .. 32 l + 31 of the superblock
+// and warp op i marking hit 32 l + i in every lane.  The lanes of an op are
+// then exactly 32 p bits = p words apart -- p is odd, so the 32 words fall in
+// 32 different banks (one wavefront per op, where consecutive hits per op
+// average 2.5) -- and they share the bit within the word.  A last partial
+// superblock of at least kTransMin hits runs the same way with the lanes
+// past the end predicated off; shorter tails use the strided loop.
+constexpr uint32_t kTransMin = 384;
+__device__ __forceinline__ void mark_transposed(uint32_t a0, uint32_t rel, uint32_t p,
+                                                uint32_t len, uint32_t lane) {
+  const uint32_t lane_off = a0 + 4u * lane * p;
+  uint32_t pos = rel;
+  while (pos + 1023u * p < len) {
+#pragma unroll 8
+    for (uint32_t i = 0; i < 32; ++i) {
+      atom_or_shared(lane_off + ((pos >> 5) << 2), 1u << (pos & 31u));
+      pos += p;
+    }
+    pos += 992u * p;
+  }
+  if (pos + (kTransMin - 1u) * p < len) {
+    // the lane's hits start at pos + 32 l p: in range while pos < len - 32 l p
+    const uint32_t lp = 32u * lane * p;
+    const uint32_t lim = len > lp ? len - lp : 0u;
+#pragma unroll 8
+    for (uint32_t i = 0; i < 32; ++i) {
+      if (pos < lim) atom_or_shared(lane_off + ((pos >> 5) << 2), 1u << (pos & 31u));
+      pos += p;
+    }
+  } else if (pos < len) {
+    mark_strided(a0, pos, p, len, lane);
+  }
+}
+
+// Phase 2: medium and large primes (NT threads per block).
+template <int NT, bool WC_LAST = false, bool WCT = false>
 __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo& si,
                                              uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr,
                                              uint32_t nprimes) {
@@ -485,18 +521,29 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       ip = __ldg(P.prime_inv + i);
     }
   };
-  uint32_t wi, wp = 0;
-  double wip = 0.0;
-  claim(wi, wp, wip);
-  while (wi < n_wc) {
-    const uint32_t i = wi, p = wp;
-    const double ip = wip;
+  auto wc_phase = [&]() {
+    uint32_t wi, wp = 0;
+    double wip = 0.0;
     claim(wi, wp, wip);
-    uint32_t rel1, rel5;
-    if (!prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
-    mark_strided(a1, rel1, p, len, lane);
-    mark_strided(a5, rel5, p, len, lane);
-  }
+    while (wi < n_wc) {
+      const uint32_t i = wi, p = wp;
+      const double ip = wip;
+      claim(wi, wp, wip);
+      uint32_t rel1, rel5;
+      if (!prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
+      if (WCT) {
+        mark_transposed(a1, rel1, p, len, lane);
+        mark_transposed(a5, rel5, p, len, lane);
+      } else {
+        mark_strided(a1, rel1, p, len, lane);
+        mark_strided(a5, rel5, p, len, lane);
+      }
+    }
+  };
+  // WC_LAST (a lone CTA per SM): the dynamically claimed primes come after the
+  // static chunks, smallest tasks last, so they even out the warps' finish
+  // times before the closing barrier
+  if (!WC_LAST) wc_phase();
   // large primes come from the window's bucket list unless it overflowed
   const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;
   const uint32_t lp_end = use_bucket ? n_mid : nprimes;
@@ -506,7 +553,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   // loads are independent of the segment, and issuing them together and early
   // turns two dependent global round trips per (prime, segment) into none on
   // the critical path.
-  constexpr uint32_t kStride = 32 * kWarps;
+  constexpr uint32_t kStride = NT;  // 32 primes per warp and round
   auto load = [&](uint32_t idx, uint32_t end, uint32_t& p, double& ip) {
     if (idx < end) {
       p = __ldg(P.prime_p + idx);
@@ -609,8 +656,8 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
     const uint4* list4 = reinterpret_cast<const uint4*>(list);
     const uint32_t n4 = n >> 2;
     uint32_t i = threadIdx.x;
-    for (; i + kThreads < n4; i += 2 * kThreads) {
-      const uint4 x = __ldcs(list4 + i), y = __ldcs(list4 + i + kThreads);
+    for (; i + NT < n4; i += 2 * NT) {
+      const uint4 x = __ldcs(list4 + i), y = __ldcs(list4 + i + NT);
       mark(a1, x.x);
       mark(a1, x.y);
       mark(a1, x.z);
@@ -627,8 +674,9 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       mark(a1, x.z);
       mark(a1, x.w);
     }
-    for (uint32_t j = 4 * n4 + threadIdx.x; j < n; j += kThreads) mark(a1, __ldcs(list + j));
+    for (uint32_t j = 4 * n4 + threadIdx.x; j < n; j += NT) mark(a1, __ldcs(list + j));
   }
+  if (WC_LAST) wc_phase();
 }
 
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
@@ -784,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
     if (si.s == ~0ull) break;
     init_words(si, tab, bm1, bm5);
     __syncthreads();
-    sieve_primes(P, si, bm1, bm5, &wc_ctr, nprimes);
+    sieve_primes<kThreads>(P, si, bm1, bm5, &wc_ctr, nprimes);
     __syncthreads();
     if (P.bucket != nullptr && threadIdx.x == 0) P.bcount[si.s - P.s_begin] = 0;
 
@@ -1016,6 +1064,227 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Wide count kernel: one 1024-thread CTA per SM owns P.wide consecutive
+// segments (2 or 3: 128 or 192 KiB of flags) as ONE sieving unit, so every
+// per-(prime, unit) cost -- offsets, loop set-up, the single-hit checks, the
+// p and 1/p loads -- is paid once per P.wide segments.  A lone CTA per SM has
+// no sibling to cover its barriers, so the unit loop is cut to two barriers:
+//   A: flags stamped          -> mark (sieve_primes)
+//   B: marks complete         -> count unit u and stamp unit u+1 in ONE pass
+//                                (each thread reads word w of u, then overwrites
+//                                it with u+1's pattern: no barrier in between)
+// The next unit's ticket and geometry are fetched by thread 0 during the
+// marking, and the unit's totals gather in shared accumulators that thread 0
+// flushes after barrier A.  Per-segment counts stay per S-slot segment.
+// Single-job count launches without bucket lists only (host-side gate).
+constexpr int kWideThreads = 1024;
+
+__device__ void fetch_unit(const SieveParams& P, SegInfo& si) {
+  const uint64_t nunits = (P.s_count + P.wide - 1) / P.wide;
+  const unsigned long long t = atomicAdd(P.ticket, 1ull);
+  if (t >= nunits) {
+    si.s = ~0ull;
+    if (atomicAdd(P.ticket + 1, 1ull) == gridDim.x - 1) {  // see fetch_segment
+      P.ticket[0] = 0;
+      P.ticket[1] = 0;
+    }
+    return;
+  }
+  const Job& J = P.job0;
+  const uint64_t local = t * P.wide;  // first segment of the unit (s_begin == seg_begin)
+  si.s = P.s_begin + local;
+  si.job = 0;
+  si.ks = J.K0 + local * P.S;
+  const uint64_t rem = J.nslots - local * P.S;
+  const uint64_t cap = static_cast<uint64_t>(P.wide) * P.S;
+  si.len = rem < cap ? static_cast<uint32_t>(rem) : static_cast<uint32_t>(cap);
+  si.lo1 = first_valid(si.ks, 1, J.L);
+  if (si.ks == 0 && si.lo1 < 1) si.lo1 = 1;
+  si.lo5 = first_valid(si.ks, 5, J.L);
+  si.hi1 = end_valid(si.ks, 1, J.R, si.len);
+  si.hi5 = end_valid(si.ks, 5, J.R, si.len);
+  si.nwords = ((si.len + 1023u) / 1024u) * 32u;
+  si.t_lo = isqrt64(6 * si.ks);
+  si.t_hi = isqrt64(6 * (si.ks + si.len));
+}
+
+struct WideAcc {
+  unsigned long long lg, sum, xr;
+  uint32_t cnt[4];
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kWideThreads, 1) sieve_wide_kernel(const SieveParams P) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const uint32_t wps = P.S / 32;  // words per class per segment (a multiple of kWideThreads)
+  uint32_t* bm1 = smem;
+  uint32_t* bm5 = smem + P.wide * wps;
+  const uint2* tab1 = reinterpret_cast<const uint2*>(P.small_tab);
+  const uint2* tab5 = tab1 + kTabPerClass;
+  __shared__ SegInfo sis[2];
+  __shared__ WideAcc acc;
+  __shared__ uint32_t wc_ctr;
+  const uint32_t lane = threadIdx.x & 31u;
+  constexpr uint32_t kStride = 32u * kWideThreads;
+
+  const uint32_t nprimes = P.nprimes_dev ? min(P.nprimes, *P.nprimes_dev) : P.nprimes;
+  if (P.tabn_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *P.tabn_out = nprimes;
+  if (threadIdx.x == 0) {
+    fetch_unit(P, sis[0]);
+    wc_ctr = 0;
+    acc.lg = acc.sum = acc.xr = 0;
+    acc.cnt[0] = acc.cnt[1] = acc.cnt[2] = acc.cnt[3] = 0;
+  }
+  __syncthreads();
+  if (sis[0].s == ~0ull) return;
+
+  // counts unit `o` (if any) and stamps unit `n` (if any) in one pass
+  auto count_and_stamp = [&](const SegInfo* o, const SegInfo* n) {
+    const uint32_t o_words = o ? o->nwords : 0u, n_words = n ? n->nwords : 0u;
+    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+    bool edge = false;
+    if (n) {
+      const uint64_t k = n->ks + 32u * threadIdx.x;
+      a0 = static_cast<uint32_t>(k % 5005u);
+      a1 = static_cast<uint32_t>(k % 7429u);
+      a2 = static_cast<uint32_t>(k % 899u);
+      a3 = static_cast<uint32_t>(k % 1517u);
+      a4 = static_cast<uint32_t>(k % 2021u);
+      const uint32_t full = 32u * n_words;
+      edge = n->lo1 != 0 || n->lo5 != 0 || n->hi1 != full || n->hi5 != full || n->ks < 8;
+    }
+    const unsigned long long vbase = o ? 6 * o->ks : 0ull;
+    unsigned long long sum = 0, xr = 0;
+    uint32_t top_w = 0, top1 = 0, top5 = 0;  // the thread's last word with a survivor
+    const uint32_t end_words = max(o_words, n_words);
+    for (uint32_t part = 0; part * wps < end_words; ++part) {
+      uint32_t cnt = 0;
+      const uint32_t w_end = min((part + 1) * wps, end_words);
+      for (uint32_t w = part * wps + threadIdx.x; w < w_end; w += kWideThreads) {
+        if (w < o_words) {
+          const uint32_t m1 = ~bm1[w], m5 = ~bm5[w];
+          cnt += __popc(m1) + __popc(m5);
+          if (m1 | m5) {
+            top_w = w;
+            top1 = m1;
+            top5 = m5;
+            if (MODE == kCountChecks) {
+              const unsigned long long wb = vbase + 192ull * w;
+              for (uint32_t x = m1; x; x &= x - 1) {
+                const unsigned long long v = wb + 6ull * (__ffs(x) - 1) + 1;
+                sum += v;
+                xr ^= v;
+              }
+              for (uint32_t x = m5; x; x &= x - 1) {
+                const unsigned long long v = wb + 6ull * (__ffs(x) - 1) + 5;
+                sum += v;
+                xr ^= v;
+              }
+            }
+          }
+        }
+        if (w < n_words) {  // see init_words
+          uint32_t m1 = tab_read(tab1, a0) & tab_read(tab1 + tab_off(1), a1) &
+                        tab_read(tab1 + tab_off(2), a2) & tab_read(tab1 + tab_off(3), a3) &
+                        tab_read(tab1 + tab_off(4), a4);
+          uint32_t m5 = tab_read(tab5, a0) & tab_read(tab5 + tab_off(1), a1) &
+                        tab_read(tab5 + tab_off(2), a2) & tab_read(tab5 + tab_off(3), a3) &
+                        tab_read(tab5 + tab_off(4), a4);
+          a0 = phase_step(a0, kStride % 5005u, 5005u);
+          a1 = phase_step(a1, kStride % 7429u, 7429u);
+          a2 = phase_step(a2, kStride % 899u, 899u);
+          a3 = phase_step(a3, kStride % 1517u, 1517u);
+          a4 = phase_step(a4, kStride % 2021u, 2021u);
+          if (edge) {
+            if (w == 0 && n->ks < 8) {
+              m1 |= 0xEEu >> n->ks;
+              m5 |= 0xDFu >> n->ks;
+            }
+            const int64_t base = 32 * static_cast<int64_t>(w);
+            m1 &= range_mask(static_cast<int64_t>(n->lo1) - base,
+                             static_cast<int64_t>(n->hi1) - base);
+            m5 &= range_mask(static_cast<int64_t>(n->lo5) - base,
+                             static_cast<int64_t>(n->hi5) - base);
+          }
+          bm1[w] = ~m1;
+          bm5[w] = ~m5;
+        }
+      }
+      if (o) {
+        cnt = __reduce_add_sync(kFull, cnt);
+        if (lane == 0 && cnt) atomicAdd(&acc.cnt[part], cnt);
+      }
+    }
+    if (o) {
+      unsigned long long lg = 0;
+      if (top1 | top5) {
+        const unsigned long long wb = vbase + 192ull * top_w;
+        const unsigned long long v1 = top1 ? wb + 6ull * (31 - __clz(top1)) + 1 : 0;
+        const unsigned long long v5 = top5 ? wb + 6ull * (31 - __clz(top5)) + 5 : 0;
+        lg = v1 > v5 ? v1 : v5;
+      }
+      lg = warp_max64(lg);
+      if (MODE == kCountChecks) {
+        sum = warp_sum64(sum);
+        xr = warp_xor64(xr);
+      }
+      if (lane == 0) {
+        if (lg) atomicMax(&acc.lg, lg);
+        if (MODE == kCountChecks) {
+          atomicAdd(&acc.sum, sum);
+          atomicXor(&acc.xr, xr);
+        }
+      }
+    }
+  };
+  // thread 0: the finished unit's totals to the job accumulators
+  auto flush = [&](const SegInfo& o) {
+    JobAcc& A = P.acc[0];
+    unsigned long long total = 0;
+    for (uint32_t part = 0; part < P.wide; ++part) {
+      if (part * P.S < o.len) {
+        if (P.per_seg) P.per_seg[o.s + part] = acc.cnt[part];
+        total += acc.cnt[part];
+      }
+      acc.cnt[part] = 0;
+    }
+    if (total) {
+      atomicAdd(&A.count, total);
+      atomicMax(&A.largest, acc.lg);
+      if (MODE == kCountChecks) {
+        atomicAdd(&A.sum, acc.sum);
+        atomicXor(&A.xr, acc.xr);
+      }
+    }
+    acc.lg = acc.sum = acc.xr = 0;
+  };
+
+  count_and_stamp(nullptr, &sis[0]);
+  uint32_t cur = 0;
+  bool pending = false;  // thread 0: unit cur^1 is counted but not flushed
+  for (;;) {
+    __syncthreads();  // A
+    if (threadIdx.x == 0) {
+      if (pending) flush(sis[cur ^ 1]);
+      fetch_unit(P, sis[cur ^ 1]);
+    }
+    if (P.wc_trans)
+      sieve_primes<kWideThreads, true, true>(P, sis[cur], bm1, bm5, &wc_ctr, nprimes);
+    else
+      sieve_primes<kWideThreads, true, false>(P, sis[cur], bm1, bm5, &wc_ctr, nprimes);
+    __syncthreads();  // B
+    const bool more = sis[cur ^ 1].s != ~0ull;
+    if (threadIdx.x == 0) wc_ctr = 0;
+    count_and_stamp(&sis[cur], more ? &sis[cur ^ 1] : nullptr);
+    pending = true;
+    cur ^= 1;
+    if (!more) break;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) flush(sis[cur ^ 1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1652,6 +1921,12 @@ cudaError_t sieve_configure(int* blocks_per_sm) {
     if (e != cudaSuccess) return e;
     blocks_per_sm[m] = b < 1 ? 1 : b;
   }
+  for (const void* f : {reinterpret_cast<const void*>(sieve_wide_kernel<kCount>),
+                        reinterpret_cast<const void*>(sieve_wide_kernel<kCountChecks>)}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kWideMax * sieve_smem_bytes(1u << 18, kCount)));
+    if (e != cudaSuccess) return e;
+  }
   // the fill kernels' histograms + per-prime state can pass the 48 KB default
   // (runs up to 4096 segments with WHEELSIEVE_FILL_PIECE)
   for (const void* f : {reinterpret_cast<const void*>(bucket_fill_kernel),
@@ -1666,6 +1941,14 @@ cudaError_t sieve_configure(int* blocks_per_sm) {
 }
 
 cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st) {
+  if (p.wide > 1) {  // count modes only (host-side gate)
+    const size_t wsmem = static_cast<size_t>(p.wide) * sieve_smem_bytes(p.S, kCount);
+    if (mode == kCount)
+      sieve_wide_kernel<kCount><<<grid, kWideThreads, wsmem, st>>>(p);
+    else
+      sieve_wide_kernel<kCountChecks><<<grid, kWideThreads, wsmem, st>>>(p);
+    return cudaGetLastError();
+  }
   const size_t smem = sieve_smem_bytes(p.S, mode);
   switch (mode) {
     case kCount: sieve_kernel<kCount><<<grid, kThreads, smem, st>>>(p); break;

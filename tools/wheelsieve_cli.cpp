@@ -16,6 +16,7 @@
 #include <atomic>
 #include <charconv>
 #include <csignal>
+#include <ctime>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -36,11 +37,19 @@ using namespace wheelsieve;
 namespace {
 
 std::atomic<bool> g_stop{false};
-std::atomic<int> g_sigints{0};
+std::atomic<long long> g_first_sigint_ms{0};
 
+// A second ^C aborts at once -- but only one that comes a while after the
+// first: `timeout -s INT` signals the child and then its whole process group,
+// so one interruption can arrive as two back-to-back SIGINTs.
 extern "C" void on_sigint(int) {
   g_stop.store(true);
-  if (g_sigints.fetch_add(1) >= 1) std::_Exit(130);  // a second ^C aborts at once
+  timespec ts{};
+  clock_gettime(CLOCK_MONOTONIC, &ts);  // async-signal-safe
+  const long long now = ts.tv_sec * 1000LL + ts.tv_nsec / 1000000 + 1;
+  long long first = 0;
+  if (g_first_sigint_ms.compare_exchange_strong(first, now)) return;
+  if (now - first > 500) std::_Exit(130);
 }
 
 struct Usage {
