@@ -264,7 +264,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
         std::max(table_primes_below(c, static_cast<uint64_t>(p.wide) * c->S), p.n_wc), c->nprimes);
     p.n_mid = c->nprimes;
     p.miss_lane = 1;
-    p.wc_trans = c->wc_trans;
+    p.skip5_max = c->wide_skip5;
     if (c->wide_n_wc) p.n_wc = std::min<uint32_t>(c->wide_n_wc, p.n_S);
     max_grid = c->sms;
   }
@@ -1488,7 +1488,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_MISS_LANE")) c->miss_lane = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_SKIP5")) c->skip5_max = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE")) c->wide = std::strtoul(e, nullptr, 10);
-  if (const char* e = std::getenv("WHEELSIEVE_WC_TRANS")) c->wc_trans = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_WIDE_SKIP5")) c->wide_skip5 = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_WC_LIMIT"))
     c->wide_n_wc = table_primes_below(c, std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_MIN_UNITS"))

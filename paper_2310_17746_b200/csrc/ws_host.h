@@ -195,7 +195,7 @@ struct DevCtx {
   int sms = 148;
   int bps[wsk::kNumModes] = {2, 2, 2, 2};  // resident blocks per SM per mode
   uint32_t wide = 3;            // > 1: long count launches sieve this many segments per unit (WHEELSIEVE_WIDE)
-  uint32_t wc_trans = 1;        // wide units: transposed warp-cooperative marking (WHEELSIEVE_WC_TRANS)
+  uint32_t wide_skip5 = 49152;  // wide units: skip5_max (3x the hits per visit; WHEELSIEVE_WIDE_SKIP5)
   uint32_t wide_n_wc = 0;       // wide units: warp-cooperative primes (0: the context's n_wc)
   uint32_t wide_min_units = 8;  // ... when every SM gets at least this many units
   std::string err;

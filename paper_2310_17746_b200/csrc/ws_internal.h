@@ -88,7 +88,6 @@ struct SieveParams {
   uint32_t miss_lane;                // single-hit misses OR 0 into word `lane` (else a word from h)
   uint32_t skip5_max;                // mid primes below it skip their hits on multiples of 5
   uint32_t wide;                     // > 1: sieve_wide_kernel, this many segments per unit
-  uint32_t wc_trans;                 // wide: transposed (conflict-free) warp-cooperative marking
   uint32_t* words1;                  // nullable (count modes): survivor flag words of
   uint32_t* words5;                  // each class, segment s at word s * S / 32
 };

@@ -113,6 +113,13 @@ __device__ __forceinline__ void atom_or_shared(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// 1 << (pos & 31) as one BMSK (no constant register, no separate mask of pos)
+__device__ __forceinline__ uint32_t bit_of(uint32_t pos) {
+  uint32_t m;
+  asm("bmsk.wrap.b32 %0, %1, 1;" : "=r"(m) : "r"(pos));
+  return m;
+}
+
 // bits [a, b) of a 32-bit word, a and b clamped to [0, 32]
 __device__ __forceinline__ uint32_t range_mask(int64_t a, int64_t b) {
   a = a < 0 ? 0 : (a > 32 ? 32 : a);
@@ -390,12 +397,12 @@ __device__ __forceinline__ void mark_or(uint32_t a0, uint32_t h, uint32_t len, u
 // (modelled: 3.09 vs 3.53 wavefronts per warp op at a 50% hit rate)
 __device__ __forceinline__ void mark_or_lane(uint32_t a0, uint32_t h, uint32_t len, uint32_t lane) {
   const bool hit = h < len;
-  atom_or_shared(a0 + ((hit ? h >> 5 : lane) << 2), hit ? 1u << (h & 31u) : 0u);
+  atom_or_shared(a0 + ((hit ? h >> 5 : lane) << 2), hit ? bit_of(h) : 0u);
 }
 
 // cross off the bit at shared-memory bit address hb
 __device__ __forceinline__ void mark_bitaddr(uint32_t hb) {
-  atom_or_shared((hb >> 3) & ~3u, 1u << (hb & 31u));
+  atom_or_shared((hb >> 3) & ~3u, bit_of(hb));
 }
 
 // Mid-prime hits with the multiples of 5 skipped.  Hit j of prime p in class
@@ -428,14 +435,14 @@ __device__ __forceinline__ uint32_t skip5_phase(uint32_t k05, uint32_t cmod, uin
 
 // cross off bit h of the bitmap at shared address a0
 __device__ __forceinline__ void mark(uint32_t a0, uint32_t h) {
-  atom_or_shared(a0 + ((h >> 5) << 2), 1u << (h & 31u));
+  atom_or_shared(a0 + ((h >> 5) << 2), bit_of(h));
 }
 
 // ... only if h < len, as a predicated atomic (no branch / reconvergence)
 __device__ __forceinline__ void mark_if(uint32_t a0, uint32_t h, uint32_t len) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %2, %3;\n\t@q red.shared.or.b32 [%0], %1;\n\t}"
-      ::"r"(a0 + ((h >> 5) << 2)), "r"(1u << (h & 31u)), "r"(h), "r"(len)
+      ::"r"(a0 + ((h >> 5) << 2)), "r"(bit_of(h)), "r"(h), "r"(len)
       : "memory");
 }
 
@@ -472,27 +479,39 @@ constexpr uint32_t kTransMin = 384;
 __device__ __forceinline__ void mark_transposed(uint32_t a0, uint32_t rel, uint32_t p,
                                                 uint32_t len, uint32_t lane) {
   const uint32_t lane_off = a0 + 4u * lane * p;
+  // word address of the lane's hit at superblock-relative position pos: one
+  // shift and one multiply-add
+  auto mark_at = [&](uint32_t pos) {
+    uint32_t addr;
+    asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(addr) : "r"(pos >> 5), "r"(lane_off));
+    atom_or_shared(addr, bit_of(pos));
+  };
   uint32_t pos = rel;
   while (pos + 1023u * p < len) {
 #pragma unroll 8
     for (uint32_t i = 0; i < 32; ++i) {
-      atom_or_shared(lane_off + ((pos >> 5) << 2), 1u << (pos & 31u));
+      mark_at(pos);
       pos += p;
     }
     pos += 992u * p;
   }
   if (pos + (kTransMin - 1u) * p < len) {
-    // the lane's hits start at pos + 32 l p: in range while pos < len - 32 l p
-    const uint32_t lp = 32u * lane * p;
-    const uint32_t lim = len > lp ? len - lp : 0u;
+    // last, partial superblock: the lanes whose 32 hits all lie below len run
+    // the same 32 ops under ONE branch (no per-op predicate); the hits after
+    // them -- fewer than 32 -- are one strided op
+    const bool full = pos + 32u * lane * p + 31u * p < len;
+    const uint32_t nfull = __popc(__ballot_sync(kFull, full));
+    if (full) {
+      uint32_t q = pos;
 #pragma unroll 8
-    for (uint32_t i = 0; i < 32; ++i) {
-      if (pos < lim) atom_or_shared(lane_off + ((pos >> 5) << 2), 1u << (pos & 31u));
-      pos += p;
+      for (uint32_t i = 0; i < 32; ++i) {
+        mark_at(q);
+        q += p;
+      }
     }
-  } else if (pos < len) {
-    mark_strided(a0, pos, p, len, lane);
+    pos += 32u * nfull * p;
   }
+  if (pos < len) mark_strided(a0, pos, p, len, lane);
 }
 
 // Phase 2: medium and large primes (NT threads per block).
@@ -1271,10 +1290,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) sieve_wide_kernel(const Sieve
       if (pending) flush(sis[cur ^ 1]);
       fetch_unit(P, sis[cur ^ 1]);
     }
-    if (P.wc_trans)
-      sieve_primes<kWideThreads, true, true>(P, sis[cur], bm1, bm5, &wc_ctr, nprimes);
-    else
-      sieve_primes<kWideThreads, true, false>(P, sis[cur], bm1, bm5, &wc_ctr, nprimes);
+    sieve_primes<kWideThreads, true, true>(P, sis[cur], bm1, bm5, &wc_ctr, nprimes);
     __syncthreads();  // B
     const bool more = sis[cur ^ 1].s != ~0ull;
     if (threadIdx.x == 0) wc_ctr = 0;

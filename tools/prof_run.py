@@ -23,6 +23,10 @@ if cfg == "c2":
     f = lambda: sv.enumerate_range(0, 10**10, out=out)[2]
 elif cfg == "c1":
     f = lambda: sv.count_range(0, 10**9 + 1)
+elif cfg in ("p10", "p11", "p95", "p2e11", "p3e11", "p5e11"):  # count-only pi(N)
+    hi_ = {"p10": 10**10, "p11": 10**11, "p95": 3 * 10**9, "p2e11": 2 * 10**11,
+           "p3e11": 3 * 10**11, "p5e11": 5 * 10**11}[cfg]
+    f = lambda: sv.count_range(0, hi_ + 1)
 elif cfg == "c3":
     f = lambda: sv.count_range(0, 10**12 + 1)
 elif cfg == "c3s":  # 1/8 share of c3 (one rank at 8 GPUs)
