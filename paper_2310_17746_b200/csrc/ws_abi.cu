@@ -256,13 +256,14 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
                        c->base_B >= static_cast<uint64_t>(c->bucket_min_ratio) * c->S;
   // wide units (sieve_wide_kernel): single-job count launches without bucket
   // lists, long enough to keep every SM's lone CTA busy for many units
-  if (c->wide > 1 && mode <= wsk::kCountChecks && nj == 1 && !buckets &&
-      c->S == (1u << 18) && c->words_out[0] == nullptr &&
-      nseg >= static_cast<uint64_t>(c->wide_min_units) * c->wide * c->sms) {
-    p.wide = std::min<uint32_t>(c->wide, wsk::kWideMax);
+  const uint32_t wide_want = buckets ? c->wide_bucket : (nj > 1 ? c->wide_multi : c->wide);
+  if (wide_want > 1 && mode <= wsk::kCountChecks && c->S == (1u << 18) &&
+      c->words_out[0] == nullptr && nseg < (1ull << 28) && nseg >= 6 * nj &&
+      nseg >= static_cast<uint64_t>(c->wide_min_units) * wide_want * c->sms) {
+    p.wide = std::min<uint32_t>(wide_want, wsk::kWideMax);
     p.n_S = std::min<uint32_t>(
         std::max(table_primes_below(c, static_cast<uint64_t>(p.wide) * c->S), p.n_wc), c->nprimes);
-    p.n_mid = c->nprimes;
+    if (!buckets) p.n_mid = c->nprimes;
     p.miss_lane = 1;
     p.skip5_max = c->wide_skip5;
     if (c->wide_n_wc) p.n_wc = std::min<uint32_t>(c->wide_n_wc, p.n_S);
@@ -343,6 +344,30 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     ck(copy_async(c, c->runs.ptr, hr, runs.size() * sizeof(wsk::Run), cudaMemcpyHostToDevice,
                   c->stream), "upload runs");
   }
+  // wide units over windows or several jobs: the launch's unit table
+  std::vector<uint32_t> unit_off(nwin + 1, 0);
+  if (p.wide > 1 && (buckets || nj > 1)) {
+    std::vector<uint32_t> units;
+    units.reserve(nseg / p.wide + nj + nwin);
+    size_t j = 0;
+    for (uint64_t w = 0; w < nwin; ++w) {
+      const uint64_t ws = w * W, we = std::min(nseg, ws + W);
+      while (j < nj && c->h_jobs[j].seg_begin + c->h_jobs[j].nseg <= ws) ++j;
+      for (size_t q = j; q < nj && c->h_jobs[q].seg_begin < we; ++q) {
+        const wsk::Job& J = c->h_jobs[q];
+        const uint64_t a0 = std::max(ws, J.seg_begin), b0 = std::min(we, J.seg_begin + J.nseg);
+        for (uint64_t x = a0; x < b0; x += p.wide)
+          units.push_back(static_cast<uint32_t>(x - ws) |
+                          static_cast<uint32_t>(std::min<uint64_t>(p.wide, b0 - x)) << 28);
+      }
+      unit_off[w + 1] = static_cast<uint32_t>(units.size());
+    }
+    c->units.reserve(std::max<size_t>(units.size(), 1), "units");
+    void* hu = c->pin_up.alloc(units.size() * sizeof(uint32_t) + 4, "pinned units");
+    std::memcpy(hu, units.data(), units.size() * sizeof(uint32_t));
+    ck(copy_async(c, c->units.ptr, hu, units.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                  c->stream), "upload units");
+  }
   // ev[2] (call start) / ev[4] order the fill stream after everything queued so far
   join_base(c);
   if (record_start) record_timing_event(c, c->ev[2]);
@@ -415,7 +440,12 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     p.s_begin = ws;
     p.s_count = we - ws;
     p.ticket = c->ticket.ptr + 2 * w;
-    const uint64_t units = p.wide > 1 ? (we - ws + p.wide - 1) / p.wide : we - ws;
+    uint64_t units = p.wide > 1 ? (we - ws + p.wide - 1) / p.wide : we - ws;
+    if (unit_off[nwin]) {
+      p.units = c->units.ptr + unit_off[w];
+      p.nunits = unit_off[w + 1] - unit_off[w];
+      units = p.nunits;
+    }
     const int grid = static_cast<int>(std::min<uint64_t>(units, max_grid));
     ck(wsk::launch_sieve(mode, p, grid, c->stream), "sieve launch");
     if (buckets) ck(cudaEventRecord(c->sieve_done[b], c->stream), "event");
@@ -1488,6 +1518,8 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_MISS_LANE")) c->miss_lane = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_SKIP5")) c->skip5_max = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE")) c->wide = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_WIDE_BUCKET")) c->wide_bucket = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_WIDE_MULTI")) c->wide_multi = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_SKIP5")) c->wide_skip5 = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_WC_LIMIT"))
     c->wide_n_wc = table_primes_below(c, std::strtoul(e, nullptr, 10));

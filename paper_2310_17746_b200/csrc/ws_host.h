@@ -195,9 +195,12 @@ struct DevCtx {
   int sms = 148;
   int bps[wsk::kNumModes] = {2, 2, 2, 2};  // resident blocks per SM per mode
   uint32_t wide = 3;            // > 1: long count launches sieve this many segments per unit (WHEELSIEVE_WIDE)
+  uint32_t wide_bucket = 3;     // ... in bucket windows (WHEELSIEVE_WIDE_BUCKET; C4 -4.8%, C5 -7.4%)
+  uint32_t wide_multi = 3;      // ... in launches over several jobs without buckets (WHEELSIEVE_WIDE_MULTI);
+                                // several jobs: only when they average at least 6 segments
   uint32_t wide_skip5 = 49152;  // wide units: skip5_max (3x the hits per visit; WHEELSIEVE_WIDE_SKIP5)
   uint32_t wide_n_wc = 0;       // wide units: warp-cooperative primes (0: the context's n_wc)
-  uint32_t wide_min_units = 8;  // ... when every SM gets at least this many units
+  uint32_t wide_min_units = 2;  // ... when every SM gets at least this many units (pi(3e9): -11% at 4.3; C1 at 1.4: no gain)
   std::string err;
   ws_timing timing{};
   cudaEvent_t ev[4] = {};
@@ -285,6 +288,7 @@ struct DevCtx {
   std::vector<cudaEvent_t> ring_ev;
   cudaEvent_t fill_done[2] = {}, sieve_done[2] = {};
   DevBuf<wsk::Run> runs;
+  DevBuf<uint32_t> units;  // wide launches over windows / several jobs: unit table
   DevBuf<wsk::Job> jobs;
   DevBuf<wsk::JobAcc> acc;
   DevBuf<wsk::JobAcc> gather;   // multi-device: every shard's records after the allgather

@@ -88,6 +88,8 @@ struct SieveParams {
   uint32_t miss_lane;                // single-hit misses OR 0 into word `lane` (else a word from h)
   uint32_t skip5_max;                // mid primes below it skip their hits on multiples of 5
   uint32_t wide;                     // > 1: sieve_wide_kernel, this many segments per unit
+  const uint32_t* units;             // wide launches over windows or several jobs: per unit,
+  uint32_t nunits;                   //   first window-local segment | segment count << 28
   uint32_t* words1;                  // nullable (count modes): survivor flag words of
   uint32_t* words5;                  // each class, segment s at word s * S / 32
 };

@@ -515,7 +515,7 @@ __device__ __forceinline__ void mark_transposed(uint32_t a0, uint32_t rel, uint3
 }
 
 // Phase 2: medium and large primes (NT threads per block).
-template <int NT, bool WC_LAST = false, bool WCT = false>
+template <int NT, bool WC_LAST = false, bool WCT = false, bool BK = true>
 __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo& si,
                                              uint32_t* bm1, uint32_t* bm5, uint32_t* wc_ctr,
                                              uint32_t nprimes) {
@@ -527,7 +527,7 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   const ModCtx mc = mod_ctx(ks);
   const uint32_t ks5 = static_cast<uint32_t>(ks % 5u);  // for the multiple-of-5 skips
   const uint32_t n_wc = min(P.n_wc, nprimes), n_mid = min(P.n_mid, nprimes);
-  const uint32_t n_S = min(P.n_S, n_mid);
+  const uint32_t n_S = min(P.n_S, nprimes);  // (mid_end below caps it when bucketing)
   // warp-cooperative primes, handed out dynamically (largest work first); the
   // next prime is claimed and its p and 1/p loaded while the current one is
   // marked
@@ -564,7 +564,12 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   // times before the closing barrier
   if (!WC_LAST) wc_phase();
   // large primes come from the window's bucket list unless it overflowed
-  const bool use_bucket = P.bucket != nullptr && P.bcount[si.s - P.s_begin] <= P.bcap;
+  // (a wide unit: every one of its segments' lists)
+  const uint32_t nparts = WC_LAST ? (len + P.S - 1) / P.S : 1u;
+  bool use_bucket = BK && P.bucket != nullptr;  // BK false: a launch without bucket lists
+  if (use_bucket)
+    for (uint32_t part = 0; part < nparts; ++part)
+      use_bucket = use_bucket && P.bcount[si.s - P.s_begin + part] <= P.bcap;
   const uint32_t lp_end = use_bucket ? n_mid : nprimes;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t mid_end = n_S < lp_end ? n_S : lp_end;
@@ -668,32 +673,45 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
   if (use_bucket) {
     // an entry is the bit index into [bm1 | bm5] (class at bit log2 S), so a
     // hit is shift + atomic; lists are read 4 entries per 128-bit streamed
-    // load, two loads in flight per thread
-    const uint64_t ls = si.s - P.s_begin;
-    const uint32_t n = P.bcount[ls];
-    const uint32_t* list = P.bucket + ls * P.bcap;  // 128 B aligned (bcap % 32 == 0)
-    const uint4* list4 = reinterpret_cast<const uint4*>(list);
-    const uint32_t n4 = n >> 2;
-    uint32_t i = threadIdx.x;
-    for (; i + NT < n4; i += 2 * NT) {
-      const uint4 x = __ldcs(list4 + i), y = __ldcs(list4 + i + NT);
-      mark(a1, x.x);
-      mark(a1, x.y);
-      mark(a1, x.z);
-      mark(a1, x.w);
-      mark(a1, y.x);
-      mark(a1, y.y);
-      mark(a1, y.z);
-      mark(a1, y.w);
+    // load, two loads in flight per thread.  In a wide unit the classes are
+    // P.wide * S bits apart and segment `part` starts S * part bits in:
+    // entry e -> e + part S + (e >> log2 S) (wide - 1) S.
+    const uint32_t log2S = 31u - __clz(P.S);
+    const uint32_t wm1S = WC_LAST ? (P.wide - 1u) * P.S : 0u;
+    for (uint32_t part = 0; part < nparts; ++part) {
+      const uint32_t partS = part * P.S;
+      auto put = [&](uint32_t e) {
+        if (WC_LAST)
+          mark(a1, e + partS + (e >> log2S) * wm1S);
+        else
+          mark(a1, e);
+      };
+      const uint64_t ls = si.s - P.s_begin + part;
+      const uint32_t n = P.bcount[ls];
+      const uint32_t* list = P.bucket + ls * P.bcap;  // 128 B aligned (bcap % 32 == 0)
+      const uint4* list4 = reinterpret_cast<const uint4*>(list);
+      const uint32_t n4 = n >> 2;
+      uint32_t i = threadIdx.x;
+      for (; i + NT < n4; i += 2 * NT) {
+        const uint4 x = __ldcs(list4 + i), y = __ldcs(list4 + i + NT);
+        put(x.x);
+        put(x.y);
+        put(x.z);
+        put(x.w);
+        put(y.x);
+        put(y.y);
+        put(y.z);
+        put(y.w);
+      }
+      if (i < n4) {
+        const uint4 x = __ldcs(list4 + i);
+        put(x.x);
+        put(x.y);
+        put(x.z);
+        put(x.w);
+      }
+      for (uint32_t j = 4 * n4 + threadIdx.x; j < n; j += NT) put(__ldcs(list + j));
     }
-    if (i < n4) {
-      const uint4 x = __ldcs(list4 + i);
-      mark(a1, x.x);
-      mark(a1, x.y);
-      mark(a1, x.z);
-      mark(a1, x.w);
-    }
-    for (uint32_t j = 4 * n4 + threadIdx.x; j < n; j += NT) mark(a1, __ldcs(list + j));
   }
   if (WC_LAST) wc_phase();
 }
@@ -1098,11 +1116,13 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
 // The next unit's ticket and geometry are fetched by thread 0 during the
 // marking, and the unit's totals gather in shared accumulators that thread 0
 // flushes after barrier A.  Per-segment counts stay per S-slot segment.
-// Single-job count launches without bucket lists only (host-side gate).
+// Count modes only (host-side gate).  Launches over bucket windows or several
+// jobs bring a unit table (units never straddle a job or a window); a unit
+// applies the bucket lists of each of its segments.
 constexpr int kWideThreads = 1024;
 
 __device__ void fetch_unit(const SieveParams& P, SegInfo& si) {
-  const uint64_t nunits = (P.s_count + P.wide - 1) / P.wide;
+  const uint64_t nunits = P.units ? P.nunits : (P.s_count + P.wide - 1) / P.wide;
   const unsigned long long t = atomicAdd(P.ticket, 1ull);
   if (t >= nunits) {
     si.s = ~0ull;
@@ -1112,13 +1132,35 @@ __device__ void fetch_unit(const SieveParams& P, SegInfo& si) {
     }
     return;
   }
-  const Job& J = P.job0;
-  const uint64_t local = t * P.wide;  // first segment of the unit (s_begin == seg_begin)
-  si.s = P.s_begin + local;
-  si.job = 0;
+  // the unit's first segment and segment count: analytic for one job without
+  // windows, else from the launch's unit table (units never straddle a job
+  // or a window): first window-local segment | count << 28
+  uint64_t first = t * P.wide;
+  uint32_t cnt = P.wide;
+  if (P.units) {
+    const uint32_t e = __ldg(P.units + t);
+    first = e & 0x0FFFFFFFu;
+    cnt = e >> 28;
+  }
+  const uint64_t s = P.s_begin + first;
+  uint32_t lo = 0;
+  Job J;
+  if (P.njobs == 1) {
+    J = P.job0;
+  } else {
+    uint32_t hi = P.njobs;  // last job with seg_begin <= s
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) / 2;
+      if (P.jobs[mid].seg_begin <= s) lo = mid; else hi = mid;
+    }
+    J = P.jobs[lo];
+  }
+  si.s = s;
+  si.job = lo;
+  const uint64_t local = s - J.seg_begin;
   si.ks = J.K0 + local * P.S;
   const uint64_t rem = J.nslots - local * P.S;
-  const uint64_t cap = static_cast<uint64_t>(P.wide) * P.S;
+  const uint64_t cap = static_cast<uint64_t>(cnt) * P.S;
   si.len = rem < cap ? static_cast<uint32_t>(rem) : static_cast<uint32_t>(cap);
   si.lo1 = first_valid(si.ks, 1, J.L);
   if (si.ks == 0 && si.lo1 < 1) si.lo1 = 1;
@@ -1135,7 +1177,7 @@ struct WideAcc {
   uint32_t cnt[4];
 };
 
-template <int MODE>
+template <int MODE, bool BK>
 __global__ void __launch_bounds__(kWideThreads, 1) sieve_wide_kernel(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   const uint32_t wps = P.S / 32;  // words per class per segment (a multiple of kWideThreads)
@@ -1261,11 +1303,12 @@ __global__ void __launch_bounds__(kWideThreads, 1) sieve_wide_kernel(const Sieve
   };
   // thread 0: the finished unit's totals to the job accumulators
   auto flush = [&](const SegInfo& o) {
-    JobAcc& A = P.acc[0];
+    JobAcc& A = P.acc[o.job];
     unsigned long long total = 0;
     for (uint32_t part = 0; part < P.wide; ++part) {
       if (part * P.S < o.len) {
         if (P.per_seg) P.per_seg[o.s + part] = acc.cnt[part];
+        if (BK && P.bucket) P.bcount[o.s - P.s_begin + part] = 0;  // list consumed
         total += acc.cnt[part];
       }
       acc.cnt[part] = 0;
@@ -1290,7 +1333,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) sieve_wide_kernel(const Sieve
       if (pending) flush(sis[cur ^ 1]);
       fetch_unit(P, sis[cur ^ 1]);
     }
-    sieve_primes<kWideThreads, true, true>(P, sis[cur], bm1, bm5, &wc_ctr, nprimes);
+    sieve_primes<kWideThreads, true, true, BK>(P, sis[cur], bm1, bm5, &wc_ctr, nprimes);
     __syncthreads();  // B
     const bool more = sis[cur ^ 1].s != ~0ull;
     if (threadIdx.x == 0) wc_ctr = 0;
@@ -1937,8 +1980,10 @@ cudaError_t sieve_configure(int* blocks_per_sm) {
     if (e != cudaSuccess) return e;
     blocks_per_sm[m] = b < 1 ? 1 : b;
   }
-  for (const void* f : {reinterpret_cast<const void*>(sieve_wide_kernel<kCount>),
-                        reinterpret_cast<const void*>(sieve_wide_kernel<kCountChecks>)}) {
+  for (const void* f : {reinterpret_cast<const void*>(sieve_wide_kernel<kCount, false>),
+                        reinterpret_cast<const void*>(sieve_wide_kernel<kCountChecks, false>),
+                        reinterpret_cast<const void*>(sieve_wide_kernel<kCount, true>),
+                        reinterpret_cast<const void*>(sieve_wide_kernel<kCountChecks, true>)}) {
     e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kWideMax * sieve_smem_bytes(1u << 18, kCount)));
     if (e != cudaSuccess) return e;
@@ -1959,10 +2004,17 @@ cudaError_t sieve_configure(int* blocks_per_sm) {
 cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t st) {
   if (p.wide > 1) {  // count modes only (host-side gate)
     const size_t wsmem = static_cast<size_t>(p.wide) * sieve_smem_bytes(p.S, kCount);
-    if (mode == kCount)
-      sieve_wide_kernel<kCount><<<grid, kWideThreads, wsmem, st>>>(p);
-    else
-      sieve_wide_kernel<kCountChecks><<<grid, kWideThreads, wsmem, st>>>(p);
+    if (p.bucket != nullptr) {
+      if (mode == kCount)
+        sieve_wide_kernel<kCount, true><<<grid, kWideThreads, wsmem, st>>>(p);
+      else
+        sieve_wide_kernel<kCountChecks, true><<<grid, kWideThreads, wsmem, st>>>(p);
+    } else {
+      if (mode == kCount)
+        sieve_wide_kernel<kCount, false><<<grid, kWideThreads, wsmem, st>>>(p);
+      else
+        sieve_wide_kernel<kCountChecks, false><<<grid, kWideThreads, wsmem, st>>>(p);
+    }
     return cudaGetLastError();
   }
   const size_t smem = sieve_smem_bytes(p.S, mode);
