@@ -434,13 +434,18 @@ def run_ours(args, cfg, world, rank, local):
         hits = bucket_hits(lo0, hi0)
         b_smem = smem_bytes(lo0, hi0)
         primes0 = shard_counts[0] if kind == "enumerate" else 0  # device 0's shard
+    # count launches long enough take the wide kernel (3 segments per unit, one
+    # 1024-thread CTA per SM); WHEELSIEVE_WIDE=0 keeps the per-segment kernel
+    wide_on = os.environ.get("WHEELSIEVE_WIDE", "3") not in ("0", "1")
+    count_kernel = ("sieve_wide_kernel" if wide_on and args.config in ("c3", "c4", "c5")
+                    else "sieve_kernel")
     alg = 8.0 * primes0 + 8.0 * hits
     roof = None
     if alg > 0:
         achieved = alg / (avg_sieve_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "kernel": ("sieve_kernel<kEnumerate>" if kind == "enumerate" else "sieve_kernel")
+                "kernel": ("sieve_kernel<kEnumerate>" if kind == "enumerate" else count_kernel)
                           + (" + bucket_fill_kernel" if hits else ""),
                 "algorithmic_bytes_per_launch": alg,
                 "model": ("8 B x primes written" if kind == "enumerate" else "")
@@ -455,6 +460,7 @@ def run_ours(args, cfg, world, rank, local):
                  "frac": sach / speak, "algorithmic_bytes_per_launch": b_smem,
                  "traffic": traffic if kind != "enumerate" else None,
                  "avg_launch_ms": avg_sieve_ms,
+                 "kernel": "sieve_kernel<kEnumerate>" if kind == "enumerate" else count_kernel,
                  "model": "SURVEY 8d: 4 B x [2W + sum_{17<=p<=sqrt R} min(hits_p, W)]",
                  "peak_source": f"{props.multi_processor_count} SMs x 128 B/clk x {smax} MHz"}
     roof_hbm = roof

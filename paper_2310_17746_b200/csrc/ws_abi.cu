@@ -266,6 +266,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     if (!buckets) p.n_mid = c->nprimes;
     p.miss_lane = 1;
     p.skip5_max = c->wide_skip5;
+    p.trans_min = c->trans_min;
     if (c->wide_n_wc) p.n_wc = std::min<uint32_t>(c->wide_n_wc, p.n_S);
     max_grid = c->sms;
   }
@@ -1520,6 +1521,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_WIDE")) c->wide = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_BUCKET")) c->wide_bucket = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_MULTI")) c->wide_multi = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_TRANS_MIN")) c->trans_min = std::max<uint32_t>(32, std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_SKIP5")) c->wide_skip5 = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_WC_LIMIT"))
     c->wide_n_wc = table_primes_below(c, std::strtoul(e, nullptr, 10));

@@ -472,12 +472,11 @@ __device__ __forceinline__ void mark_strided(uint32_t a0, uint32_t h0, uint32_t 
 // and warp op i marking hit 32 l + i in every lane.  The lanes of an op are
 // then exactly 32 p bits = p words apart -- p is odd, so the 32 words fall in
 // 32 different banks (one wavefront per op, where consecutive hits per op
-// average 2.5) -- and they share the bit within the word.  A last partial
-// superblock of at least kTransMin hits runs the same way with the lanes
-// past the end predicated off; shorter tails use the strided loop.
-constexpr uint32_t kTransMin = 384;
+// average 2.5) -- and they share the bit within the word.  In a last partial
+// superblock of at least tmin hits the lanes whose 32 hits all fit run the
+// same way; shorter tails use the strided loop.
 __device__ __forceinline__ void mark_transposed(uint32_t a0, uint32_t rel, uint32_t p,
-                                                uint32_t len, uint32_t lane) {
+                                                uint32_t len, uint32_t lane, uint32_t tmin) {
   const uint32_t lane_off = a0 + 4u * lane * p;
   // word address of the lane's hit at superblock-relative position pos: one
   // shift and one multiply-add
@@ -495,7 +494,7 @@ __device__ __forceinline__ void mark_transposed(uint32_t a0, uint32_t rel, uint3
     }
     pos += 992u * p;
   }
-  if (pos + (kTransMin - 1u) * p < len) {
+  if (pos + (tmin - 1u) * p < len) {
     // last, partial superblock: the lanes whose 32 hits all lie below len run
     // the same 32 ops under ONE branch (no per-op predicate); the hits after
     // them -- fewer than 32 -- are one strided op
@@ -551,8 +550,8 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       uint32_t rel1, rel5;
       if (!prime_offsets(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5)) break;
       if (WCT) {
-        mark_transposed(a1, rel1, p, len, lane);
-        mark_transposed(a5, rel5, p, len, lane);
+        mark_transposed(a1, rel1, p, len, lane, P.trans_min);
+        mark_transposed(a5, rel5, p, len, lane, P.trans_min);
       } else {
         mark_strided(a1, rel1, p, len, lane);
         mark_strided(a5, rel5, p, len, lane);
