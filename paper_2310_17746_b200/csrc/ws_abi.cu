@@ -263,6 +263,11 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     p.wide = std::min<uint32_t>(wide_want, wsk::kWideMax);
     p.n_S = std::min<uint32_t>(
         std::max(table_primes_below(c, static_cast<uint64_t>(p.wide) * c->S), p.n_wc), c->nprimes);
+    if (c->wide_double) {  // primes of at least half a unit: at most 2 hits per class, no loop
+      const uint64_t unit = static_cast<uint64_t>(p.wide) * c->S;
+      p.n_dbl = p.n_S;
+      p.n_S = std::min<uint32_t>(std::max(table_primes_below(c, (unit + 1) / 2), p.n_wc), p.n_dbl);
+    }
     if (!buckets) p.n_mid = c->nprimes;
     p.miss_lane = 1;
     p.skip5_max = c->wide_skip5;
@@ -1521,6 +1526,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_WIDE")) c->wide = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_BUCKET")) c->wide_bucket = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_MULTI")) c->wide_multi = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_WIDE_DOUBLE")) c->wide_double = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_TRANS_MIN")) c->trans_min = std::max<uint32_t>(32, std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_SKIP5")) c->wide_skip5 = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_WC_LIMIT"))

@@ -69,6 +69,7 @@ struct SieveParams {
   const uint32_t* nprimes_dev;       // nullable: exact table size, written on device
   uint32_t n_wc;                     // primes [0, n_wc) use the warp-cooperative loop
   uint32_t n_S;                      // primes [n_wc, n_S) (p < S): one thread per prime, loop
+  uint32_t n_dbl;                    // wide: [n_S, n_dbl) straight-line, <= 2 hits per class
   uint32_t n_mid;                    // [n_S, n_mid): one thread per prime, <= 1 hit per class;
                                      // [n_mid, nprimes) from buckets (directly if bucket == null)
   const uint32_t* bucket;            // window lists: bucket[(s - s_begin) * bcap + i]

@@ -637,17 +637,19 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
       mark_if(a5, h + d, d < 0 ? len : 0u);
     }
   }
-  // p >= S (no bucket list): at most one hit per class -- no loop, no branch;
-  // unswitched on the quotient path (ks < 2^53 everywhere but the very top)
-  auto single_hits = [&](auto fast) {
-    uint32_t base = mid_end + 32 * warp;
+  // p >= len / HITS: at most HITS hits per class -- no loop, no branch;
+  // unswitched on the quotient path (ks < 2^53 everywhere but the very top).
+  // HITS == 2 (wide units, primes of at least half the unit): the second hit
+  // is p further on.  (Three hits for primes of a third measured no faster.)
+  auto few_hits = [&](auto fast, auto hits, uint32_t begin, uint32_t end) {
+    uint32_t base = begin + 32 * warp;
     uint32_t pn;
     double ipn;
-    load(base + lane, lp_end, pn, ipn);
-    for (; base < lp_end; base += kStride) {
+    load(base + lane, end, pn, ipn);
+    for (; base < end; base += kStride) {
       const uint32_t p = pn, i = base + lane;
       const double ip = ipn;
-      load(base + kStride + lane, lp_end, pn, ipn);
+      load(base + kStride + lane, end, pn, ipn);
       if (__shfl_sync(kFull, p, 0) > t_hi) break;
       uint32_t rel1 = len, rel5 = len;
       prime_offsets_t<decltype(fast)::value>(p, ip, i, P.prime_m, mc, t_lo, t_hi, rel1, rel5);
@@ -663,12 +665,23 @@ __device__ __forceinline__ void sieve_primes(const SieveParams& P, const SegInfo
         mark_or(a1, rel1, len, P.S / 32 - 1);
         mark_or(a5, rel5, len, P.S / 32 - 1);
       }
+      if (decltype(hits)::value >= 2) {  // (wide launches set miss_lane)
+        // min: rel + p must not wrap for the out-of-range sentinel p = 2^32 - 1
+        const uint32_t step = min(p, len);
+        mark_or_lane(a1, rel1 + step, len, lane);
+        mark_or_lane(a5, rel5 + step, len, lane);
+      }
     }
   };
+  const uint32_t dbl_end = max(mid_end, min(P.n_dbl, lp_end));
+  auto few_all = [&](auto fast) {
+    if (dbl_end > mid_end) few_hits(fast, std::integral_constant<int, 2>{}, mid_end, dbl_end);
+    few_hits(fast, std::integral_constant<int, 1>{}, dbl_end, lp_end);
+  };
   if (mc.fast)
-    single_hits(std::true_type{});
+    few_all(std::true_type{});
   else
-    single_hits(std::false_type{});
+    few_all(std::false_type{});
   if (use_bucket) {
     // an entry is the bit index into [bm1 | bm5] (class at bit log2 S), so a
     // hit is shift + atomic; lists are read 4 entries per 128-bit streamed
