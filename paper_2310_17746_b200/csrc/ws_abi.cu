@@ -240,6 +240,8 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   p.mid_bitaddr = c->mid_bitaddr;
   p.miss_lane = c->miss_lane;
   p.skip5_max = c->skip5_max;
+  p.seg_trans = c->seg_trans;
+  p.trans_min = c->seg_trans_min;
   p.words1 = c->words_out[0];
   p.words5 = c->words_out[1];
   if (wire) {
@@ -272,6 +274,7 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
     p.miss_lane = 1;
     p.skip5_max = c->wide_skip5;
     p.trans_min = c->trans_min;
+    p.seg_trans = 0;
     if (c->wide_n_wc) p.n_wc = std::min<uint32_t>(c->wide_n_wc, p.n_S);
     max_grid = c->sms;
   }
@@ -1526,6 +1529,8 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_WIDE")) c->wide = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_BUCKET")) c->wide_bucket = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_MULTI")) c->wide_multi = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_SEG_TRANS")) c->seg_trans = std::atoi(e) != 0;
+  if (const char* e = std::getenv("WHEELSIEVE_SEG_TRANS_MIN")) c->seg_trans_min = std::max<uint32_t>(32, std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_DOUBLE")) c->wide_double = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_TRANS_MIN")) c->trans_min = std::max<uint32_t>(32, std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_SKIP5")) c->wide_skip5 = std::strtoul(e, nullptr, 10);

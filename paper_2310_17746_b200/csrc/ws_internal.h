@@ -89,6 +89,7 @@ struct SieveParams {
   uint32_t miss_lane;                // single-hit misses OR 0 into word `lane` (else a word from h)
   uint32_t skip5_max;                // mid primes below it skip their hits on multiples of 5
   uint32_t wide;                     // > 1: sieve_wide_kernel, this many segments per unit
+  uint32_t seg_trans;                // per-segment kernel: transposed warp-cooperative marking
   uint32_t trans_min;                // wide: shortest partial superblock marked transposed
   const uint32_t* units;             // wide launches over windows or several jobs: per unit,
   uint32_t nunits;                   //   first window-local segment | segment count << 28

@@ -35,6 +35,12 @@
 //                   the global output offset, then coalesced uint64 stores
 //                   (or the 8-bit host wire format, ws_wire.cpp).
 //
+// sieve_wide_kernel (long count launches): one 1024-thread CTA per SM owns
+// three consecutive segments as one unit -- per-(prime, unit) work is paid
+// once per three segments, count and next-unit stamping are one pass (two
+// barriers per unit), and the warp-cooperative primes are marked in
+// conflict-free transposed superblocks (mark_transposed).
+//
 // Other kernels here: bucket_fill_kernel (large-prime hit lists per window,
 // one launch per window) and bucket_fill_huge_kernel (primes of at least the
 // run length, first hits carried across runs); small_base_kernel (base tables
@@ -853,7 +859,7 @@ constexpr size_t mode_smem_extra() {
 }
 
 // ---------------------------------------------------------------------------
-template <int MODE>
+template <int MODE, bool WCT = false>
 __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bm1 = smem;
@@ -881,7 +887,7 @@ __global__ void __launch_bounds__(kThreads, 3) sieve_kernel(const SieveParams P)
     if (si.s == ~0ull) break;
     init_words(si, tab, bm1, bm5);
     __syncthreads();
-    sieve_primes<kThreads>(P, si, bm1, bm5, &wc_ctr, nprimes);
+    sieve_primes<kThreads, false, WCT>(P, si, bm1, bm5, &wc_ctr, nprimes);
     __syncthreads();
     if (P.bucket != nullptr && threadIdx.x == 0) P.bcount[si.s - P.s_begin] = 0;
 
@@ -1982,9 +1988,16 @@ cudaError_t sieve_configure(int* blocks_per_sm) {
                                 reinterpret_cast<const void*>(sieve_kernel<kCountChecks>),
                                 reinterpret_cast<const void*>(sieve_kernel<kEnumerate>),
                                 reinterpret_cast<const void*>(sieve_kernel<kEnumWire>)};
+  const void* fns_t[kNumModes] = {reinterpret_cast<const void*>(sieve_kernel<kCount, true>),
+                                  reinterpret_cast<const void*>(sieve_kernel<kCountChecks, true>),
+                                  reinterpret_cast<const void*>(sieve_kernel<kEnumerate, true>),
+                                  reinterpret_cast<const void*>(sieve_kernel<kEnumWire, true>)};
   for (int m = 0; m < kNumModes; ++m) {
     const size_t smem = sieve_smem_bytes(1u << 18, m);
     e = cudaFuncSetAttribute(fns[m], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fns_t[m], cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int b = 0;
@@ -2030,6 +2043,15 @@ cudaError_t launch_sieve(int mode, const SieveParams& p, int grid, cudaStream_t 
     return cudaGetLastError();
   }
   const size_t smem = sieve_smem_bytes(p.S, mode);
+  if (p.seg_trans) {
+    switch (mode) {
+      case kCount: sieve_kernel<kCount, true><<<grid, kThreads, smem, st>>>(p); break;
+      case kCountChecks: sieve_kernel<kCountChecks, true><<<grid, kThreads, smem, st>>>(p); break;
+      case kEnumerate: sieve_kernel<kEnumerate, true><<<grid, kThreads, smem, st>>>(p); break;
+      default: sieve_kernel<kEnumWire, true><<<grid, kThreads, smem, st>>>(p); break;
+    }
+    return cudaGetLastError();
+  }
   switch (mode) {
     case kCount: sieve_kernel<kCount><<<grid, kThreads, smem, st>>>(p); break;
     case kCountChecks: sieve_kernel<kCountChecks><<<grid, kThreads, smem, st>>>(p); break;
