@@ -200,7 +200,7 @@ struct DevCtx {
                                 // several jobs: only when they average at least 6 segments
   uint32_t trans_min = 768;     // wide units: shortest partial superblock marked transposed
                                 // (WHEELSIEVE_TRANS_MIN; 192..768 measured within 2%, 768 best)
-  uint32_t seg_trans = 0;       // per-segment kernel: transposed warp-cooperative marking (WHEELSIEVE_SEG_TRANS)
+  uint32_t seg_trans = 1;       // per-segment count kernels: transposed warp-cooperative marking (WHEELSIEVE_SEG_TRANS)
   uint32_t seg_trans_min = 768; // ... its shortest transposed partial superblock
   uint32_t wide_double = 1;     // wide units: straight-line marking for primes of at least half a
                                 // unit (WHEELSIEVE_WIDE_DOUBLE; c3s -1.9%; a third: no further gain)
