@@ -254,8 +254,9 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   // Buckets pay off only when most large primes are far above S (c4: up to
   // 120 S, c5: 16 S); up to a few S (c3: 3.8 S) the per-(prime, segment)
   // offset check in the kernel is cheaper than fill + apply + windowing.
-  const bool buckets = c->nprimes > p.n_mid && c->base_B > c->bucket_pmin &&
-                       c->base_B >= static_cast<uint64_t>(c->bucket_min_ratio) * c->S;
+  uint64_t pmin = c->bucket_pmin;
+  bool buckets = c->nprimes > p.n_mid && c->base_B > pmin &&
+                 c->base_B >= static_cast<uint64_t>(c->bucket_min_ratio) * c->S;
   // wide units (sieve_wide_kernel): single-job count launches without bucket
   // lists, long enough to keep every SM's lone CTA busy for many units
   const uint32_t wide_want = buckets ? c->wide_bucket : (nj > 1 ? c->wide_multi : c->wide);
@@ -270,6 +271,15 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
       p.n_dbl = p.n_S;
       p.n_S = std::min<uint32_t>(std::max(table_primes_below(c, (unit + 1) / 2), p.n_wc), p.n_dbl);
     }
+    // a unit pays the in-kernel visit of a large prime once per three segments,
+    // so bucketing starts higher: 6 S instead of 2 S (C4 47.4 -> 43.0 ms, C5
+    // 20.6 -> 19.4 ms; sweep over 2..16 S)
+    const uint64_t pmin_w = static_cast<uint64_t>(c->wide_pmin_ratio) * c->S;
+    if (buckets && pmin_w > pmin) {
+      pmin = pmin_w;
+      p.n_mid = std::min<uint32_t>(std::max(table_primes_below(c, pmin), p.n_wc), c->nprimes);
+      buckets = c->nprimes > p.n_mid && c->base_B > pmin;
+    }
     if (!buckets) p.n_mid = c->nprimes;
     p.miss_lane = 1;
     p.skip5_max = c->wide_skip5;
@@ -281,7 +291,8 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   uint64_t W = nseg;
   uint32_t cap = 0;
   if (buckets) {
-    const double E = expected_large_hits(c->bucket_pmin, c->S, static_cast<double>(c->base_B));
+    const double E = expected_large_hits(static_cast<uint32_t>(pmin), c->S,
+                                         static_cast<double>(c->base_B));
     cap = static_cast<uint32_t>(1.1 * E + 8.0 * std::sqrt(E) + 1024);
     cap = (cap + 31) / 32 * 32;
     if (c->cap_override) cap = c->cap_override;
@@ -1527,6 +1538,7 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_MISS_LANE")) c->miss_lane = std::atoi(e) != 0;
   if (const char* e = std::getenv("WHEELSIEVE_SKIP5")) c->skip5_max = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE")) c->wide = std::strtoul(e, nullptr, 10);
+  if (const char* e = std::getenv("WHEELSIEVE_WIDE_PMIN")) c->wide_pmin_ratio = std::max<uint32_t>(1, std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_BUCKET")) c->wide_bucket = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_MULTI")) c->wide_multi = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_SEG_TRANS")) c->seg_trans = std::atoi(e) != 0;

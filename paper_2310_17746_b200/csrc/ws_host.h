@@ -196,6 +196,7 @@ struct DevCtx {
   int bps[wsk::kNumModes] = {2, 2, 2, 2};  // resident blocks per SM per mode
   uint32_t wide = 3;            // > 1: long count launches sieve this many segments per unit (WHEELSIEVE_WIDE)
   uint32_t wide_bucket = 3;     // ... in bucket windows (WHEELSIEVE_WIDE_BUCKET; C4 -4.8%, C5 -7.4%)
+  uint32_t wide_pmin_ratio = 6; // ... where primes below this many S stay in the kernel (WHEELSIEVE_WIDE_PMIN)
   uint32_t wide_multi = 3;      // ... in launches over several jobs without buckets (WHEELSIEVE_WIDE_MULTI);
                                 // several jobs: only when they average at least 6 segments
   uint32_t trans_min = 768;     // wide units: shortest partial superblock marked transposed
