@@ -68,10 +68,13 @@ struct SieveParams {
   uint32_t nprimes;                  // host-side upper bound on the table size
   const uint32_t* nprimes_dev;       // nullable: exact table size, written on device
   uint32_t n_wc;                     // primes [0, n_wc) use the warp-cooperative loop
-  uint32_t n_S;                      // primes [n_wc, n_S) (p < S): one thread per prime, loop
+  uint32_t n_S;                      // primes [n_wc, n_S): one thread per prime, hit loop
+                                     // (p < S; wide units: p < half a unit)
   uint32_t n_dbl;                    // wide: [n_S, n_dbl) straight-line, <= 2 hits per class
-  uint32_t n_mid;                    // [n_S, n_mid): one thread per prime, <= 1 hit per class;
-                                     // [n_mid, nprimes) from buckets (directly if bucket == null)
+                                     // (half a unit <= p < a unit); 0 otherwise
+  uint32_t n_mid;                    // [max(n_S, n_dbl), n_mid): one thread per prime, <= 1 hit
+                                     // per class; [n_mid, nprimes) from buckets (directly if
+                                     // bucket == null or a list overflowed)
   const uint32_t* bucket;            // window lists: bucket[(s - s_begin) * bcap + i]
   uint32_t* bcount;                  // entries per window segment (reset after use)
   uint32_t bcap;
@@ -89,8 +92,8 @@ struct SieveParams {
   uint32_t miss_lane;                // single-hit misses OR 0 into word `lane` (else a word from h)
   uint32_t skip5_max;                // mid primes below it skip their hits on multiples of 5
   uint32_t wide;                     // > 1: sieve_wide_kernel, this many segments per unit
-  uint32_t seg_trans;                // per-segment kernel: transposed warp-cooperative marking
-  uint32_t trans_min;                // wide: shortest partial superblock marked transposed
+  uint32_t seg_trans;                // per-segment count kernels: transposed warp-cooperative marking
+  uint32_t trans_min;                // shortest partial superblock marked transposed (mark_transposed)
   const uint32_t* units;             // wide launches over windows or several jobs: per unit,
   uint32_t nunits;                   //   first window-local segment | segment count << 28
   uint32_t* words1;                  // nullable (count modes): survivor flag words of
