@@ -1546,6 +1546,8 @@ ws_status make_dev(int dev, uint32_t S, DevCtx** out) {
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_DOUBLE")) c->wide_double = std::strtoul(e, nullptr, 10);
   if (const char* e = std::getenv("WHEELSIEVE_TRANS_MIN")) c->trans_min = std::max<uint32_t>(32, std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_SKIP5")) c->wide_skip5 = std::strtoul(e, nullptr, 10);
+  // wide units mark primes below 1280 warp-cooperatively (1024 .. 1536 within 0.6%)
+  c->wide_n_wc = table_primes_below(c, 1280);
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_WC_LIMIT"))
     c->wide_n_wc = table_primes_below(c, std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("WHEELSIEVE_WIDE_MIN_UNITS"))
