@@ -398,7 +398,11 @@ void run_sieve(DevCtx* c, int mode, uint32_t* per_seg_dev, unsigned long long* o
   // primes of at least the run length take the carried-offset fill when every
   // run is a piece of the one job (consecutive in wheel slots)
   uint32_t huge_begin = c->nprimes;
-  const uint64_t huge_from = (c->huge_from ? c->huge_from : piece) * c->S;
+  // (the one-check kernels -- the default -- take primes of at least the run
+  // length only: a smaller WHEELSIEVE_HUGE_FROM needs WHEELSIEVE_HUGE_LOOP=1)
+  uint64_t huge_segs = c->huge_from ? c->huge_from : piece;
+  if (!c->huge_loop && c->huge_step == 1) huge_segs = std::max<uint64_t>(huge_segs, piece);
+  const uint64_t huge_from = huge_segs * c->S;
   if (buckets && c->fill_huge && nj == 1 && c->base_B >= huge_from)
     huge_begin = std::max(p.n_mid, table_primes_below(c, huge_from));
   // with the large-prime fill that heavy (half of a C4 window), two sieve CTAs
